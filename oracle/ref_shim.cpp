@@ -1,0 +1,348 @@
+// ref_shim.cpp -- extern "C" driver over the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile together with the
+// reference sources where they lie under /root/reference/proj/src (nothing is
+// copied into this repo) into oracle/_ref/libpythia_ref{16,64}.so.  The B=16
+// flavour sees a generated copy of hierarchy.hpp with kBlockTokens = 16
+// (written to oracle/_ref/overlay16/, git-ignored).
+//
+// Used by tests/ to pin the C restatement (oracle/pyg_oracle.c) against the
+// reference itself, by tests/golden/make_golden.py to emit golden vectors, and
+// by bench.py --impl reference as the reference CPU arm.
+//
+// Lineage ints are turned into the strings "w<k>" / "r<k>"; FutureRegistry
+// masks into sets of those role names.
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pythia/cache/hierarchy.hpp"
+#include "pythia/cache/manager.hpp"
+#include "pythia/sched/router.hpp"
+#include "pythia/workflow/path_analysis.hpp"
+#include "pythia/workflow/path_expr.hpp"
+
+using namespace pythia;
+using cache::CacheHierarchy;
+using cache::SharedL3;
+using cache::Tier;
+
+namespace {
+std::string wf_name(int32_t w) { return "w" + std::to_string(w); }
+std::string role_name(int32_t r) { return "r" + std::to_string(r); }
+int32_t parse_int(const std::string& s) { return s.size() > 1 ? std::stoi(s.substr(1)) : -1; }
+Tier to_tier(int32_t t) { return t == 0 ? Tier::L1 : (t == 1 ? Tier::L2 : Tier::L3); }
+std::set<std::string> mask_roles(uint64_t m) {
+  std::set<std::string> s;
+  for (int i = 0; i < 64; ++i)
+    if ((m >> i) & 1u) s.insert(role_name(i));
+  return s;
+}
+workflow::TokenSeq seq_of(const uint64_t* t, int64_t n) { return workflow::TokenSeq(t, t + n); }
+}  // namespace
+
+struct pref_block {
+  uint64_t id, hash;
+  int64_t s, e;
+  int32_t wf, role;
+  double la;
+  int32_t pin;
+  int32_t alive;
+};
+
+struct pref_res {
+  int64_t prompt_len, upper;
+  double alpha;
+  int64_t tokens_generated;
+};
+
+struct pref_decision {
+  int32_t target;
+  int32_t tiebreak;
+  int64_t headroom;
+  double oom_bound;
+};
+
+extern "C" {
+
+int64_t pref_block_tokens() { return cache::kBlockTokens; }
+
+uint64_t pref_fnv1a_str(const char* s, int64_t n) {
+  return workflow::fnv1a(std::string_view(s, static_cast<size_t>(n)));
+}
+uint64_t pref_fnv1a_u64(uint64_t v, uint64_t h) { return workflow::fnv1a(v, h); }
+uint64_t pref_response_token(const char* rid, int64_t index) {
+  return workflow::response_token(rid, static_cast<size_t>(index));
+}
+
+int64_t pref_chain_hashes(const uint64_t* tokens, int64_t n, uint64_t* out) {
+  auto h = cache::chain_boundary_hashes(seq_of(tokens, n));
+  if (out) std::memcpy(out, h.data(), h.size() * sizeof(uint64_t));
+  return static_cast<int64_t>(h.size());
+}
+
+// ---- CacheHierarchy / SharedL3 ----
+void* pref_cache_new(int64_t l1, int64_t l2) { return new CacheHierarchy(l1, l2); }
+void pref_cache_free(void* c) { delete static_cast<CacheHierarchy*>(c); }
+void* pref_cache_clone(void* c) { return new CacheHierarchy(*static_cast<CacheHierarchy*>(c)); }
+void* pref_l3_new() { return new SharedL3(); }
+void pref_l3_free(void* l) { delete static_cast<SharedL3*>(l); }
+void* pref_l3_clone(void* l) { return new SharedL3(*static_cast<SharedL3*>(l)); }
+
+static cache::TierStore& store_of(void* c, void* l3, int32_t tier) {
+  if (tier == 2 && l3) return static_cast<SharedL3*>(l3)->store();
+  return static_cast<CacheHierarchy*>(c)->tier(to_tier(tier));
+}
+
+void pref_lookup(void* c, void* l3, const uint64_t* tokens, int64_t n, int64_t out[3]) {
+  auto m = static_cast<CacheHierarchy*>(c)->lookup(seq_of(tokens, n),
+                                                    static_cast<SharedL3*>(l3));
+  out[0] = m.l1;
+  out[1] = m.l2;
+  out[2] = m.l3;
+}
+
+int64_t pref_matched_prefix(void* c, void* l3, int32_t tier, const uint64_t* tokens, int64_t n) {
+  auto seq = seq_of(tokens, n);
+  auto h = cache::chain_boundary_hashes(seq);
+  return store_of(c, l3, tier).matched_prefix(seq, h);
+}
+
+void pref_insert_chain(void* c, int32_t tier, const uint64_t* tokens, int64_t n, int64_t upto,
+                       int32_t wf, int32_t role, double now, int32_t pin) {
+  static_cast<CacheHierarchy*>(c)->insert_chain(to_tier(tier), seq_of(tokens, n), upto,
+                                                {wf_name(wf), role_name(role)}, now, pin);
+}
+
+void pref_unpin_chain(void* c, const uint64_t* tokens, int64_t n, int64_t upto) {
+  static_cast<CacheHierarchy*>(c)->unpin_chain(seq_of(tokens, n), upto);
+}
+
+uint64_t pref_tier_put(void* c, void* l3, int32_t tier, uint64_t hash, int64_t s, int64_t e,
+                       int32_t wf, int32_t role, double now, int32_t pin) {
+  uint64_t* ctr = (tier == 2 && l3) ? static_cast<SharedL3*>(l3)->id_counter()
+                                    : static_cast<CacheHierarchy*>(c)->id_counter();
+  return store_of(c, l3, tier).put(hash, s, e, {wf_name(wf), role_name(role)}, now, pin, ctr);
+}
+
+void pref_tier_erase(void* c, void* l3, int32_t tier, uint64_t id) {
+  store_of(c, l3, tier).erase(id);
+}
+
+int64_t pref_tier_occupancy(void* c, void* l3, int32_t tier) {
+  return store_of(c, l3, tier).occupancy();
+}
+
+int64_t pref_tier_dump(void* c, void* l3, int32_t tier, pref_block* out, int64_t cap) {
+  const auto& blocks = store_of(c, l3, tier).blocks();
+  int64_t k = 0;
+  for (const auto& [id, b] : blocks) {
+    if (out && k < cap) {
+      out[k] = {b.block_id, b.chain_hash, b.span_start, b.span_end,
+                parse_int(b.lineage.workflow_id), parse_int(b.lineage.role_id),
+                b.last_access, b.pin_count, 1};
+    }
+    ++k;
+  }
+  return k;
+}
+
+void pref_add_decode_tokens(void* c, int64_t n) {
+  static_cast<CacheHierarchy*>(c)->add_decode_tokens(n);
+}
+int64_t pref_l1_occupancy(void* c) { return static_cast<CacheHierarchy*>(c)->l1_occupancy(); }
+
+// ---- FutureRegistry ----
+void* pref_registry_new() { return new cache::FutureRegistry(); }
+void pref_registry_free(void* r) { delete static_cast<cache::FutureRegistry*>(r); }
+void pref_registry_update(void* r, int32_t wf, uint64_t mask) {
+  static_cast<cache::FutureRegistry*>(r)->update(wf_name(wf), mask_roles(mask));
+}
+void pref_registry_drop(void* r, int32_t wf) {
+  static_cast<cache::FutureRegistry*>(r)->drop(wf_name(wf));
+}
+
+// ---- evict_for_space ----
+int32_t pref_evict(void* c, int32_t tier, int64_t needed, void* reg, int32_t speculative,
+                   uint64_t* out_ids, int64_t cap, int64_t* n_freed, int64_t* freed_tokens) {
+  auto res = cache::evict_for_space(*static_cast<CacheHierarchy*>(c), to_tier(tier), needed,
+                                    *static_cast<cache::FutureRegistry*>(reg), speculative != 0);
+  int64_t k = 0;
+  for (uint64_t id : res.freed) {
+    if (out_ids && k < cap) out_ids[k] = id;
+    ++k;
+  }
+  *n_freed = k;
+  *freed_tokens = res.freed_tokens;
+  return res.satisfied ? 1 : 0;
+}
+
+// ---- router ----
+pref_decision pref_route(int32_t n_nodes, const int32_t* replica_id, const int64_t* kv_capacity,
+                         const int64_t* asg_off, const pref_res* asg, const int64_t* staged,
+                         const pref_res* req, double epsilon) {
+  std::vector<sched::NodeView> nodes(static_cast<size_t>(n_nodes));
+  for (int32_t n = 0; n < n_nodes; ++n) {
+    nodes[n].replica_id = replica_id[n];
+    nodes[n].kv_capacity = kv_capacity[n];
+    nodes[n].staged_l2_prefix = staged[n];
+    for (int64_t i = asg_off[n]; i < asg_off[n + 1]; ++i) {
+      nodes[n].assigned.push_back({asg[i].prompt_len, asg[i].upper, asg[i].alpha,
+                                   asg[i].tokens_generated});
+    }
+  }
+  sched::Reservation r{req->prompt_len, req->upper, req->alpha, req->tokens_generated};
+  auto d = sched::route(nodes, r, epsilon);
+  pref_decision out{};
+  out.target = d.target ? *d.target : -1;
+  out.tiebreak = d.cache_tiebreak_used ? 1 : 0;
+  out.headroom = d.headroom;
+  out.oom_bound = d.oom_bound;
+  return out;
+}
+
+int32_t pref_route_least_outstanding(int32_t n_nodes, const int32_t* replica_id,
+                                     const int64_t* asg_off) {
+  std::vector<sched::NodeView> nodes(static_cast<size_t>(n_nodes));
+  for (int32_t n = 0; n < n_nodes; ++n) {
+    nodes[n].replica_id = replica_id[n];
+    nodes[n].assigned.resize(static_cast<size_t>(asg_off[n + 1] - asg_off[n]));
+  }
+  auto t = sched::route_least_outstanding(nodes);
+  return t ? *t : -1;
+}
+
+// ---- path analysis (host-side workflow ingestion; used to derive future masks) ----
+// history is a list of role names separated by ','; returns -1 if the history
+// cannot be located.  Role names must be "r<k>" with k < 64.
+int64_t pref_future_mask(const char* expr, const char* history, uint64_t* mask_out) {
+  auto e = std::make_shared<const workflow::PathExpr>(workflow::parse_path_expr(expr));
+  std::vector<std::string> h;
+  std::string cur;
+  for (const char* p = history;; ++p) {
+    if (*p == ',' || *p == '\0') {
+      if (!cur.empty()) h.push_back(cur);
+      cur.clear();
+      if (*p == '\0') break;
+    } else {
+      cur.push_back(*p);
+    }
+  }
+  auto pos = workflow::locate_position(*e, h);
+  if (!pos) return -1;
+  uint64_t m = 0;
+  for (const auto& r : workflow::future_roles(*pos)) {
+    int32_t k = parse_int(r);
+    if (k >= 0 && k < 64) m |= uint64_t{1} << k;
+  }
+  *mask_out = m;
+  return 0;
+}
+
+// expected_distance_to (path_analysis.cpp:553-557); returns 0 and writes the
+// distance, 1 if nullopt, -1 if the history cannot be located.
+int64_t pref_expected_distance(const char* expr, const char* history, const char* role,
+                               double* out) {
+  auto e = std::make_shared<const workflow::PathExpr>(workflow::parse_path_expr(expr));
+  std::vector<std::string> h;
+  std::string cur;
+  for (const char* p = history;; ++p) {
+    if (*p == ',' || *p == '\0') {
+      if (!cur.empty()) h.push_back(cur);
+      cur.clear();
+      if (*p == '\0') break;
+    } else {
+      cur.push_back(*p);
+    }
+  }
+  auto pos = workflow::locate_position(*e, h);
+  if (!pos) return -1;
+  auto d = workflow::expected_distance_to(*pos, role);
+  if (!d) return 1;
+  *out = *d;
+  return 0;
+}
+
+// ---- completion (manager.cpp:25-58) with an explicit future mask ----
+// Builds the action list the way on_request_complete does, but from a mask
+// instead of a PathCursor, then runs the reference apply_completion.  The
+// cursor-driven variant is pref_complete_expr below.
+int64_t pref_complete_mask(void* c, void* l3, int32_t wf, uint64_t future_mask, double now) {
+  auto* cache = static_cast<CacheHierarchy*>(c);
+  std::set<std::string> future = mask_roles(future_mask);
+  std::vector<cache::CompletionAction> actions;
+  for (Tier t : {Tier::L1, Tier::L2}) {
+    for (const auto& [id, block] : cache->tier(t).blocks()) {
+      if (block.pinned()) continue;
+      if (block.lineage.workflow_id != wf_name(wf)) continue;
+      actions.push_back({future.count(block.lineage.role_id)
+                             ? cache::CompletionAction::Kind::RetainAndWriteL3
+                             : cache::CompletionAction::Kind::Free,
+                         t, id});
+    }
+  }
+  cache::apply_completion(actions, *cache, *static_cast<SharedL3*>(l3), now);
+  return static_cast<int64_t>(actions.size());
+}
+
+// Cursor-driven: the reference on_request_complete on a real envelope.
+int64_t pref_complete_expr(void* c, void* l3, int32_t wf, const char* expr, const char* history,
+                           double now) {
+  auto e = std::make_shared<const workflow::PathExpr>(workflow::parse_path_expr(expr));
+  std::vector<std::string> h;
+  std::string cur;
+  for (const char* p = history;; ++p) {
+    if (*p == ',' || *p == '\0') {
+      if (!cur.empty()) h.push_back(cur);
+      cur.clear();
+      if (*p == '\0') break;
+    } else {
+      cur.push_back(*p);
+    }
+  }
+  auto pos = workflow::locate_position(*e, h);
+  if (!pos) return -1;
+  workflow::RequestEnvelope env;
+  env.request_id = "req";
+  env.app_metadata = {"t", wf_name(wf), h.back()};
+  env.sys_annotations = workflow::SysAnnotations{};
+  env.sys_annotations->path_regex = e;
+  env.position = *pos;
+  auto* cache = static_cast<CacheHierarchy*>(c);
+  auto actions = cache::on_request_complete(env, *cache);
+  cache::apply_completion(actions, *cache, *static_cast<SharedL3*>(l3), now);
+  return static_cast<int64_t>(actions.size());
+}
+
+// L3 dead-lineage sweep of apply_completion_policy (engine.cpp:1074-1080).
+void pref_l3_dead_sweep(void* l3, int32_t wf, uint64_t future_mask) {
+  auto& store = static_cast<SharedL3*>(l3)->store();
+  std::set<std::string> future = mask_roles(future_mask);
+  std::vector<uint64_t> dead;
+  for (const auto& [id, block] : store.blocks()) {
+    if (block.lineage.workflow_id == wf_name(wf) && !future.count(block.lineage.role_id)) {
+      dead.push_back(id);
+    }
+  }
+  for (uint64_t id : dead) store.erase(id);
+}
+
+// erase_chain_span (engine.cpp:849-861 is a private static of the engine; this is the same
+// loop over the public TierStore API).
+void pref_erase_chain_span(void* c, void* l3, int32_t tier, const uint64_t* tokens, int64_t n,
+                           int64_t from, int64_t to) {
+  auto& store = store_of(c, l3, tier);
+  auto hashes = cache::chain_boundary_hashes(seq_of(tokens, n));
+  for (size_t i = 0; i < hashes.size(); ++i) {
+    int64_t span_end = std::min<int64_t>(static_cast<int64_t>(i + 1) * cache::kBlockTokens, n);
+    if (span_end <= from || span_end > to) continue;
+    if (const cache::CacheBlock* b = store.find_chain(hashes[i])) {
+      if (!b->pinned()) store.erase(b->block_id);
+    }
+  }
+}
+
+}  // extern "C"
