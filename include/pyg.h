@@ -1,0 +1,244 @@
+/*
+ * pyg.h -- C-ABI of the B200-native Pythia scheduling hot path.
+ *
+ * The reference (arXiv 2604.25899, /root/reference/proj) has no FFI: its
+ * engine calls the cache/scheduler classes directly.  Each
+ * entry point below replaces one reference call and names it.  A C++ engine
+ * keeps its interfaces by routing the class methods through these functions
+ * (INTEGRATION.md shows the adapter); nothing in the signatures is C++ or torch.
+ *
+ * Conventions
+ *   - Every call returns PYG_OK (0) or a negative PYG_E* code; the message is
+ *     in pyg_last_error() (thread-local).  No C++ exception crosses the ABI.
+ *   - Caller owns every host buffer; the library owns the device tables.
+ *   - One pyg_ctx per caller thread and GPU (the reference engine is single-
+ *     threaded).  Calls are stream-ordered on the ctx stream and,
+ *     unless the name ends in _dev, synchronous.
+ *   - Lineage strings (workflow_id, role_id) are interned by the caller to
+ *     dense ints; FutureRegistry role sets are 64-bit masks over role ids.
+ *   - Tier ids: 0 = L1, 1 = L2, 2 = L3.  CacheHierarchy-level calls keep the
+ *     reference quirk that tier(L3) aliases L2 (hierarchy.cpp:106-107);
+ *     TierStore-level calls (pyg_tier_*, pyg_matched_prefix) address the
+ *     shared L3 store with tier 2.
+ *   - _dev calls take device pointers and do not synchronize.
+ *   - There is no CPU fallback: every call runs CUDA kernels, and a missing or
+ *     failing device is an error (PYG_ECUDA).
+ */
+#ifndef PYG_H
+#define PYG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PYG_OK 0
+#define PYG_EINVAL (-1)
+#define PYG_ENOMEM (-2)
+#define PYG_ECUDA (-3)
+#define PYG_ECAPACITY (-4)
+#define PYG_ENOTSUP (-5)
+
+#define PYG_L1 0
+#define PYG_L2 1
+#define PYG_L3 2
+
+typedef struct pyg_ctx pyg_ctx;
+
+typedef struct {
+  int32_t block_tokens;        /* B, 1..64; reference: kBlockTokens (hierarchy.hpp:15) */
+  int32_t n_replicas;          /* CacheHierarchy instances on this GPU (engine.cpp:141-155) */
+  int32_t device;              /* CUDA device ordinal */
+  int32_t reserved;
+  const int64_t* l1_capacity;  /* [n_replicas] tokens, CacheHierarchy(l1, l2) (hierarchy.hpp:100) */
+  const int64_t* l2_capacity;  /* [n_replicas] */
+  int64_t min_blocks;          /* initial per-tier block capacity hint (tables grow) */
+} pyg_config;
+
+/* Mirrors CacheBlock (hierarchy.hpp:29-40) with interned lineage. 56 bytes. */
+typedef struct {
+  uint64_t block_id;
+  uint64_t chain_hash;
+  int64_t span_start, span_end;
+  int32_t workflow, role;
+  double last_access;
+  int32_t pin_count;
+  int32_t alive;
+} pyg_block;
+
+/* Mirrors sched::Reservation (router.hpp:15-22). */
+typedef struct {
+  int64_t prompt_len, upper;
+  double alpha;
+  int64_t tokens_generated;
+} pyg_reservation;
+
+/* Mirrors sched::RoutingDecision (router.hpp:31-36); target -1 == nullopt (wait). */
+typedef struct {
+  int32_t target;
+  int32_t tiebreak;
+  int64_t headroom;
+  double oom_bound;
+} pyg_decision;
+
+/* ---------------------------------------------------------------- context */
+int pyg_create(const pyg_config* cfg, pyg_ctx** out);
+void pyg_destroy(pyg_ctx* ctx);
+const char* pyg_last_error(void);
+/* Launch on an external stream (cudaStream_t); NULL restores the ctx's own stream. */
+int pyg_set_stream(pyg_ctx* ctx, void* cuda_stream);
+int pyg_synchronize(pyg_ctx* ctx);
+/* number of kernels this ctx has launched (for the bench's gpu_launches claim) */
+int64_t pyg_kernel_launches(pyg_ctx* ctx);
+
+/* ------------------------------------------------------------- hashing */
+/* chain_boundary_hashes (hierarchy.cpp:21-30).  out holds ceil(n/B) hashes. */
+int pyg_chain_hashes(pyg_ctx* ctx, const uint64_t* tokens, int64_t n, uint64_t* out,
+                     int64_t* n_out);
+
+/* ------------------------------------------------- TierStore (per tier) */
+/* TierStore::put (hierarchy.cpp:44-66); id counter = replica's for L1/L2, L3's for L3. */
+int pyg_tier_put(pyg_ctx* ctx, int32_t replica, int32_t tier, uint64_t chain_hash,
+                 int64_t span_start, int64_t span_end, int32_t workflow, int32_t role, double now,
+                 int32_t pin_delta, uint64_t* out_id);
+/* TierStore::erase (hierarchy.cpp:68-82) */
+int pyg_tier_erase(pyg_ctx* ctx, int32_t replica, int32_t tier, uint64_t block_id);
+/* TierStore::find_chain (hierarchy.cpp:32-42) */
+int pyg_tier_find(pyg_ctx* ctx, int32_t replica, int32_t tier, uint64_t chain_hash,
+                  pyg_block* out, int32_t* found);
+/* TierStore::occupancy/capacity/blocks().size() (hierarchy.hpp:50-52) */
+int pyg_tier_stats(pyg_ctx* ctx, int32_t replica, int32_t tier, int64_t* occupancy,
+                   int64_t* capacity, int64_t* n_blocks);
+/* TierStore::blocks() in id order (hierarchy.hpp:52); returns the count in *n (may exceed cap) */
+int pyg_tier_dump(pyg_ctx* ctx, int32_t replica, int32_t tier, pyg_block* out, int64_t cap,
+                  int64_t* n);
+/* TierStore::matched_prefix (hierarchy.cpp:84-104) */
+int pyg_matched_prefix(pyg_ctx* ctx, int32_t replica, int32_t tier, const uint64_t* tokens,
+                       int64_t n, int64_t* out);
+
+/* -------------------------------------------------------- CacheHierarchy */
+/* CacheHierarchy::lookup (hierarchy.cpp:109-117); with_l3 = 0 passes nullptr */
+int pyg_lookup(pyg_ctx* ctx, int32_t replica, const uint64_t* tokens, int64_t n,
+               int32_t with_l3, int64_t out[3]);
+/* CacheHierarchy::insert_chain (hierarchy.cpp:119-130) */
+int pyg_insert_chain(pyg_ctx* ctx, int32_t replica, int32_t tier, const uint64_t* tokens,
+                     int64_t n, int64_t upto, int32_t workflow, int32_t role, double now,
+                     int32_t pin_delta);
+/* CacheHierarchy::unpin_chain (hierarchy.cpp:132-142) */
+int pyg_unpin_chain(pyg_ctx* ctx, int32_t replica, const uint64_t* tokens, int64_t n,
+                    int64_t upto);
+/* CacheHierarchy::add_decode_tokens / l1_occupancy (hierarchy.hpp:111-114) */
+int pyg_add_decode_tokens(pyg_ctx* ctx, int32_t replica, int64_t n);
+int pyg_l1_occupancy(pyg_ctx* ctx, int32_t replica, int64_t* out);
+/* Engine::erase_chain_span (engine.cpp:849-861); tier is TierStore-level (2 = shared L3) */
+int pyg_erase_chain_span(pyg_ctx* ctx, int32_t replica, int32_t tier, const uint64_t* tokens,
+                         int64_t n, int64_t from, int64_t to);
+/* replica status Off (engine.cpp:145; the completion sweep skips it, engine.cpp:1069) */
+int pyg_set_replica_off(pyg_ctx* ctx, int32_t replica, int32_t off);
+
+/* ------------------------------------------------------- cache manager */
+/* FutureRegistry::update / drop (manager.cpp:13-17) */
+int pyg_registry_update(pyg_ctx* ctx, int32_t workflow, uint64_t role_mask);
+int pyg_registry_drop(pyg_ctx* ctx, int32_t workflow);
+/* evict_for_space (manager.cpp:102-138).  freed ids in eviction order (up to cap); *n_freed is
+   the full count. */
+int pyg_evict_for_space(pyg_ctx* ctx, int32_t replica, int32_t tier, int64_t needed,
+                        int32_t speculative, uint64_t* freed, int64_t cap, int64_t* n_freed,
+                        int64_t* freed_tokens, int32_t* satisfied);
+/* on_request_complete + apply_completion on one replica (manager.cpp:25-58).  future_mask =
+   future_roles(position) (path_analysis.cpp:547-551, evaluated on the host); profiled = 0 for
+   an unprofiled request (no actions). */
+int pyg_complete(pyg_ctx* ctx, int32_t replica, int32_t workflow, uint64_t future_mask,
+                 int32_t profiled, double now, int64_t* n_actions);
+/* L3 dead-lineage erase of apply_completion_policy (engine.cpp:1074-1080) */
+int pyg_l3_dead_sweep(pyg_ctx* ctx, int32_t workflow, uint64_t future_mask);
+/* the whole apply_completion_policy (engine.cpp:1063-1080): registry update, sweep of every
+   non-Off replica, then the L3 dead sweep */
+int pyg_completion_policy(pyg_ctx* ctx, int32_t workflow, uint64_t future_mask, double now);
+
+/* ----------------------------------------------------------------- router */
+/* sched::route (router.cpp:19-50) for one request; nodes as arrays, assigned reservations as a
+   CSR (asg_off[n_nodes+1]); staged[n] = NodeView::staged_l2_prefix. */
+int pyg_route(pyg_ctx* ctx, int32_t n_nodes, const int32_t* replica_id,
+              const int64_t* kv_capacity, const int64_t* asg_off, const pyg_reservation* asg,
+              const int64_t* staged, const pyg_reservation* req, double epsilon,
+              pyg_decision* out);
+/* sched::route_least_outstanding (router.cpp:52-62) */
+int pyg_route_least_outstanding(pyg_ctx* ctx, int32_t n_nodes, const int32_t* replica_id,
+                                const int64_t* asg_off, int32_t* out);
+
+/* ============================================================ batched path */
+/* A batch of R requests, device resident.  tokens CSR: tok_off[R+1]; boundary hashes CSR:
+   hash_off[R+1] with hash_off[r+1]-hash_off[r] = ceil(len_r / B) (pyg_hash_offsets_dev). */
+
+/* hash_off from tok_off (exclusive scan of ceil(len/B)); also returns the total on the host
+   if total != NULL (one sync). */
+int pyg_hash_offsets_dev(pyg_ctx* ctx, const int64_t* d_tok_off, int32_t n_req,
+                         int64_t* d_hash_off, int64_t* total);
+/* K1: chain_boundary_hashes for every request of the batch. */
+int pyg_hash_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                       int32_t n_req, const int64_t* d_hash_off, uint64_t* d_hashes);
+
+/* K2: staged matrix.  For request r and its j-th candidate replica cand[cand_off[g_r]+j]
+   (g_r = d_group[r]), d_staged[r*max_cand + j] = tier(L2).matched_prefix(prompt_r)
+   == lookup(prompt, nullptr).l2 as node_view computes it (engine.cpp:646). */
+int pyg_staged_matrix_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                          const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t n_req,
+                          const int32_t* d_group, const int32_t* d_cand_off,
+                          const int32_t* d_cand, int32_t max_cand, int32_t* d_staged);
+
+/* K2: lookup (l1,l2,l3 matches) of request r against replica d_replica[r] (-1 = skip). */
+int pyg_lookup_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                         const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t n_req,
+                         const int32_t* d_replica, int32_t with_l3, int64_t* d_match3);
+
+/* Node table for batched routing: one node per replica of this ctx, in replica order.
+   assigned reservations as a CSR over replicas (device). */
+typedef struct {
+  const int32_t* replica_id;      /* [n_rep] NodeView::replica_id */
+  const int64_t* kv_capacity;     /* [n_rep] */
+  const int64_t* asg_off;         /* [n_rep+1] */
+  const pyg_reservation* asg;     /* assigned reservations, pool then active (engine.cpp:644-645) */
+} pyg_nodes_dev;
+
+#define PYG_ROUTE_SNAPSHOT 0
+#define PYG_ROUTE_SEQ_COMMIT 1
+
+/* K3: route every request of the batch.  Candidate groups: group g's candidates are
+   cand[cand_off[g] .. cand_off[g+1]) (replica indices of this ctx, ascending id order =
+   ready_replicas, engine.cpp:630-638).  SNAPSHOT: each request sees the same node state
+   (bit-exact to sched::route per request).  SEQ_COMMIT: requests are routed in order and each
+   placement is appended to its node before the next request (engine.cpp:683-688).
+   d_placed_off/d_placed (optional, SEQ_COMMIT): per-replica lists of placed request indices
+   in placement order, CSR [n_rep+1] and [n_req]. */
+int pyg_route_batch_dev(pyg_ctx* ctx, int32_t mode, const pyg_nodes_dev* nodes,
+                        const pyg_reservation* d_req, int32_t n_req, const int32_t* d_group,
+                        int32_t n_groups, const int32_t* d_cand_off, const int32_t* d_cand,
+                        int32_t max_cand, const int32_t* d_staged, double epsilon,
+                        pyg_decision* d_out, int32_t* d_placed_off, int32_t* d_placed);
+
+/* K4+K5: admission of placed requests (cache side of start_prefill, engine.cpp:799-829), one
+   CTA per replica in placement order: lookup(seq,&l3) -> evict_for_space(L1, len-l1) ->
+   erase promoted L2 span -> insert_chain(L1, pin+1).  L3 lookups see the L3 state at the start
+   of the call; promoted L3 spans are erased after all admissions (replica order).
+   d_admitted[r] = 1 admitted, 0 blocked; d_match3[3r..] = lookup. */
+int pyg_admit_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                        const int64_t* d_hash_off, const uint64_t* d_hashes,
+                        const int32_t* d_wf, const int32_t* d_role, int32_t n_req,
+                        const int32_t* d_placed_off, const int32_t* d_placed, double now,
+                        int32_t speculative, int32_t* d_admitted, int64_t* d_match3);
+
+/* K5: release admitted requests: unpin_chain(seq, len) on the target replica for every r with
+   d_admitted[r] != 0 (hierarchy.cpp:132-142). */
+int pyg_release_batch_dev(pyg_ctx* ctx, const int64_t* d_tok_off, const int64_t* d_hash_off,
+                          const uint64_t* d_hashes, int32_t n_req, const int32_t* d_placed_off,
+                          const int32_t* d_placed, const int32_t* d_admitted);
+
+/* device error flag set by batched kernels (capacity overflow etc.); reads and clears it */
+int pyg_check_device_error(pyg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

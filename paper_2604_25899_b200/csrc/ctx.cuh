@@ -1,0 +1,58 @@
+// ctx.cuh -- host-side context shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/pyg.h"
+#include "common.cuh"
+
+struct TierHost {
+  pyg::TierDev d;   // host mirror of the static fields (pointers, caps)
+  int64_t bound;    // upper bound of the device log_len
+  void* mem;        // one allocation: log | idx | ridx | scratch
+};
+
+struct pyg_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int32_t B = 16;
+  int32_t n_rep = 0;
+  std::vector<TierHost> tiers;  // 2*n_rep + 1
+  pyg::CtxDev hd{};             // host copy of the device-pointer bundle
+  pyg::TierDev* d_tiers = nullptr;
+  // scratch (device), grown on demand
+  void* d_scratch = nullptr;
+  size_t d_scratch_size = 0;
+  // completion lists
+  void* d_list = nullptr;
+  size_t d_list_size = 0;
+  int64_t launches = 0;
+};
+
+namespace pyg_host {
+void set_error(const std::string& msg);
+int cuda_check(cudaError_t e, const char* what);
+int tier_index(pyg_ctx* c, int32_t replica, int32_t tier, bool hierarchy_level, int* out);
+int ensure_capacity(pyg_ctx* c, int ti, int64_t k_new);
+int read_tier(pyg_ctx* c, int ti, pyg::TierDev* out);
+int scratch(pyg_ctx* c, size_t bytes, void** out);
+inline void count_launch(pyg_ctx* c, int n = 1) { c->launches += n; }
+}  // namespace pyg_host
+
+#define PYG_CUDA(call)                                                  \
+  do {                                                                  \
+    int _rc = pyg_host::cuda_check((call), #call);                      \
+    if (_rc != PYG_OK) return _rc;                                      \
+  } while (0)
+
+#define PYG_LAUNCHED(c)                                                 \
+  do {                                                                  \
+    pyg_host::count_launch(c);                                          \
+    int _rc = pyg_host::cuda_check(cudaGetLastError(), "kernel launch"); \
+    if (_rc != PYG_OK) return _rc;                                      \
+  } while (0)

@@ -1,0 +1,504 @@
+// device_ops.cuh -- warp/CTA-level building blocks of the hot path:
+// ordered block puts (K5), compaction, eviction select (K4), prefix match (K2)
+// and route evaluation (K3).  Each cites the reference function it restates.
+#pragma once
+
+#include "common.cuh"
+
+namespace pyg {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// --------------------------------------------------------------- block scan
+// Exclusive scan of one int64 per thread over the CTA; returns the prefix and
+// writes the total to *total (all threads).  smem: >= 33 int64.
+__device__ __forceinline__ int64_t block_exscan(int64_t v, int64_t* sm, int64_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t s = lane < nw ? sm[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(kFull, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) sm[lane] = s;  // inclusive per-warp totals
+    if (lane == 31) sm[32] = s;
+  }
+  __syncthreads();
+  const int64_t wp = w ? sm[w - 1] : 0;
+  *total = sm[32];
+  __syncthreads();
+  return wp + x - v;
+}
+
+// ------------------------------------------------------------ ordered puts
+// One item of an ordered put list (TierStore::put semantics per item).
+struct PutItem {
+  uint64_t hash, parent;
+  int64_t s, e;
+  int32_t wf, role;
+  int32_t orphan;
+};
+
+// Applies TierStore::put (hierarchy.cpp:44-66) for items 0..n-1 IN ORDER,
+// 32 at a time on one warp.  Equal hashes inside a chunk are grouped with
+// __match_any_sync so the first occurrence inserts (taking the next id) and
+// the later ones touch it, exactly as the sequential loop does.  New ids are
+// counter + rank among new items (ids follow item order).  Must be called by
+// all 32 lanes of one warp; the caller owns the tier (no concurrent mutation).
+// Returns (to lane 0) the id of the last item (for single puts).
+template <class Get>
+__device__ uint64_t warp_put_ordered(const CtxDev& c, TierDev* tp, int64_t n, Get get, double now,
+                                     int32_t pin_delta) {
+  const int lane = threadIdx.x & 31;
+  const TierDev t = *tp;
+  uint64_t* ctr = &c.counters[t.counter];
+  int64_t log_len = t.log_len;
+  uint64_t next_id = *ctr;
+  int64_t occ_add = 0, nnew_total = 0;
+  uint64_t last_id = 0;
+  for (int64_t base = 0; base < n; base += 32) {
+    const int64_t i = base + lane;
+    const bool active = i < n;
+    PutItem it{};
+    if (active) it = get(i);
+    const unsigned am = __ballot_sync(kFull, active);
+    unsigned grp = __match_any_sync(kFull, it.hash) & am;
+    const bool leader = active && (__ffs(grp) - 1) == lane;
+    const int cnt = __popc(grp);
+    int64_t li = -1;
+    if (leader) li = idx_find(t, it.hash);
+    const bool isnew = leader && li < 0;
+    const unsigned nm = __ballot_sync(kFull, isnew);
+    const int rank = __popc(nm & lanemask_lt());
+    int64_t sz = 0;
+    uint64_t my_id = 0;
+    if (isnew) {
+      const int64_t pos = log_len + rank;
+      Block b;
+      b.id = next_id + rank;
+      b.hash = it.hash;
+      b.parent = it.parent;
+      b.s = it.s;
+      b.e = it.e;
+      b.la = now;
+      b.wf = it.wf;
+      b.role = it.role;
+      b.pin = (pin_delta > 0 ? pin_delta : 0) + (cnt - 1) * pin_delta;
+      b.flags = kAlive | (it.orphan ? kOrphan : 0);
+      t.log[pos] = b;
+      idx_insert(t, it.hash, pos);
+      sz = b.e - b.s;
+      my_id = b.id;
+    } else if (leader) {
+      Block& b = t.log[li];
+      b.la = now;
+      b.pin += cnt * pin_delta;
+      my_id = b.id;
+    }
+    // the id seen by each item (followers take their leader's)
+    const int src = active ? __ffs(grp) - 1 : lane;
+    my_id = __shfl_sync(kFull, my_id, src);
+    // ragged-index notes for new blocks, serialized (several may share a parent)
+    unsigned rm = __ballot_sync(kFull, isnew && (it.s % c.B == 0) && (it.e % c.B != 0));
+    while (rm) {
+      const int l = __ffs(rm) - 1;
+      if (lane == l) {
+        Block b;
+        b.s = it.s;
+        b.e = it.e;
+        b.parent = it.parent;
+        b.flags = it.orphan ? kOrphan : 0;
+        ridx_note(t, b, c.B);
+        if (it.orphan && (it.e - it.s) >= 64) atomicAdd(reinterpret_cast<unsigned long long*>(&tp->n_long_orphans), 1ULL);
+      }
+      __syncwarp();
+      rm &= rm - 1;
+    }
+    const int nnew = __popc(nm);
+    occ_add += warp_sum(sz);
+    log_len += nnew;
+    next_id += nnew;
+    nnew_total += nnew;
+    const int lastl = __popc(am) - 1;
+    last_id = __shfl_sync(kFull, my_id, lastl < 0 ? 0 : lastl);
+    __syncwarp();
+  }
+  __syncwarp();
+  if (lane == 0) {
+    tp->log_len = log_len;
+    tp->n_alive += nnew_total;
+    tp->occupancy += occ_add;
+    tp->idx_used += nnew_total;
+    *ctr = next_id;
+  }
+  __syncwarp();
+  return last_id;
+}
+
+// ------------------------------------------------------------- compaction
+// In-place stable compaction of a tier's log (drops dead records, keeps id
+// order) and rebuild of idx / ridx.  Whole CTA; smem >= 33 int64.
+__device__ inline void block_compact(const CtxDev& c, TierDev* tp, int64_t* sm) {
+  const TierDev t = *tp;
+  const int64_t n = t.log_len;
+  int64_t write = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool alive = i < n && (t.log[i].flags & kAlive);
+    Block b;
+    if (alive) b = t.log[i];
+    __syncthreads();
+    int64_t tot;
+    const int64_t pos = write + block_exscan(alive ? 1 : 0, sm, &tot);
+    if (alive) t.log[pos] = b;
+    write += tot;
+    __syncthreads();
+  }
+  const uint64_t nslots = t.idx_mask + 1;
+  for (uint64_t i = threadIdx.x; i < nslots; i += blockDim.x) {
+    t.idx[i] = Slot{0, 0};
+    t.ridx[i] = RSlot{0, 0};
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < write; i += blockDim.x) idx_insert(t, t.log[i].hash, i);
+  __syncthreads();
+  // ragged index: warp 0, chunks of 32, equal keys grouped
+  int64_t long_orphans = 0;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int64_t base = 0; base < write; base += 32) {
+      const int64_t i = base + lane;
+      bool el = false;
+      uint64_t key = 0, bits = 0;
+      if (i < write) {
+        const Block& b = t.log[i];
+        if (b.s % c.B == 0 && b.e % c.B != 0 && b.e > b.s) {
+          const int64_t len = b.e - b.s;
+          if (b.flags & kOrphan) {
+            if (len < 64) {
+              el = true;
+              key = orphan_key(b.s);
+              bits = 1ULL << len;
+            } else {
+              long_orphans++;
+            }
+          } else {
+            el = true;
+            key = b.parent;
+            bits = 1ULL << len;
+          }
+        }
+      }
+      const unsigned em = __ballot_sync(kFull, el);
+      unsigned grp = __match_any_sync(kFull, key) & em;
+      // OR the bits of the group into the leader
+      uint64_t acc = 0;
+      for (int l = 0; l < 32; ++l) {
+        const uint64_t v = __shfl_sync(kFull, bits, l);
+        if ((grp >> l) & 1u) acc |= v;
+      }
+      if (el && (__ffs(grp) - 1) == lane) ridx_add(t, key, acc);
+      __syncwarp();
+    }
+    long_orphans = warp_sum(long_orphans);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tp->log_len = write;
+    tp->n_alive = write;
+    tp->idx_used = write;
+    tp->n_long_orphans = long_orphans;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ prefix match
+// Aligned walk of TierStore::matched_prefix (hierarchy.cpp:84-91), one warp:
+// probes 32 boundary hashes at a time and stops at the first miss.
+// Returns the number of leading blocks present (all lanes).
+__device__ __forceinline__ int64_t warp_walk(const TierDev& t, const uint64_t* hashes, int64_t nh) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = 0; base < nh; base += 32) {
+    const int64_t i = base + lane;
+    const bool miss = i < nh && idx_find(t, hashes[i]) < 0;
+    const unsigned mm = __ballot_sync(kFull, miss);
+    if (mm) return base + __ffs(mm) - 1;
+  }
+  return nh;
+}
+
+// Same walk by one thread (staged-matrix / admission path).
+__device__ __forceinline__ int64_t thread_walk(const TierDev& t, const uint64_t* hashes,
+                                               int64_t nh) {
+  int64_t k = 0;
+  while (k < nh && idx_find(t, hashes[k]) >= 0) ++k;
+  return k;
+}
+
+// Ragged check of TierStore::matched_prefix (hierarchy.cpp:92-103), one
+// thread.  The reference scans every block starting at `matched` and re-hashes
+// tokens[0, span_end) for each; here the candidates are the span lengths noted
+// under the query's own prefix hash (ridx), and each candidate is verified by
+// one idx probe of the running hash plus a span check.  Identical result up to
+// 64-bit hash collisions (the reference itself treats equal chain hashes as
+// equal prefixes, hierarchy.hpp:26-28).
+__device__ inline int64_t ragged_extend(const TierDev& t, const Block* log, const uint64_t* tokens,
+                                 int64_t L, const uint64_t* hashes, int64_t matched, int B) {
+  if (matched >= L || matched % B != 0) return matched;
+  const uint64_t parent = matched == 0 ? kFnvOffset : hashes[matched / B - 1];
+  uint64_t mask = ridx_get(t, parent) | ridx_get(t, orphan_key(matched));
+  mask &= ~1ULL;
+  int64_t best = matched;
+  if (mask) {
+    uint64_t h = parent;
+    const int64_t lim = L - matched < 63 ? L - matched : 63;
+    for (int64_t o = 1; o <= lim; ++o) {
+      h = fnv_token(h, tokens[matched + o - 1]);
+      if ((mask >> o) & 1ULL) {
+        const int64_t e = matched + o;
+        if (e % B != 0) {
+          const int64_t li = idx_find(t, h);
+          if (li >= 0 && log[li].s == matched && log[li].e == e) best = e;
+        }
+      }
+      if ((mask >> o) <= 1ULL) break;  // no higher candidate
+    }
+  }
+  if (t.n_long_orphans > 0) {
+    // orphan blocks (direct TierStore::put) longer than 63 tokens: literal scan
+    for (int64_t k = 0; k < t.log_len; ++k) {
+      const Block& b = log[k];
+      if (!(b.flags & kAlive) || !(b.flags & kOrphan) || b.s != matched) continue;
+      if (b.e > L || b.e % B == 0 || b.e - b.s < 64 || b.e <= best) continue;
+      uint64_t h = parent;
+      for (int64_t x = matched; x < b.e; ++x) h = fnv_token(h, tokens[x]);
+      if (h == b.hash) best = b.e;
+    }
+  }
+  return best;
+}
+
+__device__ __forceinline__ int64_t matched_from_blocks(int64_t k, int64_t L, int B) {
+  const int64_t m = k * B;
+  return m < L ? m : L;
+}
+
+// ---------------------------------------------------------------- eviction
+// Sort key of evict_for_space (manager.cpp:125-129): dead lineage first, then
+// last_access ascending, then block_id ascending.  The log is in id order, so
+// the log index stands in for the id.  hi = order(last_access); lo = class<<31
+// | log index (class 0 = dead).
+__device__ __forceinline__ bool key_less(uint64_t ah, uint32_t al, uint64_t bh, uint32_t bl) {
+  const uint32_t ac = al >> 31, bc = bl >> 31;
+  if (ac != bc) return ac < bc;
+  if (ah != bh) return ah < bh;
+  return (al & 0x7fffffffu) < (bl & 0x7fffffffu);
+}
+
+__device__ inline void block_bitonic(uint64_t* hi, uint32_t* lo, int64_t n) {
+  for (int64_t k = 2; k <= n; k <<= 1) {
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int64_t ixj = i ^ j;
+        if (ixj > i) {
+          const bool asc = (i & k) == 0;
+          const uint64_t h1 = hi[i], h2 = hi[ixj];
+          const uint32_t l1 = lo[i], l2 = lo[ixj];
+          const bool gt = key_less(h2, l2, h1, l1);
+          if (gt == asc) {
+            hi[i] = h2;
+            hi[ixj] = h1;
+            lo[i] = l2;
+            lo[ixj] = l1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+constexpr int64_t kSmemSortCap = 8192;  // 96 KB of keys
+
+struct EvictOut {
+  int64_t n_freed;
+  int64_t freed_tokens;
+  int32_t satisfied;
+};
+
+// evict_for_space (manager.cpp:102-138) on one tier, whole CTA.
+// excess = base + needed - capacity must be computed by the caller (base =
+// l1_occupancy for L1).  Candidates = alive unpinned blocks (pin <= 0);
+// sorted by the reference key; the shortest prefix with sum(size) >= excess
+// is erased (all candidates if that is unsatisfiable).  freed ids are written
+// in eviction order to out_ids[0..cap).  smem_keys: kSmemSortCap*12 bytes or
+// nullptr (then the tier scratch is used); sm: >= 33 int64.
+__device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t excess, int speculative,
+                                uint64_t* out_ids, int64_t cap, unsigned char* smem_keys,
+                                int64_t* sm) {
+  EvictOut r{0, 0, 1};
+  if (excess <= 0) return r;
+  const TierDev t = *tp;
+  const int64_t n = t.log_len;
+  // count candidates
+  int64_t mine = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const Block& b = t.log[i];
+    mine += ((b.flags & kAlive) && b.pin <= 0) ? 1 : 0;
+  }
+  int64_t ncand;
+  block_exscan(mine, sm, &ncand);
+  int64_t np2 = 1;
+  while (np2 < ncand) np2 <<= 1;
+  uint64_t* khi;
+  uint32_t* klo;
+  if (smem_keys && np2 <= kSmemSortCap) {
+    khi = reinterpret_cast<uint64_t*>(smem_keys);
+    klo = reinterpret_cast<uint32_t*>(smem_keys + kSmemSortCap * 8);
+  } else {
+    khi = t.scratch;
+    klo = reinterpret_cast<uint32_t*>(t.scratch + 2 * t.log_cap);
+  }
+  // gather (chunked stable compaction into the key buffer)
+  int64_t write = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool cand = false;
+    uint64_t h = 0;
+    uint32_t l = 0;
+    if (i < n) {
+      const Block& b = t.log[i];
+      cand = (b.flags & kAlive) && b.pin <= 0;
+      if (cand) {
+        bool dead = false;
+        if (speculative) {
+          const bool live = b.wf >= 0 && b.wf < c.reg_cap && c.reg_present[b.wf] &&
+                            b.role >= 0 && b.role < 64 && ((c.reg_mask[b.wf] >> b.role) & 1ULL);
+          dead = !live;  // FutureRegistry::lineage_live (manager.cpp:19-23)
+        }
+        h = order_double(b.la);
+        l = (dead ? 0u : 0x80000000u) | static_cast<uint32_t>(i);
+      }
+    }
+    int64_t tot;
+    const int64_t pos = write + block_exscan(cand ? 1 : 0, sm, &tot);
+    if (cand) {
+      khi[pos] = h;
+      klo[pos] = l;
+    }
+    write += tot;
+  }
+  for (int64_t i = ncand + threadIdx.x; i < np2; i += blockDim.x) {
+    khi[i] = ~0ULL;
+    klo[i] = 0xffffffffu;
+  }
+  __syncthreads();
+  block_bitonic(khi, klo, np2);
+  // shortest sorted prefix with cumulative size >= excess
+  int64_t cum = 0, cut = ncand;  // cut = number of victims
+  for (int64_t base = 0; base < ncand; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    int64_t sz = 0;
+    if (i < ncand) {
+      const Block& b = t.log[klo[i] & 0x7fffffffu];
+      sz = b.e - b.s;
+    }
+    int64_t tot;
+    const int64_t before = cum + block_exscan(sz, sm, &tot);
+    // victim i is taken iff the running total before it is < excess
+    const bool stop_here = i < ncand && before < excess && before + sz >= excess;
+    if (stop_here) sm[40] = i + 1;
+    __syncthreads();
+    const bool found = (cum + tot) >= excess;
+    if (found) {
+      cut = sm[40];
+      __syncthreads();
+      break;
+    }
+    cum += tot;
+    __syncthreads();
+  }
+  // erase victims, emit ids
+  int64_t freed = 0;
+  for (int64_t i = threadIdx.x; i < cut; i += blockDim.x) {
+    const int64_t li = klo[i] & 0x7fffffffu;
+    if (out_ids && i < cap) out_ids[i] = t.log[li].id;
+    freed += erase_at(t, li);
+  }
+  int64_t ftot;
+  block_exscan(freed, sm, &ftot);
+  if (threadIdx.x == 0) {
+    tp->occupancy -= ftot;
+    tp->n_alive -= cut;
+  }
+  __syncthreads();
+  r.n_freed = cut;
+  r.freed_tokens = ftot;
+  r.satisfied = ftot >= excess;
+  return r;
+}
+
+// ----------------------------------------------------------------- routing
+// Per-node evaluation of sched::route (router.cpp:19-50): capacity_holds
+// (router.cpp:7-11) + oom_bound ordered sum (router.cpp:13-17).
+struct NodeEval {
+  bool feasible;
+  int64_t headroom;
+  double bound;
+};
+
+__device__ __forceinline__ int64_t res_tokens(const int64_t p, const int64_t u, const int64_t g) {
+  return p + (u > g ? u : g);  // Reservation::tokens (router.hpp:21)
+}
+
+// Lexicographic route reduction state.  W = argmax (headroom, staged, -id, -pos)
+// (the reference's running update is a strict lexicographic max on
+// (headroom, staged, -replica_id) taken in input order);
+// tiebreak = first position with headroom H < first position with
+// (headroom, staged) == (H, S): that is exactly when the last non-id-tie update
+// of the reference loop was a staged tie-win (router.cpp:35-39).
+struct RouteAcc {
+  int64_t h;
+  int64_t s;
+  int32_t id;
+  int32_t pos;  // -1 = none
+};
+
+__device__ __forceinline__ bool acc_better(const RouteAcc& a, const RouteAcc& b) {
+  if (a.pos < 0) return false;
+  if (b.pos < 0) return true;
+  if (a.h != b.h) return a.h > b.h;
+  if (a.s != b.s) return a.s > b.s;
+  if (a.id != b.id) return a.id < b.id;
+  return a.pos < b.pos;
+}
+
+__device__ __forceinline__ RouteAcc warp_best(RouteAcc a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    RouteAcc b;
+    b.h = __shfl_xor_sync(kFull, a.h, o);
+    b.s = __shfl_xor_sync(kFull, a.s, o);
+    b.id = __shfl_xor_sync(kFull, a.id, o);
+    b.pos = __shfl_xor_sync(kFull, a.pos, o);
+    if (acc_better(b, a)) a = b;
+  }
+  return a;
+}
+
+__device__ __forceinline__ int32_t warp_min_i32(int32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+}  // namespace pyg
