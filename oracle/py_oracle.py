@@ -105,6 +105,7 @@ class Restated(_Backend):
         s("o_route_least_outstanding", i32, i32, vp, vp)
         s("o_erase_chain_span", None, vp, vp, i64, i64, i64, i64)
         s("o_completion_policy", None, vp, i32, vp, vp, i32, u64, dbl)
+        s("o_admit", C.c_int, vp, vp, vp, vp, C.c_int, vp, i64, i32, i32, dbl, i64, vp)
 
     # -- hashing
     def fnv1a_u64(self, v, h=1469598103934665603):
@@ -218,6 +219,14 @@ class Restated(_Backend):
         self.lib.o_on_request_complete(c, wf, future_mask, int(profiled), _p(acts), n)
         self.lib.o_apply_completion(_p(acts), n, c, l3, now)
         return n
+
+    def admit(self, c, l3_lookup, l3_live, reg, speculative, seq, wf, role, now):
+        """cache side of start_prefill (engine.cpp:799-829); returns (admitted, (l1,l2,l3))"""
+        t = _u64(seq)
+        m = np.zeros(3, np.int64)
+        ok = self.lib.o_admit(c, l3_lookup, l3_live, reg, int(speculative), _p(t), len(t), wf,
+                              role, now, self.B, _p(m))
+        return bool(ok), tuple(int(x) for x in m)
 
     def l3_dead_sweep(self, l3, wf, mask):
         # apply_completion_policy's L3 pass (engine.cpp:1074-1080) via the policy helper with
@@ -400,6 +409,24 @@ class Reference(_Backend):
     def complete_expr(self, c, l3, wf, expr, history, now):
         return self.lib.pref_complete_expr(c, l3, wf, expr.encode(), ",".join(history).encode(),
                                            now)
+
+    def admit(self, c, l3_lookup, l3_live, reg, speculative, seq, wf, role, now):
+        """start_prefill cache side (engine.cpp:799-829) composed from reference calls."""
+        m = self.lookup(c, l3_lookup, seq)
+        L = len(seq)
+        ok, _, _ = self.evict_ids(c, 0, L - m[0], reg, speculative, cap=1)
+        if not ok:
+            return False, m
+        reusable = max(m)
+        l2_part = max(min(reusable, m[1]) - m[0], 0)
+        l12 = max(m[0], m[1])
+        l3_part = max(reusable - l12, 0)
+        if l2_part > 0:
+            self.erase_chain_span(c, None, 1, seq, m[0], m[0] + l2_part)
+        if l3_part > 0:
+            self.erase_chain_span(c, l3_live, 2, seq, l12, reusable)
+        self.insert_chain(c, 0, seq, L, wf, role, now, +1)
+        return True, m
 
     def future_mask(self, expr, history):
         m = C.c_uint64()

@@ -1,0 +1,105 @@
+"""GPU parity of the batched step (K1 hash, K2 staged matrix, K3 route in both
+modes, K4/K5 admission + release) against the oracle composition in
+tests/batch_oracle.py, over several consecutive steps on an evolving cluster."""
+import numpy as np
+import pytest
+import torch
+
+from batch_oracle import (SEQ_COMMIT, SNAPSHOT, apply_warm_gpu, apply_warm_oracle, oracle_step,
+                          warm_ops)
+from oracle.py_oracle import Restated
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(trace, cl, B, seed):
+    from paper_2604_25899_b200 import Context
+    o = Restated(B)
+    caches = [o.new_cache(int(cl.kv_capacity[n]), int(cl.l2_capacity[n]))
+              for n in range(cl.n_replicas)]
+    l3, reg = o.new_l3(), o.new_registry()
+    ctx = Context(cl.n_replicas, cl.kv_capacity, cl.l2_capacity, B)
+    ops = warm_ops(trace, cl, seed)
+    apply_warm_oracle(o, caches, l3, reg, trace, ops)
+    apply_warm_gpu(ctx, trace, ops)
+    return o, caches, l3, reg, ctx
+
+
+def _compare_state(o, caches, l3, ctx, cl):
+    for n in range(cl.n_replicas):
+        for tier in (0, 1):
+            g = ctx.dump(n, tier)
+            w = o.dump(caches[n], None, tier)
+            assert g.tobytes() == w.tobytes(), f"replica {n} tier {tier} differs"
+    assert ctx.dump(0, 2).tobytes() == o.dump(caches[0], l3, 2).tobytes(), "L3 differs"
+
+
+def _run(trace, cl, B, mode, steps, seed=0, spec=True):
+    from paper_2604_25899_b200 import batch as PB
+    o, caches, l3, reg, ctx = _setup(trace, cl, B, seed)
+    db = PB.upload_batch(ctx, trace.tokens_np(), trace.tok_off, trace.res, trace.group, trace.wf,
+                         trace.role)
+    dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand)
+    out = PB.alloc_out(ctx, db, dn)
+    total_placed = 0
+    for s in range(steps):
+        now = 10.0 + s
+        PB.step(ctx, db, dn, out, now, mode=mode, speculative=spec, release=True)
+        torch.cuda.synchronize()
+        ctx.check_device_error()
+        got = out.host()
+        want = oracle_step(o, caches, l3, reg, trace, cl, mode, 0.05, now, spec, True)
+        # hashes
+        hs = db.hashes.cpu().numpy().view(np.uint64)
+        for r in range(0, trace.R, max(1, trace.R // 50)):
+            hw = o.chain_hashes(trace.prompt(r))
+            a = int(db.hash_off[r].item())
+            assert np.array_equal(hs[a:a + len(hw)], hw)
+        assert np.array_equal(got["staged"][:trace.R], want["staged"])
+        d = got["decisions"][:trace.R]
+        for r in range(trace.R):
+            wt = want["decisions"][r]
+            assert (int(d["target"][r]), int(d["tiebreak"][r]), int(d["headroom"][r])) == wt[:3], r
+            assert d["oom_bound"][r].tobytes() == np.float64(wt[3]).tobytes(), r
+        po = got["placed_off"]
+        for n in range(cl.n_replicas):
+            assert got["placed"][po[n]:po[n + 1]].tolist() == want["placed"][n]
+        assert np.array_equal(got["admitted"][:trace.R], want["admitted"])
+        assert np.array_equal(got["match3"][:trace.R], want["match3"])
+        _compare_state(o, caches, l3, ctx, cl)
+        total_placed += int(sum(len(p) for p in want["placed"]))
+    return total_placed
+
+
+@pytest.mark.parametrize("B", [16, 64])
+def test_batch_seq_commit_deep_research(B):
+    from paper_2604_25899_b200 import workload as W
+    tr = W.deep_research(n_workflows=24, seed=5, device="cpu")
+    cl = W.make_cluster(8, 2, kv=24_000, l2=30_000, seed=1)
+    placed = _run(tr, cl, B, SEQ_COMMIT, steps=3)
+    assert placed > 10  # admissions and evictions were exercised
+
+
+def test_batch_snapshot_small():
+    from paper_2604_25899_b200 import workload as W
+    tr = W.deep_research(n_workflows=4, seed=7, device="cpu")
+    cl = W.make_cluster(6, 2, kv=400_000, l2=30_000, seed=2)
+    _run(tr, cl, 16, SNAPSHOT, steps=2)
+
+
+def test_batch_mixed_alphas_and_lru_only():
+    from paper_2604_25899_b200 import workload as W
+    tr = W.deep_research(n_workflows=16, seed=9, device="cpu")
+    rng = np.random.default_rng(0)
+    k = rng.random(tr.R)
+    tr.res["alpha"] = np.where(k < 0.2, 0.02, np.where(k < 0.3, 0.0, tr.res["alpha"]))
+    tr.res["alpha"][np.nonzero(k > 0.95)[0]] = -0.0
+    cl = W.make_cluster(8, 2, kv=20_000, l2=20_000, seed=3)
+    _run(tr, cl, 16, SEQ_COMMIT, steps=2, spec=False)
+
+
+def test_batch_coding_assistant_chat_accumulate():
+    from paper_2604_25899_b200 import workload as W
+    tr = W.coding_assistant(n_workflows=12, seed=2, device="cpu")
+    cl = W.make_cluster(4, 1, kv=40_000, l2=40_000, seed=4)
+    _run(tr, cl, 16, SEQ_COMMIT, steps=3)
