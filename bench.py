@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Routed requests/sec of the B200 scheduling hot path (BASELINE.json metric).
+
+One *step* = one burst of R requests of the config-2 trace (deep-research DAG,
+10k workflows, 6 roles, 2 models x 16 replicas, 16-token blocks) routed
+through the whole hot path on device:
+  K1 chain hashing -> K2 staged-L2 matrix (every request x candidate replica)
+  -> K3 sequential-commit routing (engine order) -> K4/K5 admission of placed
+  requests (lookup with L3, evict_for_space, promoted-span erase, insert_chain
+  pinned) -> K5 release (unpin).
+Inputs are resident in HBM for `value`; `e2e` runs the same step through the
+host-buffer C-ABI entry pyg_step_host (pinned host arrays copied in and results
+copied out every step).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU (torchrun, one rank per GPU): weak scaling -- each rank owns its own
+cluster shard (its models' replicas) and its own burst; no data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "routed requests/sec (prefix-match+evict+route) at 1/2/4/8 B200; % HBM peak"
+UNIT = "requests/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workflows", type=int, default=10_000)
+    ap.add_argument("--replicas", type=int, default=32)
+    ap.add_argument("--block", type=int, default=16)
+    ap.add_argument("--kv", type=int, default=100_000)
+    ap.add_argument("--l2", type=int, default=200_000)
+    ap.add_argument("--mode", default="seq", choices=["seq", "snapshot"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.out = []
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = []
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        busy = [x for x in sm if x > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ workload
+def build_workload(args, rank, device):
+    from paper_2604_25899_b200 import workload as W
+    tr = W.deep_research(n_workflows=args.workflows, seed=1 + rank, device=device)
+    cl = W.make_cluster(args.replicas, 2, kv=args.kv, l2=args.l2, seed=rank,
+                        id_base=rank * args.replicas)
+    return tr, cl
+
+
+def warm_l2(ctx, tr, cl, rng, frac=0.01):
+    """Stage a sample of prompts' prefixes into replicas' L2 (what forward staging does,
+    manager.cpp:60-100), so the staged matrix has real hits and tie-breaks."""
+    n = max(1, int(tr.R * frac))
+    for r in rng.choice(tr.R, n, replace=False):
+        g = int(tr.group[r])
+        cands = cl.cand[cl.cand_off[g]:cl.cand_off[g + 1]]
+        rep = int(rng.choice(cands))
+        p = tr.prompt(int(r))
+        ctx.insert_chain(rep, 1, p, int(len(p) * rng.uniform(0.3, 1.0)), int(tr.wf[r]),
+                         int(tr.role[r]), 0.5, 0)
+    for w in range(0, int(tr.wf.max()) + 1):
+        ctx.registry_update(w, 0x3E)  # every workflow still expects roles 1..5
+
+
+def algorithmic_bytes(tr, B, staged, max_cand, cl, placed, match3):
+    """SURVEY.md 8(d) per-step byte count of the hot path."""
+    L = np.diff(tr.tok_off)
+    nb = (L + B - 1) // B
+    hash_bytes = 8 * int(L.sum()) + 8 * int(nb.sum()) + 16 * (tr.R + 1)
+    ncand = np.diff(cl.cand_off)[tr.group]
+    st = staged[:tr.R]
+    mask = np.arange(max_cand)[None, :] < ncand[:, None]
+    probes = int(((st + B - 1) // B + 1)[mask].sum())
+    staged_bytes = 32 * probes + 4 * int(mask.sum())
+    route_bytes = 32 * tr.R + 24 * tr.R
+    adm = placed
+    l1 = match3[:tr.R, 0]
+    admit_bytes = 0
+    if adm.size:
+        admit_bytes = int(sum(32 * (3 * (nb[r] // 4 + 1)) + 64 * nb[r] for r in adm))
+    return {"hash": hash_bytes, "staged": staged_bytes, "route": route_bytes,
+            "admit": admit_bytes, "total": hash_bytes + staged_bytes + route_bytes + admit_bytes,
+            "probes": probes}
+
+
+# --------------------------------------------------------------- CPU baseline
+def _cpu_worker(payload):
+    """Reference engine composition (oracle/_ref, unmodified sources) on one core."""
+    wf_count, seed, seconds, replicas, kv, l2, B, rank_base = payload
+    import torch  # noqa: F401
+    from oracle.py_oracle import Reference
+    from oracle.step import apply_warm_oracle, warm_ops
+    from paper_2604_25899_b200 import workload as W
+    ref = Reference(B)
+    tr = W.deep_research(n_workflows=wf_count, seed=seed, device="cpu")
+    cl = W.make_cluster(replicas, 2, kv=kv, l2=l2, seed=seed, id_base=rank_base)
+    caches = [ref.new_cache(int(cl.kv_capacity[n]), int(cl.l2_capacity[n])) for n in range(replicas)]
+    l3, reg = ref.new_l3(), ref.new_registry()
+    apply_warm_oracle(ref, caches, l3, reg, tr, warm_ops(tr, cl, seed, n_chains=4))
+    toks = tr.tokens_np()
+    done, t0 = 0, time.perf_counter()
+    chunk = 64
+    step = 0
+    while time.perf_counter() - t0 < seconds:
+        a = (done % tr.R)
+        b = min(a + chunk, tr.R)
+        idx = np.arange(a, b)
+        sub = tr.subset(idx)
+        ref.step(caches, l3, reg, True, sub.tokens_np(), sub.tok_off, sub.res, sub.group, sub.wf,
+                 sub.role, cl, 1, 0.05, 1.0 + step, True, want_out=False)
+        done += b - a
+        step += 1
+    el = time.perf_counter() - t0
+    return done, el, float(np.diff(tr.tok_off).mean())
+
+
+def cpu_baseline(args, cores, seconds):
+    from oracle.py_oracle import reference_available
+    if not reference_available(args.block):
+        return None
+    wf = max(40, min(args.workflows, 400))
+    payloads = [(wf, 100 + i, seconds, args.replicas, args.kv, args.l2, args.block, 0)
+                for i in range(cores)]
+    if cores == 1:
+        res = [_cpu_worker(payloads[0])]
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(cores) as pool:
+            res = pool.map(_cpu_worker, payloads)
+    rate = sum(d / e for d, e, _ in res)
+    n = sum(d for d, _, _ in res)
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": (f"{n} config-2 requests (mean prompt {res[0][2]:.0f} tokens) routed through "
+                       f"the unmodified reference (oracle/_ref/libpythia_ref{args.block}.so, "
+                       f"pref_step: per-candidate lookup, route, admit, release) on "
+                       f"{args.replicas} replicas, {cores} process(es) x {seconds:.0f}s")}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    if args.profile:
+        cores = 1
+    t_budget = max(5.0, min(args.cpu_seconds, 20.0))
+    t0 = time.perf_counter()
+    bl = cpu_baseline(args, cores, t_budget)
+    if bl is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    el = time.perf_counter() - t0
+    line = {"impl": "reference", "metric": METRIC, "value": bl["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * el / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "config-2 deep_research burst (bounded CPU sample)",
+                       "replicas": args.replicas, "block_tokens": args.block,
+                       "route_mode": "seq_commit"},
+            "cpu_baseline": bl,
+            "e2e": {"value": bl["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2604_25899_b200 import Context
+    from paper_2604_25899_b200 import batch as PB
+
+    tr, cl = build_workload(args, rank, dev)
+    ctx = Context(cl.n_replicas, cl.kv_capacity, cl.l2_capacity, args.block, device=local)
+    PB.bind_current_stream(ctx)
+    rng = np.random.default_rng(rank)
+    warm_l2(ctx, tr, cl, rng)
+    db = PB.DeviceBatch(tr.R, tr.tokens, torch.from_numpy(tr.tok_off).to(dev), None, None,
+                        torch.from_numpy(tr.res.view(np.int64).reshape(tr.R, 4).copy()).to(dev),
+                        torch.from_numpy(tr.group).to(dev), torch.from_numpy(tr.wf).to(dev),
+                        torch.from_numpy(tr.role).to(dev), 0, tr.n_tokens)
+    nb = (np.diff(tr.tok_off) + args.block - 1) // args.block
+    hoff = np.zeros(tr.R + 1, np.int64)
+    np.cumsum(nb, out=hoff[1:])
+    db.hash_off = torch.from_numpy(hoff).to(dev)
+    db.hashes = torch.empty(int(hoff[-1]), dtype=torch.int64, device=dev)
+    db.n_hashes = int(hoff[-1])
+    dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand,
+                         device=dev)
+    out = PB.alloc_out(ctx, db, dn, device=dev)
+    mode = PB.SEQ_COMMIT if args.mode == "seq" else PB.SNAPSHOT
+    now = [1.0]
+
+    phases = ["hash", "staged", "route", "admit", "release"]
+
+    def one_step(evs=None):
+        fns = [lambda: PB.hash_batch(ctx, db), lambda: PB.staged_matrix(ctx, db, dn, out),
+               lambda: PB.route_batch(ctx, db, dn, out, mode),
+               lambda: PB.admit_batch(ctx, db, out, now[0], True),
+               lambda: PB.release_batch(ctx, db, out)]
+        for i, f in enumerate(fns):
+            if evs is not None:
+                evs[i].record()
+            f()
+        if evs is not None:
+            evs[len(fns)].record()
+        now[0] += 1.0
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    ctx.check_device_error()
+
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = ctx.kernel_launches()
+    ev_all = [[torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)]
+              for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for s in range(args.steps):
+        one_step(ev_all[s])
+    t_end.record()
+    torch.cuda.synchronize()
+    launches = ctx.kernel_launches() - launches0
+    clk = clocks.stop()
+    ctx.check_device_error()
+    ms = t_start.elapsed_time(t_end)
+    phase_ms = {p: sum(e[i].elapsed_time(e[i + 1]) for e in ev_all) / args.steps
+                for i, p in enumerate(phases)}
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    total_req = tr.R * ws * args.steps
+    value = total_req / (ms / 1000.0)
+
+    h = out.host()
+    placed = h["placed"][:h["placed_off"][-1]]
+    n_placed = int(len(placed))
+    n_admitted = int(h["admitted"][:tr.R].sum())
+    ab = algorithmic_bytes(tr, args.block, h["staged"], dn.max_cand, cl, placed, h["match3"])
+    peak, peak_src = peaks()
+    hash_gbs = ab["hash"] / (phase_ms["hash"] / 1000.0) / 1e9
+    step_gbs = ab["total"] / (ms_step / 1000.0) / 1e9
+
+    # e2e through the host-buffer C-ABI
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        hs = PB.HostStep(ctx, tr.tokens_np(), tr.tok_off, tr.res, tr.group, tr.wf, tr.role, cl)
+        for _ in range(2):
+            hs(now[0], mode)
+            now[0] += 1.0
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e2e_steps = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            hs(now[0], mode)
+            now[0] += 1.0
+        e_ms = (time.perf_counter() - t0) * 1000.0
+        if ws > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": tr.R * ws * e2e_steps / (e_ms / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": hs.h2d_bytes, "d2h_bytes_per_step": hs.d2h_bytes,
+               "ms_per_step": e_ms / e2e_steps, "via": "pyg_step_host (pinned host buffers)"}
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "hash_kernel_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
+        cpu = cpu_baseline(args, 1, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {
+                "workload": (f"config-2 deep_research burst: {args.workflows} workflows = "
+                             f"{tr.R} requests/step/GPU, 6 roles, 2 models x {args.replicas // 2} "
+                             f"replicas, B={args.block}, kv={args.kv}, l2={args.l2}"),
+                "route_mode": "seq_commit" if mode == PB.SEQ_COMMIT else "snapshot",
+                "requests_per_step_per_gpu": tr.R, "tokens_per_step_per_gpu": tr.n_tokens,
+                "placed_per_step": n_placed, "admitted_per_step": n_admitted,
+                "l2_flush": "none needed: step inputs (tokens %.2f GB) exceed the 126 MB L2"
+                            % (tr.n_tokens * 8 / 1e9),
+                "parallelism": f"replica shards x{ws} (weak)"},
+            "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1)", "achieved": hash_gbs,
+                         "peak": peak, "unit": "GB/s", "frac": hash_gbs / peak,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": ab["hash"],
+                         "avg_launch_ms": phase_ms["hash"]},
+            "step_roofline": {"achieved": step_gbs, "frac": step_gbs / peak,
+                              "algorithmic_bytes_per_step": ab["total"], "probes": ab["probes"]},
+            "phase_ms": phase_ms,
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

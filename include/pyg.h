@@ -86,7 +86,8 @@ typedef struct {
 int pyg_create(const pyg_config* cfg, pyg_ctx** out);
 void pyg_destroy(pyg_ctx* ctx);
 const char* pyg_last_error(void);
-/* Launch on an external stream (cudaStream_t); NULL restores the ctx's own stream. */
+/* Launch on an external stream (cudaStream_t); NULL is the default stream.  Until this is
+   called the ctx uses its own non-blocking stream. */
 int pyg_set_stream(pyg_ctx* ctx, void* cuda_stream);
 int pyg_synchronize(pyg_ctx* ctx);
 /* number of kernels this ctx has launched (for the bench's gpu_launches claim) */
@@ -234,6 +235,36 @@ int pyg_admit_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d
 int pyg_release_batch_dev(pyg_ctx* ctx, const int64_t* d_tok_off, const int64_t* d_hash_off,
                           const uint64_t* d_hashes, int32_t n_req, const int32_t* d_placed_off,
                           const int32_t* d_placed, const int32_t* d_admitted);
+
+/* ------------------------------------------------- host-buffer batch entry */
+/* The drop-in batch call for a C++ engine: host arrays in, host arrays out.  Copies the batch
+   to the device (pinned host memory is fastest), runs K1..K5 exactly as the _dev sequence
+   hash -> staged -> route -> admit [-> release] does, copies the results back, synchronizes. */
+typedef struct {
+  int32_t n_req;
+  int32_t reserved;
+  const uint64_t* tokens;       /* CSR by tok_off */
+  const int64_t* tok_off;       /* [n_req+1] */
+  const pyg_reservation* req;   /* [n_req] */
+  const int32_t* group;         /* [n_req] candidate group (model) */
+  const int32_t* workflow;      /* [n_req] interned lineage */
+  const int32_t* role;          /* [n_req] */
+} pyg_batch_host;
+
+typedef struct {
+  const int32_t* replica_id;    /* [n_rep] */
+  const int64_t* kv_capacity;   /* [n_rep] */
+  const int64_t* asg_off;       /* [n_rep+1] */
+  const pyg_reservation* asg;
+  int32_t n_groups;
+  int32_t reserved;
+  const int32_t* cand_off;      /* [n_groups+1] */
+  const int32_t* cand;
+} pyg_nodes_host;
+
+int pyg_step_host(pyg_ctx* ctx, const pyg_batch_host* batch, const pyg_nodes_host* nodes,
+                  int32_t mode, double epsilon, double now, int32_t speculative, int32_t release,
+                  pyg_decision* out_decisions, int32_t* out_admitted, int64_t* out_match3);
 
 /* device error flag set by batched kernels (capacity overflow etc.); reads and clears it */
 int pyg_check_device_error(pyg_ctx* ctx);

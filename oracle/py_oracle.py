@@ -307,6 +307,8 @@ class Reference(_Backend):
         s("pref_complete_expr", i64, vp, vp, i32, C.c_char_p, C.c_char_p, dbl)
         s("pref_l3_dead_sweep", None, vp, i32, u64)
         s("pref_erase_chain_span", None, vp, vp, i32, vp, i64, i64, i64)
+        s("pref_step", i64, vp, i32, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+          vp, i32, dbl, dbl, i32, vp, vp)
 
     def fnv1a_u64(self, v, h=1469598103934665603):
         return self.lib.pref_fnv1a_u64(v, h)
@@ -427,6 +429,32 @@ class Reference(_Backend):
             self.erase_chain_span(c, l3_live, 2, seq, l12, reusable)
         self.insert_chain(c, 0, seq, L, wf, role, now, +1)
         return True, m
+
+    def step(self, caches, l3, reg, speculative, tokens, tok_off, res, group, wf, role, cl, mode,
+             eps, now, release, want_out=True):
+        """pref_step: one burst through the reference engine's call pattern (C++)."""
+        R = len(tok_off) - 1
+        arr = (C.c_void_p * len(caches))(*caches)
+        t = _u64(tokens)
+        off = np.ascontiguousarray(tok_off, np.int64)
+        rs = np.ascontiguousarray(res, RES_DTYPE)
+        g = np.ascontiguousarray(group, np.int32)
+        w = np.ascontiguousarray(wf, np.int32)
+        ro = np.ascontiguousarray(role, np.int32)
+        a = np.ascontiguousarray(cl.asg, RES_DTYPE) if len(cl.asg) else np.zeros(1, RES_DTYPE)
+        rid = np.ascontiguousarray(cl.replica_id, np.int32)
+        kv = np.ascontiguousarray(cl.kv_capacity, np.int64)
+        ao = np.ascontiguousarray(cl.asg_off, np.int64)
+        co = np.ascontiguousarray(cl.cand_off, np.int32)
+        cd = np.ascontiguousarray(cl.cand, np.int32)
+        dec = np.zeros(max(R, 1), np.dtype([("target", "<i4"), ("tiebreak", "<i4"),
+                                            ("headroom", "<i8"), ("oom_bound", "<f8")]))
+        adm = np.zeros(max(R, 1), np.int32)
+        n = self.lib.pref_step(C.cast(arr, C.c_void_p), len(caches), l3, reg, int(speculative),
+                               _p(t), _p(off), R, _p(rs), _p(g), _p(w), _p(ro), _p(rid), _p(kv),
+                               _p(ao), _p(a), _p(co), _p(cd), mode, eps, now, int(release),
+                               _p(dec) if want_out else None, _p(adm) if want_out else None)
+        return n, dec[:R], adm[:R]
 
     def future_mask(self, expr, history):
         m = C.c_uint64()

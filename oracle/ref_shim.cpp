@@ -345,4 +345,90 @@ void pref_erase_chain_span(void* c, void* l3, int32_t tier, const uint64_t* toke
   }
 }
 
+// One burst of R requests through the reference engine's hot-path call
+// pattern (the CPU baseline of bench.py; same contract as pyg_step_host):
+//   node_view per candidate: staged = cache.lookup(prompt, nullptr).l2   engine.cpp:640-648
+//   sched::route in issue order; SEQ_COMMIT pushes to the pool first     engine.cpp:650-692
+//   per replica, per placed request: start_prefill cache side            engine.cpp:799-829
+//     (L3 lookups against the L3 as of the start of admission)
+//   release: unpin_chain(seq, len)                                        hierarchy.cpp:132-142
+// Returns the number of placed requests.
+int64_t pref_step(void** caches, int32_t n_rep, void* l3v, void* regv, int32_t spec,
+                  const uint64_t* tokens, const int64_t* tok_off, int32_t R, const pref_res* res,
+                  const int32_t* group, const int32_t* wf, const int32_t* role,
+                  const int32_t* replica_id, const int64_t* kv_cap, const int64_t* asg_off,
+                  const pref_res* asg, const int32_t* cand_off, const int32_t* cand, int32_t mode,
+                  double eps, double now, int32_t release, pref_decision* out_dec,
+                  int32_t* out_adm) {
+  auto* l3 = static_cast<SharedL3*>(l3v);
+  auto* reg = static_cast<cache::FutureRegistry*>(regv);
+  std::vector<std::vector<sched::Reservation>> pools(static_cast<size_t>(n_rep));
+  for (int n = 0; n < n_rep; ++n)
+    for (int64_t k = asg_off[n]; k < asg_off[n + 1]; ++k)
+      pools[n].push_back({asg[k].prompt_len, asg[k].upper, asg[k].alpha, asg[k].tokens_generated});
+  std::vector<std::vector<int32_t>> placed(static_cast<size_t>(n_rep));
+  int64_t n_placed = 0;
+  for (int32_t r = 0; r < R; ++r) {
+    workflow::TokenSeq prompt(tokens + tok_off[r], tokens + tok_off[r + 1]);
+    const int g = group[r];
+    std::vector<sched::NodeView> views;
+    for (int32_t j = cand_off[g]; j < cand_off[g + 1]; ++j) {
+      const int n = cand[j];
+      sched::NodeView v;
+      v.replica_id = replica_id[n];
+      v.kv_capacity = kv_cap[n];
+      v.assigned = pools[n];
+      v.staged_l2_prefix = static_cast<CacheHierarchy*>(caches[n])->lookup(prompt, nullptr).l2;
+      views.push_back(std::move(v));
+    }
+    sched::Reservation q{res[r].prompt_len, res[r].upper, res[r].alpha, res[r].tokens_generated};
+    auto d = sched::route(views, q, eps);
+    pref_decision od{};
+    od.target = d.target ? *d.target : -1;
+    od.tiebreak = d.cache_tiebreak_used;
+    od.headroom = d.headroom;
+    od.oom_bound = d.oom_bound;
+    if (out_dec) out_dec[r] = od;
+    if (out_adm) out_adm[r] = 0;
+    if (d.target) {
+      for (int32_t j = cand_off[g]; j < cand_off[g + 1]; ++j) {
+        if (replica_id[cand[j]] == *d.target) {
+          if (mode == 1) pools[cand[j]].push_back(q);
+          placed[cand[j]].push_back(r);
+          ++n_placed;
+          break;
+        }
+      }
+    }
+  }
+  SharedL3 l3snap = *l3;
+  std::vector<std::pair<int, int32_t>> admitted;
+  for (int n = 0; n < n_rep; ++n) {
+    auto* c = static_cast<CacheHierarchy*>(caches[n]);
+    for (int32_t r : placed[n]) {
+      workflow::TokenSeq seq(tokens + tok_off[r], tokens + tok_off[r + 1]);
+      const int64_t len = static_cast<int64_t>(seq.size());
+      auto m = c->lookup(seq, &l3snap);
+      auto ev = cache::evict_for_space(*c, Tier::L1, len - m.l1, *reg, spec != 0);
+      if (!ev.satisfied) continue;
+      const int64_t reusable = std::max({m.l1, m.l2, m.l3});
+      const int64_t l2_part = std::max<int64_t>(std::min(reusable, m.l2) - m.l1, 0);
+      const int64_t l3_part = std::max<int64_t>(reusable - std::max(m.l1, m.l2), 0);
+      if (l2_part > 0) pref_erase_chain_span(c, nullptr, 1, seq.data(), len, m.l1, m.l1 + l2_part);
+      if (l3_part > 0)
+        pref_erase_chain_span(c, l3, 2, seq.data(), len, std::max(m.l1, m.l2), reusable);
+      c->insert_chain(Tier::L1, seq, len, {wf_name(wf[r]), role_name(role[r])}, now, +1);
+      if (out_adm) out_adm[r] = 1;
+      admitted.emplace_back(n, r);
+    }
+  }
+  if (release) {  // after every admission, as pyg_release_batch_dev
+    for (auto [n, r] : admitted) {
+      workflow::TokenSeq seq(tokens + tok_off[r], tokens + tok_off[r + 1]);
+      static_cast<CacheHierarchy*>(caches[n])->unpin_chain(seq, static_cast<int64_t>(seq.size()));
+    }
+  }
+  return n_placed;
+}
+
 }  // extern "C"

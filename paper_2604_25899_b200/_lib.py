@@ -109,6 +109,21 @@ _sig("pyg_route_batch_dev", vp, i32, C.POINTER(NodesDev), vp, i32, vp, i32, vp, 
 _sig("pyg_admit_batch_dev", vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, dbl, i32, vp, vp)
 _sig("pyg_release_batch_dev", vp, vp, vp, vp, i32, vp, vp, vp)
 
+
+
+class BatchHost(C.Structure):
+    _fields_ = [("n_req", i32), ("reserved", i32), ("tokens", vp), ("tok_off", vp), ("req", vp),
+                ("group", vp), ("workflow", vp), ("role", vp)]
+
+
+class NodesHost(C.Structure):
+    _fields_ = [("replica_id", vp), ("kv_capacity", vp), ("asg_off", vp), ("asg", vp),
+                ("n_groups", i32), ("reserved", i32), ("cand_off", vp), ("cand", vp)]
+
+
+_sig("pyg_step_host", vp, C.POINTER(BatchHost), C.POINTER(NodesHost), i32, dbl, dbl, i32, i32,
+     vp, vp, vp)
+
 EXPORTED = [n for n in dir(_lib) if n.startswith("pyg_")]
 
 

@@ -194,3 +194,62 @@ def step(ctx, b: DeviceBatch, nodes: DeviceNodes, out: StepOut, now: float, mode
     if release:
         release_batch(ctx, b, out)
     return out
+
+
+class HostStep:
+    """The host-buffer batch entry (pyg_step_host): pinned host arrays in/out, every step
+    copies the batch to the device, runs K1..K5 and copies the results back."""
+
+    def __init__(self, ctx, tokens: np.ndarray, tok_off, res, group, wf, role, cluster,
+                 pinned=True):
+        def pin(a, dtype):
+            a = np.ascontiguousarray(a, dtype)
+            if not pinned or a.size == 0:
+                return a
+            t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+            v = t.numpy().view(dtype).reshape(a.shape)
+            v[...] = a
+            self._keep.append(t)
+            return v
+
+        self._keep = []
+        self.ctx = ctx
+        self.R = len(tok_off) - 1
+        self.tokens = pin(tokens, np.uint64)
+        self.tok_off = pin(tok_off, np.int64)
+        self.res = pin(res, RES_DTYPE)
+        self.group = pin(group, np.int32)
+        self.wf = pin(wf, np.int32)
+        self.role = pin(role, np.int32)
+        cl = cluster
+        self.rid = np.ascontiguousarray(cl.replica_id, np.int32)
+        self.kv = np.ascontiguousarray(cl.kv_capacity, np.int64)
+        self.aoff = np.ascontiguousarray(cl.asg_off, np.int64)
+        self.asg = np.ascontiguousarray(cl.asg, RES_DTYPE) if len(cl.asg) else np.zeros(1, RES_DTYPE)
+        self.coff = np.ascontiguousarray(cl.cand_off, np.int32)
+        self.cand = np.ascontiguousarray(cl.cand, np.int32)
+        self.out_dec = pin(np.zeros(max(self.R, 1), DEC_DTYPE), DEC_DTYPE)
+        self.out_adm = pin(np.zeros(max(self.R, 1), np.int32), np.int32)
+        self.out_m3 = pin(np.zeros((max(self.R, 1), 3), np.int64), np.int64)
+        p = lambda a: a.ctypes.data  # noqa: E731
+        self.bh = _lib.BatchHost(self.R, 0, p(self.tokens), p(self.tok_off), p(self.res),
+                                 p(self.group), p(self.wf), p(self.role))
+        self.nh = _lib.NodesHost(p(self.rid), p(self.kv), p(self.aoff), p(self.asg),
+                                 len(self.coff) - 1, 0, p(self.coff), p(self.cand))
+
+    @property
+    def h2d_bytes(self):
+        return int(self.tokens.nbytes + self.tok_off.nbytes + self.res.nbytes + self.group.nbytes
+                   + self.wf.nbytes + self.role.nbytes + self.rid.nbytes + self.kv.nbytes
+                   + self.aoff.nbytes + self.asg.nbytes + self.coff.nbytes + self.cand.nbytes)
+
+    @property
+    def d2h_bytes(self):
+        return int(self.R * (DEC_DTYPE.itemsize + 4 + 24))
+
+    def __call__(self, now, mode=SEQ_COMMIT, eps=0.05, speculative=True, release=True):
+        check(_lib._lib.pyg_step_host(self.ctx.h, C.byref(self.bh), C.byref(self.nh), mode, eps,
+                                      now, int(bool(speculative)), int(bool(release)),
+                                      self.out_dec.ctypes.data, self.out_adm.ctypes.data,
+                                      self.out_m3.ctypes.data))
+        return self.out_dec, self.out_adm, self.out_m3

@@ -9,6 +9,8 @@
 
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+
 #include "ctx.cuh"
 #include "device_ops.cuh"
 
@@ -16,74 +18,6 @@ using namespace pyg;
 using namespace pyg_host;
 
 namespace {
-
-// ------------------------------------------------------------------- K1
-// One lane per request; 16-byte read-only loads, software-pipelined 8 tokens
-// ahead so each lane keeps 64 B in flight (hashing is a serial FNV chain per
-// request; parallelism comes from requests).
-__global__ void __launch_bounds__(256) k_hash_batch(const uint64_t* __restrict__ tokens,
-                                                    const int64_t* __restrict__ tok_off, int R,
-                                                    const int64_t* __restrict__ hash_off,
-                                                    uint64_t* __restrict__ hashes, int B) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= R) return;
-  const int64_t s = tok_off[r];
-  const int64_t n = tok_off[r + 1] - s;
-  uint64_t* out = hashes + hash_off[r];
-  const uint64_t* p = tokens + s;
-  uint64_t h = kFnvOffset;
-  int cd = B;
-  int64_t k = 0, i = 0;
-  if ((s & 1) && n > 0) {  // 16-byte alignment of the vector loads
-    h = fnv_token(h, __ldg(p));
-    if (--cd == 0) {
-      out[k++] = h;
-      cd = B;
-    }
-    i = 1;
-  }
-  const ulonglong2* v = reinterpret_cast<const ulonglong2*>(p + i);
-  const int64_t nv = (n - i) / 8;  // groups of 8 tokens
-  ulonglong2 a0, a1, a2, a3;
-  if (nv > 0) {
-    a0 = __ldg(v);
-    a1 = __ldg(v + 1);
-    a2 = __ldg(v + 2);
-    a3 = __ldg(v + 3);
-  }
-  for (int64_t g = 0; g < nv; ++g) {
-    const uint64_t t[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
-    if (g + 1 < nv) {
-      const ulonglong2* q = v + 4 * (g + 1);
-      a0 = __ldg(q);
-      a1 = __ldg(q + 1);
-      a2 = __ldg(q + 2);
-      a3 = __ldg(q + 3);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      h = fnv_token(h, t[j]);
-      if (--cd == 0) {
-        out[k++] = h;
-        cd = B;
-      }
-    }
-  }
-  for (int64_t x = i + nv * 8; x < n; ++x) {
-    h = fnv_token(h, __ldg(p + x));
-    if (--cd == 0) {
-      out[k++] = h;
-      cd = B;
-    }
-  }
-  if (n > 0 && cd != B) out[k] = h;  // the ragged last block (hierarchy.cpp:26)
-}
-
-__global__ void k_nblocks(const int64_t* tok_off, int R, int B, int64_t* nb) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < R) nb[r] = (tok_off[r + 1] - tok_off[r] + B - 1) / B;
-  if (r == R) nb[R] = 0;
-}
 
 // ------------------------------------------------------------------- K2
 // staged[r][j] = tier(L2 of candidate j).matched_prefix(prompt_r)
@@ -139,272 +73,6 @@ __global__ void k_lookup_batch(CtxDev c, const uint64_t* __restrict__ tokens,
     const int64_t kb = thread_walk(t, hs, nh);
     const int64_t m = kb ? matched_from_blocks(kb, L, c.B) : 0;
     out[3 * r + k] = ragged_extend(t, t.log, tokens + tok_off[r], L, hs, m, c.B);
-  }
-}
-
-// ------------------------------------------------------------------- K3
-struct NodeScratch {
-  int64_t* free_;    // kv_capacity - sum of assigned tokens()
-  double* b0;        // oom_bound(node, alpha=+0.0): 0.0 + a_1 + ... (router.cpp:13-17)
-  double* ba;        // oom_bound(node, alpha=a*)
-  int32_t* head;     // appended placements (seq-commit): linked list of alphas
-  int32_t* tail;
-  double* app_alpha; // [R]
-  int32_t* app_next; // [R]
-};
-
-// Per replica: capacity_holds / oom_bound aggregates over the assigned set.
-__global__ void k_node_prep(int n, const pyg_nodes_dev nodes, NodeScratch ns) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int64_t sum = 0;
-  double b = 0.0;
-  for (int64_t k = nodes.asg_off[i]; k < nodes.asg_off[i + 1]; ++k) {
-    const pyg_reservation& a = nodes.asg[k];
-    sum += res_tokens(a.prompt_len, a.upper, a.tokens_generated);
-    b += a.alpha;
-  }
-  ns.free_[i] = nodes.kv_capacity[i] - sum;
-  ns.b0[i] = b;
-  ns.head[i] = -1;
-  ns.tail[i] = -1;
-}
-
-__device__ __forceinline__ bool same_bits(double a, double b) {
-  return __double_as_longlong(a) == __double_as_longlong(b);
-}
-
-// oom_bound(node i, alpha): alpha + assigned alphas in order + appended placements.
-__device__ __forceinline__ double node_bound(const pyg_nodes_dev& nodes, const NodeScratch& ns,
-                                             int i, double alpha, bool have_star, double astar) {
-  if (same_bits(alpha, 0.0)) return ns.b0[i];
-  if (have_star && same_bits(alpha, astar)) return ns.ba[i];
-  double b = alpha;
-  for (int64_t k = nodes.asg_off[i]; k < nodes.asg_off[i + 1]; ++k) b += nodes.asg[k].alpha;
-  for (int32_t q = ns.head[i]; q >= 0; q = ns.app_next[q]) b += ns.app_alpha[q];
-  return b;
-}
-
-struct RouteCtx {
-  pyg_nodes_dev nodes;
-  NodeScratch ns;
-  const int32_t* cand_off;
-  const int32_t* cand;
-  int max_cand;
-  const int32_t* staged;
-  double eps;
-};
-
-// sched::route (router.cpp:19-50) of one request over its group's candidates,
-// one warp (lanes over candidates).  Returns the decision and the winner's
-// candidate slot (-1 = wait).
-__device__ pyg_decision warp_route(const RouteCtx& rc, int r, int g, const pyg_reservation& q,
-                                   bool have_star, double astar, int* win_slot) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = res_tokens(q.prompt_len, q.upper, q.tokens_generated);
-  const int c0 = rc.cand_off[g], nc = rc.cand_off[g + 1] - c0;
-  RouteAcc best{0, 0, 0, -1};
-  for (int j = lane; j < nc; j += 32) {
-    const int n = rc.cand[c0 + j];
-    const int64_t fr = rc.ns.free_[n];
-    if (t > fr) continue;  // capacity_holds (router.cpp:7-11)
-    const double b = node_bound(rc.nodes, rc.ns, n, q.alpha, have_star, astar);
-    if (b > rc.eps) continue;
-    RouteAcc a{fr - t, rc.staged[static_cast<int64_t>(r) * rc.max_cand + j],
-               rc.nodes.replica_id[n], j};
-    if (acc_better(a, best)) best = a;
-  }
-  best = warp_best(best);
-  int32_t p1 = 0x7fffffff, p2 = 0x7fffffff;
-  if (best.pos >= 0) {
-    for (int j = lane; j < nc; j += 32) {
-      const int n = rc.cand[c0 + j];
-      const int64_t fr = rc.ns.free_[n];
-      if (t > fr || fr - t != best.h) continue;
-      const double b = node_bound(rc.nodes, rc.ns, n, q.alpha, have_star, astar);
-      if (b > rc.eps) continue;
-      p1 = min(p1, j);
-      if (rc.staged[static_cast<int64_t>(r) * rc.max_cand + j] == best.s) p2 = min(p2, j);
-    }
-  }
-  p1 = warp_min_i32(p1);
-  p2 = warp_min_i32(p2);
-  pyg_decision d{-1, 0, 0, 0.0};
-  *win_slot = best.pos;
-  if (best.pos >= 0) {
-    const int n = rc.cand[c0 + best.pos];
-    d.target = best.id;
-    d.headroom = best.h;
-    d.oom_bound = node_bound(rc.nodes, rc.ns, n, q.alpha, have_star, astar);
-    d.tiebreak = p1 < p2 ? 1 : 0;
-  }
-  return d;
-}
-
-// SNAPSHOT: every request against the same node state; one warp per request.
-__global__ void k_route_snapshot(RouteCtx rc, const pyg_reservation* req, const int32_t* group,
-                                 int R, pyg_decision* out, int32_t* t_idx) {
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= R) return;
-  const int g = group[r];
-  int slot;
-  const pyg_decision d = warp_route(rc, r, g, req[r], false, 0.0, &slot);
-  if ((threadIdx.x & 31) == 0) {
-    out[r] = d;
-    t_idx[r] = slot >= 0 ? rc.cand[rc.cand_off[g] + slot] : -1;
-  }
-}
-
-// SEQ_COMMIT (engine.cpp:650-692): the group's requests in order; a placement
-// is appended to its node before the next request is routed.  One warp per
-// group.  Requests that provably cannot be placed (t > the largest free
-// capacity among nodes whose bound admits their alpha) wait without a full
-// evaluation -- the exact feasibility test for alpha in {+0.0, a*}; other
-// alphas always take the full evaluation.
-__global__ void k_route_seq(RouteCtx rc, const pyg_reservation* req, const int32_t* group, int R,
-                            pyg_decision* out, int32_t* t_idx) {
-  const int g = blockIdx.x;
-  const int lane = threadIdx.x;
-  const int c0 = rc.cand_off[g], nc = rc.cand_off[g + 1] - c0;
-  // a* = alpha of the group's first request with alpha != +0.0
-  bool have_star = false;
-  double astar = 0.0;
-  for (int base = 0; base < R && !have_star; base += 32) {
-    const int r = base + lane;
-    const bool nz = r < R && group[r] == g && !same_bits(req[r].alpha, 0.0);
-    const unsigned m = __ballot_sync(kFull, nz);
-    if (m) {
-      const int src = __ffs(m) - 1;
-      astar = __shfl_sync(kFull, r < R ? req[r].alpha : 0.0, src);
-      have_star = true;
-    }
-  }
-  if (have_star) {
-    for (int j = lane; j < nc; j += 32) {
-      const int n = rc.cand[c0 + j];
-      double b = astar;
-      for (int64_t k = rc.nodes.asg_off[n]; k < rc.nodes.asg_off[n + 1]; ++k)
-        b += rc.nodes.asg[k].alpha;
-      rc.ns.ba[n] = b;
-    }
-    __syncwarp();
-  }
-  // F0 / Fa: max free over candidates whose bound admits alpha = +0.0 / a*
-  auto refresh = [&](int64_t& F0, int64_t& Fa) {
-    int64_t f0 = INT64_MIN, fa = INT64_MIN;
-    for (int j = lane; j < nc; j += 32) {
-      const int n = rc.cand[c0 + j];
-      const int64_t fr = rc.ns.free_[n];
-      if (!(rc.ns.b0[n] > rc.eps)) f0 = max(f0, fr);
-      if (have_star && !(rc.ns.ba[n] > rc.eps)) fa = max(fa, fr);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      f0 = max(f0, __shfl_xor_sync(kFull, f0, o));
-      fa = max(fa, __shfl_xor_sync(kFull, fa, o));
-    }
-    F0 = f0;
-    Fa = fa;
-  };
-  int64_t F0, Fa;
-  refresh(F0, Fa);
-  int32_t napp = 0;  // appended placements of this group live at app index (g, ...) -> use r
-  for (int base = 0; base < R; base += 32) {
-    const int r = base + lane;
-    const bool mine = r < R && group[r] == g;
-    pyg_reservation q{0, 0, 0.0, 0};
-    if (mine) q = req[r];
-    const int64_t t = res_tokens(q.prompt_len, q.upper, q.tokens_generated);
-    const bool z = same_bits(q.alpha, 0.0);
-    const bool s = have_star && same_bits(q.alpha, astar);
-    unsigned todo = __ballot_sync(kFull, mine);
-    while (todo) {
-      // candidates that could still be placed under the current state
-      const bool could = ((todo >> lane) & 1u) && ((z && t <= F0) || (s && t <= Fa) || (!z && !s));
-      const unsigned cm = __ballot_sync(kFull, could);
-      // lanes before the first candidate wait
-      const unsigned first = cm ? (1u << (__ffs(cm) - 1)) : 0u;
-      const unsigned waiting = cm ? (todo & (first - 1)) : todo;
-      if ((waiting >> lane) & 1u) {
-        out[r] = pyg_decision{-1, 0, 0, 0.0};
-        t_idx[r] = -1;
-      }
-      todo &= ~waiting;
-      if (!cm) break;
-      const int jl = __ffs(cm) - 1;
-      const int rr = base + jl;
-      pyg_reservation qq;
-      qq.prompt_len = __shfl_sync(kFull, q.prompt_len, jl);
-      qq.upper = __shfl_sync(kFull, q.upper, jl);
-      qq.alpha = __shfl_sync(kFull, q.alpha, jl);
-      qq.tokens_generated = __shfl_sync(kFull, q.tokens_generated, jl);
-      int slot;
-      const pyg_decision d = warp_route(rc, rr, g, qq, have_star, astar, &slot);
-      if (lane == 0) {
-        out[rr] = d;
-        t_idx[rr] = slot >= 0 ? rc.cand[c0 + slot] : -1;
-      }
-      if (slot >= 0) {
-        const int n = rc.cand[c0 + slot];
-        if (lane == 0) {
-          const int64_t tt = res_tokens(qq.prompt_len, qq.upper, qq.tokens_generated);
-          rc.ns.free_[n] -= tt;
-          rc.ns.b0[n] += qq.alpha;  // oom_bound appends this alpha last (router.cpp:15)
-          rc.ns.ba[n] += qq.alpha;
-          rc.ns.app_alpha[rr] = qq.alpha;
-          rc.ns.app_next[rr] = -1;
-          if (rc.ns.tail[n] >= 0)
-            rc.ns.app_next[rc.ns.tail[n]] = rr;
-          else
-            rc.ns.head[n] = rr;
-          rc.ns.tail[n] = rr;
-        }
-        __syncwarp();
-        __threadfence_block();
-        refresh(F0, Fa);
-        ++napp;
-      }
-      todo &= ~(1u << jl);
-    }
-  }
-}
-
-// Stable per-replica lists of placed requests (placement order == request order).
-__global__ void k_count_placed(const int32_t* t_idx, int R, int32_t* cnt) {
-  __shared__ int32_t sc[32];
-  const int rep = blockIdx.x;
-  int32_t c = 0;
-  for (int r = threadIdx.x; r < R; r += blockDim.x) c += t_idx[r] == rep;
-  c = warp_sum(c);
-  if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t s = 0;
-    for (int w = 0; w < (blockDim.x + 31) / 32; ++w) s += sc[w];
-    cnt[rep] = s;
-  }
-}
-
-__global__ void k_scan_placed(const int32_t* cnt, int n, int32_t* off) {
-  if (threadIdx.x || blockIdx.x) return;
-  int32_t s = 0;
-  for (int i = 0; i < n; ++i) {
-    off[i] = s;
-    s += cnt[i];
-  }
-  off[n] = s;
-}
-
-__global__ void k_fill_placed(const int32_t* t_idx, int R, const int32_t* off, int32_t* placed) {
-  const int rep = blockIdx.x;
-  const int lane = threadIdx.x;  // one warp, in order
-  int32_t w = off[rep];
-  for (int base = 0; base < R; base += 32) {
-    const int r = base + lane;
-    const bool m = r < R && t_idx[r] == rep;
-    const unsigned bm = __ballot_sync(kFull, m);
-    if (m) placed[w + __popc(bm & lanemask_lt())] = r;
-    w += __popc(bm);
   }
 }
 
@@ -638,12 +306,6 @@ __global__ void k_release(CtxDev c, const int64_t* tok_off, const int64_t* hash_
   }
 }
 
-struct NbOp {
-  int B;
-  const int64_t* off;
-  __device__ int64_t operator()(int64_t r) const { return (off[r + 1] - off[r] + B - 1) / B; }
-};
-
 }  // namespace
 
 // =================================================================== C-ABI
@@ -658,39 +320,6 @@ int pyg_check_device_error(pyg_ctx* c) {
     set_error("device-side log capacity exhausted in a batched kernel");
     return PYG_ECAPACITY;
   }
-  return PYG_OK;
-}
-
-int pyg_hash_offsets_dev(pyg_ctx* c, const int64_t* d_tok_off, int32_t R, int64_t* d_hash_off,
-                         int64_t* total) {
-  if (!c || R < 0) return PYG_EINVAL;
-  void* sp;
-  int rc = scratch(c, (R + 2) * sizeof(int64_t), &sp);
-  if (rc) return rc;
-  auto* nb = static_cast<int64_t*>(sp);
-  k_nblocks<<<(R + 256) / 256, 256, 0, c->stream>>>(d_tok_off, R, c->B, nb);
-  PYG_LAUNCHED(c);
-  size_t tmp = 0;
-  PYG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nb, d_hash_off, R + 1, c->stream));
-  void* d_tmp = nullptr;
-  PYG_CUDA(cudaMallocAsync(&d_tmp, tmp, c->stream));
-  PYG_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp, nb, d_hash_off, R + 1, c->stream));
-  PYG_LAUNCHED(c);
-  PYG_CUDA(cudaFreeAsync(d_tmp, c->stream));
-  if (total) {
-    PYG_CUDA(cudaMemcpyAsync(total, d_hash_off + R, 8, cudaMemcpyDeviceToHost, c->stream));
-    PYG_CUDA(cudaStreamSynchronize(c->stream));
-  }
-  return PYG_OK;
-}
-
-int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off, int32_t R,
-                       const int64_t* d_hash_off, uint64_t* d_hashes) {
-  if (!c || R < 0) return PYG_EINVAL;
-  if (R == 0) return PYG_OK;
-  k_hash_batch<<<(R + 255) / 256, 256, 0, c->stream>>>(d_tokens, d_tok_off, R, d_hash_off,
-                                                       d_hashes, c->B);
-  PYG_LAUNCHED(c);
   return PYG_OK;
 }
 
@@ -716,64 +345,6 @@ int pyg_lookup_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_
   k_lookup_batch<<<(R + 127) / 128, 128, 0, c->stream>>>(c->hd, d_tokens, d_tok_off, d_hash_off,
                                                          d_hashes, R, d_rep, with_l3, d_match3);
   PYG_LAUNCHED(c);
-  return PYG_OK;
-}
-
-int pyg_route_batch_dev(pyg_ctx* c, int32_t mode, const pyg_nodes_dev* nodes,
-                        const pyg_reservation* d_req, int32_t R, const int32_t* d_group,
-                        int32_t n_groups, const int32_t* d_cand_off, const int32_t* d_cand,
-                        int32_t max_cand, const int32_t* d_staged, double eps,
-                        pyg_decision* d_out, int32_t* d_placed_off, int32_t* d_placed) {
-  if (!c || !nodes || R < 0 || n_groups < 0) return PYG_EINVAL;
-  const int n = c->n_rep;
-  // scratch: free, b0, ba, head, tail, app_alpha, app_next, t_idx, counts
-  const size_t bytes = n * (8 + 8 + 8 + 4 + 4 + 4) + static_cast<size_t>(R) * (8 + 4 + 4) + 256;
-  void* sp;
-  int rc = scratch(c, bytes, &sp);
-  if (rc) return rc;
-  char* p = static_cast<char*>(sp);
-  NodeScratch ns;
-  ns.free_ = reinterpret_cast<int64_t*>(p);
-  p += n * 8;
-  ns.b0 = reinterpret_cast<double*>(p);
-  p += n * 8;
-  ns.ba = reinterpret_cast<double*>(p);
-  p += n * 8;
-  ns.app_alpha = reinterpret_cast<double*>(p);
-  p += static_cast<size_t>(R) * 8;
-  ns.head = reinterpret_cast<int32_t*>(p);
-  p += n * 4;
-  ns.tail = reinterpret_cast<int32_t*>(p);
-  p += n * 4;
-  ns.app_next = reinterpret_cast<int32_t*>(p);
-  p += static_cast<size_t>(R) * 4;
-  int32_t* t_idx = reinterpret_cast<int32_t*>(p);
-  p += static_cast<size_t>(R) * 4;
-  int32_t* cnt = reinterpret_cast<int32_t*>(p);
-  if (n) {
-    k_node_prep<<<(n + 127) / 128, 128, 0, c->stream>>>(n, *nodes, ns);
-    PYG_LAUNCHED(c);
-  }
-  RouteCtx rcx{*nodes, ns, d_cand_off, d_cand, max_cand, d_staged, eps};
-  if (R) {
-    if (mode == PYG_ROUTE_SNAPSHOT) {
-      k_route_snapshot<<<(R + 7) / 8, 256, 0, c->stream>>>(rcx, d_req, d_group, R, d_out, t_idx);
-    } else if (mode == PYG_ROUTE_SEQ_COMMIT) {
-      k_route_seq<<<n_groups, 32, 0, c->stream>>>(rcx, d_req, d_group, R, d_out, t_idx);
-    } else {
-      set_error("unknown route mode");
-      return PYG_EINVAL;
-    }
-    PYG_LAUNCHED(c);
-  }
-  if (d_placed_off && d_placed && n) {
-    k_count_placed<<<n, 256, 0, c->stream>>>(t_idx, R, cnt);
-    PYG_LAUNCHED(c);
-    k_scan_placed<<<1, 1, 0, c->stream>>>(cnt, n, d_placed_off);
-    PYG_LAUNCHED(c);
-    k_fill_placed<<<n, 32, 0, c->stream>>>(t_idx, R, d_placed_off, d_placed);
-    PYG_LAUNCHED(c);
-  }
   return PYG_OK;
 }
 
@@ -814,3 +385,108 @@ int pyg_release_batch_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d
 }
 
 }  // extern "C"
+
+// ======================================================= host-buffer entry
+// Device buffers for the host entry live in pyg_ctx::d_list (shared with the completion
+// sweep's lists; both are synchronous calls).
+extern "C" int pyg_step_host(pyg_ctx* c, const pyg_batch_host* b, const pyg_nodes_host* nd,
+                             int32_t mode, double eps, double now, int32_t spec, int32_t release,
+                             pyg_decision* out_dec, int32_t* out_adm, int64_t* out_m3) {
+  if (!c || !b || !nd || b->n_req < 0 || nd->n_groups < 0) return PYG_EINVAL;
+  const int32_t R = b->n_req;
+  const int nrep = c->n_rep;
+  const int64_t T = R ? b->tok_off[R] : 0;
+  const int64_t A = nrep ? nd->asg_off[nrep] : 0;
+  const int32_t G = nd->n_groups;
+  const int32_t NC = G ? nd->cand_off[G] : 0;
+  int32_t max_cand = 0;
+  for (int g = 0; g < G; ++g) max_cand = std::max(max_cand, nd->cand_off[g + 1] - nd->cand_off[g]);
+  int64_t H = 0;
+  for (int32_t r = 0; r < R; ++r) H += (b->tok_off[r + 1] - b->tok_off[r] + c->B - 1) / c->B;
+  // device layout (each region 256-byte aligned)
+  auto al = [](size_t x) { return (x + 255) & ~size_t{255}; };
+  size_t off = 0;
+  const size_t o_tok = off; off += al(T * 8 + 16);
+  const size_t o_toff = off; off += al((R + 1) * 8);
+  const size_t o_hoff = off; off += al((R + 1) * 8);
+  const size_t o_hash = off; off += al(H * 8 + 8);
+  const size_t o_req = off; off += al(R * sizeof(pyg_reservation) + 8);
+  const size_t o_grp = off; off += al(R * 4 + 4);
+  const size_t o_wf = off; off += al(R * 4 + 4);
+  const size_t o_role = off; off += al(R * 4 + 4);
+  const size_t o_rid = off; off += al(nrep * 4 + 4);
+  const size_t o_kv = off; off += al(nrep * 8 + 8);
+  const size_t o_aoff = off; off += al((nrep + 1) * 8);
+  const size_t o_asg = off; off += al(A * sizeof(pyg_reservation) + 8);
+  const size_t o_coff = off; off += al((G + 1) * 4);
+  const size_t o_cand = off; off += al(NC * 4 + 4);
+  const size_t o_stg = off; off += al(static_cast<size_t>(R) * std::max(max_cand, 1) * 4);
+  const size_t o_dec = off; off += al(R * sizeof(pyg_decision) + 8);
+  const size_t o_poff = off; off += al((nrep + 1) * 4);
+  const size_t o_pl = off; off += al(R * 4 + 4);
+  const size_t o_adm = off; off += al(R * 4 + 4);
+  const size_t o_m3 = off; off += al(R * 24 + 8);
+  if (off > c->d_list_size) {
+    if (c->d_list) {
+      PYG_CUDA(cudaStreamSynchronize(c->stream));
+      cudaFree(c->d_list);
+      c->d_list = nullptr;
+    }
+    PYG_CUDA(cudaMalloc(&c->d_list, off));
+    c->d_list_size = off;
+  }
+  char* d = static_cast<char*>(c->d_list);
+  auto h2d = [&](size_t o, const void* src, size_t n) -> int {
+    if (n) PYG_CUDA(cudaMemcpyAsync(d + o, src, n, cudaMemcpyHostToDevice, c->stream));
+    return PYG_OK;
+  };
+  int rc;
+  if ((rc = h2d(o_tok, b->tokens, T * 8))) return rc;
+  if ((rc = h2d(o_toff, b->tok_off, (R + 1) * 8))) return rc;
+  if ((rc = h2d(o_req, b->req, R * sizeof(pyg_reservation)))) return rc;
+  if ((rc = h2d(o_grp, b->group, R * 4))) return rc;
+  if ((rc = h2d(o_wf, b->workflow, R * 4))) return rc;
+  if ((rc = h2d(o_role, b->role, R * 4))) return rc;
+  if ((rc = h2d(o_rid, nd->replica_id, nrep * 4))) return rc;
+  if ((rc = h2d(o_kv, nd->kv_capacity, nrep * 8))) return rc;
+  if ((rc = h2d(o_aoff, nd->asg_off, (nrep + 1) * 8))) return rc;
+  if ((rc = h2d(o_asg, nd->asg, A * sizeof(pyg_reservation)))) return rc;
+  if ((rc = h2d(o_coff, nd->cand_off, (G + 1) * 4))) return rc;
+  if ((rc = h2d(o_cand, nd->cand, NC * 4))) return rc;
+  auto* tok = reinterpret_cast<uint64_t*>(d + o_tok);
+  auto* toff = reinterpret_cast<int64_t*>(d + o_toff);
+  auto* hoff = reinterpret_cast<int64_t*>(d + o_hoff);
+  auto* hash = reinterpret_cast<uint64_t*>(d + o_hash);
+  if ((rc = pyg_hash_offsets_dev(c, toff, R, hoff, nullptr))) return rc;
+  if ((rc = pyg_hash_batch_dev(c, tok, toff, R, hoff, hash))) return rc;
+  auto* grp = reinterpret_cast<int32_t*>(d + o_grp);
+  auto* coff = reinterpret_cast<int32_t*>(d + o_coff);
+  auto* cand = reinterpret_cast<int32_t*>(d + o_cand);
+  auto* stg = reinterpret_cast<int32_t*>(d + o_stg);
+  if ((rc = pyg_staged_matrix_dev(c, tok, toff, hoff, hash, R, grp, coff, cand, max_cand, stg)))
+    return rc;
+  pyg_nodes_dev ndv{reinterpret_cast<int32_t*>(d + o_rid), reinterpret_cast<int64_t*>(d + o_kv),
+                    reinterpret_cast<int64_t*>(d + o_aoff),
+                    reinterpret_cast<pyg_reservation*>(d + o_asg)};
+  auto* dec = reinterpret_cast<pyg_decision*>(d + o_dec);
+  auto* poff = reinterpret_cast<int32_t*>(d + o_poff);
+  auto* pl = reinterpret_cast<int32_t*>(d + o_pl);
+  if ((rc = pyg_route_batch_dev(c, mode, &ndv, reinterpret_cast<pyg_reservation*>(d + o_req), R,
+                                grp, G, coff, cand, max_cand, stg, eps, dec, poff, pl)))
+    return rc;
+  auto* adm = reinterpret_cast<int32_t*>(d + o_adm);
+  auto* m3 = reinterpret_cast<int64_t*>(d + o_m3);
+  if ((rc = pyg_admit_batch_dev(c, tok, toff, hoff, hash, reinterpret_cast<int32_t*>(d + o_wf),
+                                reinterpret_cast<int32_t*>(d + o_role), R, poff, pl, now, spec,
+                                adm, m3)))
+    return rc;
+  if (release && (rc = pyg_release_batch_dev(c, toff, hoff, hash, R, poff, pl, adm))) return rc;
+  if (R && out_dec)
+    PYG_CUDA(cudaMemcpyAsync(out_dec, dec, R * sizeof(pyg_decision), cudaMemcpyDeviceToHost,
+                             c->stream));
+  if (R && out_adm)
+    PYG_CUDA(cudaMemcpyAsync(out_adm, adm, R * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (R && out_m3) PYG_CUDA(cudaMemcpyAsync(out_m3, m3, R * 24, cudaMemcpyDeviceToHost, c->stream));
+  PYG_CUDA(cudaStreamSynchronize(c->stream));
+  return pyg_check_device_error(c);
+}

@@ -268,7 +268,7 @@ void pyg_destroy(pyg_ctx* c) {
 
 int pyg_set_stream(pyg_ctx* c, void* s) {
   if (!c) return PYG_EINVAL;
-  c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+  c->stream = static_cast<cudaStream_t>(s);  // NULL = the default (legacy) stream
   return PYG_OK;
 }
 

@@ -98,9 +98,13 @@ __device__ __forceinline__ uint64_t fnv_token(uint64_t h, uint64_t v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t w = i < 4 ? vl : vh;
-    lo ^= (w >> (8 * (i & 3))) & 0xffu;
-    const uint64_t p = static_cast<uint64_t>(lo) * 0x1B3u;
-    hi = hi * 0x1B3u + static_cast<uint32_t>(p >> 32) + (lo << 8);
+    const uint32_t x = lo ^ ((w >> (8 * (i & 3))) & 0xffu);  // LOP3 (+SHF)
+    uint64_t p;                                                // IMAD.WIDE.U32
+    asm("mul.wide.u32 %0, %1, 435;" : "=l"(p) : "r"(x));
+    uint32_t t;                                                // LEA: (x << 8) + carry
+    asm("{\n\t.reg .u32 s;\n\tshl.b32 s, %1, 8;\n\tadd.u32 %0, s, %2;\n\t}"
+        : "=r"(t) : "r"(x), "r"(static_cast<uint32_t>(p >> 32)));
+    asm("mad.lo.u32 %0, %1, 435, %2;" : "=r"(hi) : "r"(hi), "r"(t));  // IMAD
     lo = static_cast<uint32_t>(p);
   }
   return (static_cast<uint64_t>(hi) << 32) | lo;

@@ -1,0 +1,192 @@
+// k_hash.cu -- K1: batched chain_boundary_hashes (hierarchy.cpp:21-30).
+//
+// FNV-1a is a serial chain per request, so parallelism comes from requests:
+// one lane owns one request.  To keep HBM reads coalesced, each warp stages
+// its 32 requests' tokens through shared memory in 16-token chunks with 16-byte
+// cp.async copies (8 lanes x 16 B = one request's chunk, 4 requests per warp
+// instruction), double-buffered, and each lane then hashes its own row with
+// conflict-free LDS.128 (row stride 144 B: lanes i and i+8 share a bank group,
+// 4 wavefronts per 512 B = the minimum).  Requests are processed in descending
+// length order (a 16-bit radix sort on ceil(len/4)) so lanes of a warp carry
+// equal work and the longest chains start first.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "ctx.cuh"
+#include "device_ops.cuh"
+
+using namespace pyg;
+using namespace pyg_host;
+
+namespace {
+
+constexpr int kChunk = 16;                      // tokens per staged chunk
+constexpr int kRowBytes = kChunk * 8 + 16;      // 144: padded row
+constexpr int kStageBytes = 32 * kRowBytes;     // one warp, one stage
+constexpr int kWarps = 8;                       // warps per CTA
+constexpr int kSmemBytes = kWarps * 2 * kStageBytes;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// Chunks are aligned to each request's own first token, so with B % 16 == 0 a
+// block boundary always coincides with the end of a chunk: the emit decision
+// is per chunk and warp-uniform (no per-token test).  The last, partial chunk
+// and B % 16 != 0 take the generic per-token path.
+__global__ void __launch_bounds__(kWarps * 32, 2)
+k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
+              int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
+              uint64_t* __restrict__ hashes, int B) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbuf = smem + warp * 2 * kStageBytes;
+  // warps of one CTA take sorted warp-tasks gridDim.x apart: every CTA gets a
+  // mix of long and short requests
+  const int task = blockIdx.x + gridDim.x * warp;
+  const int idx = task * 32 + lane;
+  const bool valid = idx < R;
+  const int r = valid ? (order ? order[idx] : idx) : 0;
+  const int64_t s = valid ? tok_off[r] : 0;
+  const int64_t n = valid ? tok_off[r + 1] - s : 0;
+  const int nch = static_cast<int>((n + kChunk - 1) / kChunk);
+  const int maxch = __reduce_max_sync(kFull, nch);
+  if (maxch == 0) return;
+  uint64_t* out = hashes + (valid ? hash_off[r] : 0);
+  const bool fast = (B % kChunk) == 0;
+  const int cpb = B / kChunk;  // chunks per block (fast path)
+
+  const int sub = lane >> 4, q = lane & 15;  // 2 requests per instruction, 16 lanes x 8 B
+  auto issue = [&](int c) {
+    unsigned char* st = wbuf + (c & 1) * kStageBytes;
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const int jj = j + sub;
+      const int64_t sj = __shfl_sync(kFull, s, jj);
+      const int64_t nj = __shfl_sync(kFull, n, jj);
+      const int64_t pos = static_cast<int64_t>(c) * kChunk + q;
+      if (pos < nj) cp_async8(st + jj * kRowBytes + q * 8, tokens + sj + pos, 8);
+    }
+    cp_commit();
+  };
+
+  uint64_t h = kFnvOffset;
+  int64_t k = 0;
+  issue(0);
+  for (int c = 0; c < maxch; ++c) {
+    if (c + 1 < maxch)
+      issue(c + 1);
+    else
+      cp_commit();
+    cp_wait1();
+    __syncwarp();
+    if (c < nch) {
+      const unsigned char* row = wbuf + (c & 1) * kStageBytes + lane * kRowBytes;
+      const int64_t rem = n - static_cast<int64_t>(c) * kChunk;
+      if (fast && rem >= kChunk) {
+#pragma unroll
+        for (int x = 0; x < kChunk / 2; ++x) {
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(row + 16 * x);
+          h = fnv_token(h, v.x);
+          h = fnv_token(h, v.y);
+        }
+        if ((c + 1) % cpb == 0 || rem == kChunk) out[k++] = h;  // boundary or last token
+      } else {
+        const int p1 = rem < kChunk ? static_cast<int>(rem) : kChunk;
+        for (int p = 0; p < p1; ++p) {
+          h = fnv_token(h, *reinterpret_cast<const uint64_t*>(row + 8 * p));
+          const int64_t j = static_cast<int64_t>(c) * kChunk + p;  // position in the request
+          if ((j + 1) % B == 0 || j + 1 == n) out[k++] = h;  // hierarchy.cpp:26
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int64_t L = (tok_off[r + 1] - tok_off[r] + 3) >> 2;
+  key[r] = static_cast<uint16_t>(L > 65535 ? 65535 : L);
+  val[r] = r;
+}
+
+__global__ void k_nblocks(const int64_t* tok_off, int R, int B, int64_t* nb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) nb[r] = (tok_off[r + 1] - tok_off[r] + B - 1) / B;
+  if (r == R) nb[R] = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pyg_hash_offsets_dev(pyg_ctx* c, const int64_t* d_tok_off, int32_t R, int64_t* d_hash_off,
+                         int64_t* total) {
+  if (!c || R < 0) return PYG_EINVAL;
+  size_t tmp = 0;
+  PYG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, static_cast<int64_t*>(nullptr), d_hash_off,
+                                         R + 1, c->stream));
+  void* sp;
+  int rc = scratch(c, (R + 2) * sizeof(int64_t) + tmp + 256, &sp);
+  if (rc) return rc;
+  auto* nb = static_cast<int64_t*>(sp);
+  void* d_tmp = static_cast<char*>(sp) + (((R + 2) * sizeof(int64_t) + 255) & ~size_t{255});
+  k_nblocks<<<(R + 256) / 256, 256, 0, c->stream>>>(d_tok_off, R, c->B, nb);
+  PYG_LAUNCHED(c);
+  PYG_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp, nb, d_hash_off, R + 1, c->stream));
+  PYG_LAUNCHED(c);
+  if (total) {
+    PYG_CUDA(cudaMemcpyAsync(total, d_hash_off + R, 8, cudaMemcpyDeviceToHost, c->stream));
+    PYG_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  return PYG_OK;
+}
+
+int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off, int32_t R,
+                       const int64_t* d_hash_off, uint64_t* d_hashes) {
+  if (!c || R < 0) return PYG_EINVAL;
+  if (R == 0) return PYG_OK;
+  // length sort (descending) for warp balance
+  size_t tmp = 0;
+  PYG_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+      nullptr, tmp, static_cast<uint16_t*>(nullptr), static_cast<uint16_t*>(nullptr),
+      static_cast<int32_t*>(nullptr), static_cast<int32_t*>(nullptr), R, 0, 16, c->stream));
+  const size_t kb = (static_cast<size_t>(R) * 2 + 255) & ~size_t{255};
+  const size_t vb = (static_cast<size_t>(R) * 4 + 255) & ~size_t{255};
+  void* sp;
+  int rc = scratch(c, 2 * kb + 2 * vb + tmp + 256, &sp);
+  if (rc) return rc;
+  char* p = static_cast<char*>(sp);
+  auto* k_in = reinterpret_cast<uint16_t*>(p);
+  auto* k_out = reinterpret_cast<uint16_t*>(p + kb);
+  auto* v_in = reinterpret_cast<int32_t*>(p + 2 * kb);
+  auto* v_out = reinterpret_cast<int32_t*>(p + 2 * kb + vb);
+  void* d_tmp = p + 2 * kb + 2 * vb;
+  k_len_keys<<<(R + 255) / 256, 256, 0, c->stream>>>(d_tok_off, R, k_in, v_in);
+  PYG_LAUNCHED(c);
+  PYG_CUDA(cub::DeviceRadixSort::SortPairsDescending(d_tmp, tmp, k_in, k_out, v_in, v_out, R, 0,
+                                                     16, c->stream));
+  PYG_LAUNCHED(c);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_hash_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr = true;
+  }
+  const int per_block = kWarps * 32;
+  const int tasks = (R + 31) / 32;
+  const int grid = (tasks + kWarps - 1) / kWarps;  // task = blockIdx.x + grid * warp
+  k_hash_staged<<<grid, per_block, kSmemBytes, c->stream>>>(
+      d_tokens, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+}  // extern "C"

@@ -51,3 +51,24 @@ def test_step_restated_equals_reference():
         assert np.array_equal(x["admitted"], y["admitted"])
         assert np.array_equal(x["match3"], y["match3"])
     assert da == db
+
+
+@pytest.mark.skipif(not reference_available(16), reason="oracle/_ref not built")
+def test_reference_cpp_step_equals_composition():
+    """pref_step (the CPU baseline, C++ over the reference) == the Python composition."""
+    ref = Reference(16)
+    tr = W.deep_research(n_workflows=10, seed=6, device="cpu")
+    cl = W.make_cluster(6, 2, kv=20_000, l2=20_000, seed=7)
+    c1, l1, g1 = _state(ref, tr, cl)
+    c2, l2, g2 = _state(ref, tr, cl)
+    for s in range(2):
+        a = oracle_step(ref, c1, l1, g1, tr, cl, SEQ_COMMIT, 0.05, 5.0 + s, True, True)
+        n, dec, adm = ref.step(c2, l2, g2, True, tr.tokens_np(), tr.tok_off, tr.res, tr.group,
+                               tr.wf, tr.role, cl, SEQ_COMMIT, 0.05, 5.0 + s, True)
+        assert [tuple(x) for x in dec.tolist()] == [tuple(d) for d in a["decisions"]]
+        assert np.array_equal(adm, a["admitted"])
+        assert n == sum(len(p) for p in a["placed"])
+    for x, y in zip(c1, c2):
+        for t in (0, 1):
+            assert ref.dump(x, None, t).tobytes() == ref.dump(y, None, t).tobytes()
+    assert ref.dump(c1[0], l1, 2).tobytes() == ref.dump(c2[0], l2, 2).tobytes()

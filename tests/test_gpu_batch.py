@@ -103,3 +103,29 @@ def test_batch_coding_assistant_chat_accumulate():
     tr = W.coding_assistant(n_workflows=12, seed=2, device="cpu")
     cl = W.make_cluster(4, 1, kv=40_000, l2=40_000, seed=4)
     _run(tr, cl, 16, SEQ_COMMIT, steps=3)
+
+
+@pytest.mark.parametrize("B", [1, 5, 16, 32, 48, 64])
+def test_hash_batch_all_lengths(B):
+    """K1 over ragged batches: every length 0..300 and some long ones, odd/even starts."""
+    from paper_2604_25899_b200 import Context
+    from paper_2604_25899_b200 import batch as PB
+    rng = np.random.default_rng(B)
+    lens = np.concatenate([np.arange(0, 301), rng.integers(1000, 5000, 40)])
+    rng.shuffle(lens)
+    off = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    toks = rng.integers(0, 1 << 63, size=int(off[-1]), dtype=np.uint64) * np.uint64(2)
+    ctx = Context(1, 1000, 1000, B)
+    z = np.zeros(len(lens), np.int32)
+    res = np.zeros(len(lens), PB.RES_DTYPE)
+    db = PB.upload_batch(ctx, toks, off, res, z, z, z)
+    PB.bind_current_stream(ctx)
+    PB.hash_batch(ctx, db)
+    torch.cuda.synchronize()
+    got = db.hashes.cpu().numpy().view(np.uint64)
+    hoff = db.hash_off.cpu().numpy()
+    o = Restated(B)
+    for r in range(len(lens)):
+        want = o.chain_hashes(toks[off[r]:off[r + 1]])
+        assert np.array_equal(got[hoff[r]:hoff[r + 1]], want), (r, lens[r])

@@ -1,0 +1,6 @@
+set -x
+python paper_2604_25899_b200/build.py > gpurun_out/build.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+timeout 900 python bench.py --steps 5 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+tail -5 gpurun_out/bench.err
+cat gpurun_out/bench.json
