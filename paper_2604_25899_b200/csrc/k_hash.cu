@@ -14,6 +14,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+
 #include "ctx.cuh"
 #include "device_ops.cuh"
 
@@ -43,13 +45,17 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 __global__ void __launch_bounds__(kWarps * 32, 2)
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
-              uint64_t* __restrict__ hashes, int B) {
+              uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbuf = smem + warp * 2 * kStageBytes;
-  // warps of one CTA take sorted warp-tasks gridDim.x apart: every CTA gets a
-  // mix of long and short requests
-  const int task = blockIdx.x + gridDim.x * warp;
+  const int ntasks = (R + 31) / 32;
+  // persistent: each warp pulls 32-request tasks, longest first, until none are left
+  for (;;) {
+  int task = 0;
+  if (lane == 0) task = atomicAdd(next_task, 1);
+  task = __shfl_sync(kFull, task, 0);
+  if (task >= ntasks) break;
   const int idx = task * 32 + lane;
   const bool valid = idx < R;
   const int r = valid ? (order ? order[idx] : idx) : 0;
@@ -57,10 +63,11 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   const int64_t n = valid ? tok_off[r + 1] - s : 0;
   const int nch = static_cast<int>((n + kChunk - 1) / kChunk);
   const int maxch = __reduce_max_sync(kFull, nch);
-  if (maxch == 0) return;
+  if (maxch == 0) continue;
   uint64_t* out = hashes + (valid ? hash_off[r] : 0);
   const bool fast = (B % kChunk) == 0;
-  const int cpb = B / kChunk;  // chunks per block (fast path)
+  const int cpb = fast ? B / kChunk : 1;  // chunks per block (fast path)
+  int cc = cpb;
 
   const int sub = lane >> 4, q = lane & 15;  // 2 requests per instruction, 16 lanes x 8 B
   auto issue = [&](int c) {
@@ -96,7 +103,10 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
           h = fnv_token(h, v.x);
           h = fnv_token(h, v.y);
         }
-        if ((c + 1) % cpb == 0 || rem == kChunk) out[k++] = h;  // boundary or last token
+        if (--cc == 0 || rem == kChunk) {  // block boundary or the last token
+          out[k++] = h;
+          cc = cpb;
+        }
       } else {
         const int p1 = rem < kChunk ? static_cast<int>(rem) : kChunk;
         for (int p = 0; p < p1; ++p) {
@@ -108,6 +118,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
     }
     __syncwarp();
   }
+  }  // task loop
 }
 
 __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val) {
@@ -162,7 +173,7 @@ int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_to
   const size_t kb = (static_cast<size_t>(R) * 2 + 255) & ~size_t{255};
   const size_t vb = (static_cast<size_t>(R) * 4 + 255) & ~size_t{255};
   void* sp;
-  int rc = scratch(c, 2 * kb + 2 * vb + tmp + 256, &sp);
+  int rc = scratch(c, 2 * kb + 2 * vb + tmp + 512, &sp);
   if (rc) return rc;
   char* p = static_cast<char*>(sp);
   auto* k_in = reinterpret_cast<uint16_t*>(p);
@@ -182,9 +193,13 @@ int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_to
   }
   const int per_block = kWarps * 32;
   const int tasks = (R + 31) / 32;
-  const int grid = (tasks + kWarps - 1) / kWarps;  // task = blockIdx.x + grid * warp
+  static int n_sm = 0;
+  if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
+  const int grid = std::min((tasks + kWarps - 1) / kWarps, 2 * n_sm);  // persistent: 2 CTAs/SM
+  auto* ctr = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
+  PYG_CUDA(cudaMemsetAsync(ctr, 0, 4, c->stream));
   k_hash_staged<<<grid, per_block, kSmemBytes, c->stream>>>(
-      d_tokens, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B);
+      d_tokens, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
