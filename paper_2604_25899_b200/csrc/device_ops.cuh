@@ -495,6 +495,15 @@ __device__ __forceinline__ RouteAcc warp_best(RouteAcc a) {
   return a;
 }
 
+// single-instruction warp reductions (REDUX); 64-bit values as (signed hi, unsigned lo)
+__device__ __forceinline__ int64_t redux_max_i64(int64_t v) {
+  const int hi = static_cast<int>(v >> 32);
+  const unsigned lo = static_cast<unsigned>(v);
+  const int mh = __reduce_max_sync(kFull, hi);
+  const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+  return (static_cast<int64_t>(mh) << 32) | ml;
+}
+
 __device__ __forceinline__ int32_t warp_min_i32(int32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));

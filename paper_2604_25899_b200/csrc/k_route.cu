@@ -123,91 +123,121 @@ __global__ void k_route_snapshot(const pyg_nodes_dev nodes, const NodeScratch ns
 }
 
 // -------------------------------------------------------------- SEQ_COMMIT
-struct SeqIn {
-  int64_t t;     // reservation tokens()
-  double alpha;
-};
-
-// Parallel prep over the group-sorted order: tokens(), alpha; every decision
-// starts as "wait" (target nullopt, headroom 0, bound 0.0, no tiebreak); group
-// ranges; first non-zero-alpha position per group (defines a*).
 struct GroupStat {
-  int32_t start, end;
-  int32_t first_nz;   // position of the first alpha != +0.0 (INT32_MAX: none)
+  int32_t first_nz;   // smallest request index with alpha != +0.0 (defines a*; INT32_MAX none)
+  int32_t count;      // requests in the group
   int32_t n_other;    // requests whose alpha is neither +0.0 nor a*
+  int32_t nplaced;    // placements (written by the group's warp)
   int64_t min_t0;     // smallest tokens() among alpha == +0.0 requests
   int64_t min_t1;     // smallest tokens() among alpha == a* requests
 };
 
-__device__ __forceinline__ bool seg_head(uint32_t g, int lane) {
-  const uint32_t up = __shfl_up_sync(kFull, g, 1);
-  return lane == 0 || up != g;
-}
-
-template <class T, class Op>
-__device__ __forceinline__ T seg_reduce(T v, uint32_t g, int lane, Op op) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const T y = __shfl_down_sync(kFull, v, o);
-    const uint32_t gy = __shfl_down_sync(kFull, g, o);
-    if (lane + o < 32 && gy == g) v = op(v, y);
-  }
-  return v;
-}
-
-__global__ void k_seq_prep(const pyg_reservation* req, const int32_t* order,
-                           const uint32_t* gkey, int R, SeqIn* in, GroupStat* gs,
-                           pyg_decision* out, int32_t* t_idx) {
+__global__ void k_gs_init(GroupStat* gs, int G, int32_t* rcount, int32_t* rcur, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const bool ok = i < R;
-  const uint32_t g = ok ? gkey[i] : 0xffffffffu;
-  int32_t nz = INT32_MAX;
-  if (ok) {
-    const int r = order[i];
-    const pyg_reservation q = req[r];
-    in[i] = SeqIn{res_tokens(q.prompt_len, q.upper, q.tokens_generated), q.alpha};
+  if (i < G) gs[i] = GroupStat{INT32_MAX, 0, 0, 0, INT64_MAX, INT64_MAX};
+  if (i < n) {
+    rcount[i] = 0;
+    rcur[i] = 0;
+  }
+}
+
+// pass 1 (parallel): every decision starts as "wait"; per-group request count
+// and first non-zero alpha, reduced in shared memory then once per CTA.
+__global__ void k_seq_stats1(const pyg_reservation* req, const int32_t* group, int R, int G,
+                             GroupStat* gs, pyg_decision* out, int32_t* t_idx) {
+  extern __shared__ int32_t sh[];  // [2G]: first_nz, count
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    sh[g] = INT32_MAX;
+    sh[G + g] = 0;
+  }
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) {
+    const int g = group[r];
     out[r] = pyg_decision{-1, 0, 0, 0.0};
     t_idx[r] = -1;
-    if (i == 0 || gkey[i - 1] != g) gs[g].start = i;
-    if (i == R - 1 || gkey[i + 1] != g) gs[g].end = i + 1;
-    if (!same_bits(q.alpha, 0.0)) nz = i;
+    atomicAdd(&sh[G + g], 1);
+    if (!same_bits(req[r].alpha, 0.0)) atomicMin(&sh[g], r);
   }
-  nz = seg_reduce(nz, g, lane, [](int32_t a, int32_t b) { return a < b ? a : b; });
-  if (ok && seg_head(g, lane) && nz != INT32_MAX) atomicMin(&gs[g].first_nz, nz);
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    if (sh[g] != INT32_MAX) atomicMin(&gs[g].first_nz, sh[g]);
+    if (sh[G + g]) atomicAdd(&gs[g].count, sh[G + g]);
+  }
 }
 
-__global__ void k_seq_classes(const SeqIn* in, const uint32_t* gkey, int R, GroupStat* gs) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const bool ok = i < R;
-  const uint32_t g = ok ? gkey[i] : 0xffffffffu;
-  int64_t m0 = INT64_MAX, m1 = INT64_MAX;
-  int32_t other = 0;
-  if (ok) {
-    const SeqIn v = in[i];
+// pass 2 (parallel, one CTA per 128-request chunk): with a* known, per chunk
+// and group the smallest tokens() of alpha == +0.0 and alpha == a* requests and
+// the count of other alphas.  A chunk can hold a placement only if one of its
+// minima fits the current largest free capacity F0 / Fa (exact for those
+// classes), so the group's warp skips every other chunk.
+__global__ void k_chunk_stats(const pyg_reservation* req, const int32_t* group, int R, int G,
+                              GroupStat* gs, int64_t* cmin0, int64_t* cmin1, int32_t* cother,
+                              int64_t* smin0, int64_t* smin1, int32_t* sother, int64_t* rt,
+                              int32_t* rcls) {
+  extern __shared__ int64_t sh64[];  // [2G] minima, then [G] int32 counts
+  int32_t* shc = reinterpret_cast<int32_t*>(sh64 + 2 * G);
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    sh64[g] = INT64_MAX;
+    sh64[G + g] = INT64_MAX;
+    shc[g] = 0;
+  }
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) {
+    const int g = group[r];
+    const pyg_reservation q = req[r];
+    const int64_t t = res_tokens(q.prompt_len, q.upper, q.tokens_generated);
     const int32_t f = gs[g].first_nz;
-    if (same_bits(v.alpha, 0.0))
-      m0 = v.t;
-    else if (same_bits(v.alpha, in[f].alpha))
-      m1 = v.t;
-    else
-      other = 1;
+    int cls;
+    if (same_bits(q.alpha, 0.0)) {
+      cls = 0;
+      atomicMin(reinterpret_cast<long long*>(&sh64[g]), t);
+    } else if (f != INT32_MAX && same_bits(q.alpha, req[f].alpha)) {
+      cls = 1;
+      atomicMin(reinterpret_cast<long long*>(&sh64[G + g]), t);
+    } else {
+      cls = 2;
+      atomicAdd(&shc[g], 1);
+    }
+    rt[r] = t;
+    rcls[r] = (g << 2) | cls;  // group and alpha class of the request
   }
-  auto mn = [](int64_t a, int64_t b) { return a < b ? a : b; };
-  m0 = seg_reduce(m0, g, lane, mn);
-  m1 = seg_reduce(m1, g, lane, mn);
-  other = seg_reduce(other, g, lane, [](int32_t a, int32_t b) { return a + b; });
-  if (ok && seg_head(g, lane)) {
-    if (m0 != INT64_MAX) atomicMin(reinterpret_cast<long long*>(&gs[g].min_t0), m0);
-    if (m1 != INT64_MAX) atomicMin(reinterpret_cast<long long*>(&gs[g].min_t1), m1);
-    if (other) atomicAdd(&gs[g].n_other, other);
+  __syncthreads();
+  const int sup = blockIdx.x / 32;  // level-2 summary: 32 chunks
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    const size_t k = static_cast<size_t>(blockIdx.x) * G + g;
+    const size_t k2 = static_cast<size_t>(sup) * G + g;
+    cmin0[k] = sh64[g];
+    cmin1[k] = sh64[G + g];
+    cother[k] = shc[g];
+    if (shc[g]) {
+      atomicAdd(&gs[g].n_other, shc[g]);
+      atomicAdd(&sother[k2], shc[g]);
+    }
+    if (sh64[g] != INT64_MAX) atomicMin(reinterpret_cast<long long*>(&smin0[k2]), sh64[g]);
+    if (sh64[G + g] != INT64_MAX) atomicMin(reinterpret_cast<long long*>(&smin1[k2]), sh64[G + g]);
   }
 }
 
-__global__ void k_gs_init(GroupStat* gs, int G) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < G) gs[g] = GroupStat{0, 0, INT32_MAX, 0, INT64_MAX, INT64_MAX};
+__global__ void k_super_init(int64_t* smin0, int64_t* smin1, int32_t* sother, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    smin0[i] = INT64_MAX;
+    smin1[i] = INT64_MAX;
+    sother[i] = 0;
+  }
+}
+
+// group list offsets (exclusive scan of counts); tiny
+__global__ void k_group_off(const GroupStat* gs, int G, int32_t* goff) {
+  if (threadIdx.x || blockIdx.x) return;
+  int32_t a = 0;
+  for (int g = 0; g < G; ++g) {
+    goff[g] = a;
+    a += gs[g].count;
+  }
+  goff[G] = a;
 }
 
 struct SeqArgs {
@@ -218,12 +248,29 @@ struct SeqArgs {
   int max_cand;
   const int32_t* staged;
   double eps;
-  const int32_t* order;
-  const SeqIn* in;
-  const GroupStat* gs;
+  const pyg_reservation* req;
+  const int32_t* group;
+  int R;
+  GroupStat* gs;
+  const int32_t* goff;
+  int32_t* glist;   // placements per group, in order: request index
+  int32_t* rcount;  // placements per replica
+  const int64_t* cmin0;  // [nchunks][G] chunk summaries (k_chunk_stats)
+  const int64_t* cmin1;
+  const int32_t* cother;
+  const int64_t* smin0;  // [nchunks/32][G] level-2 summaries
+  const int64_t* smin1;
+  const int32_t* sother;
+  const int64_t* rt;     // [R] tokens()
+  const int32_t* rcls;   // [R] group << 2 | alpha class
+  int G;
   pyg_decision* out;
   int32_t* t_idx;
 };
+
+constexpr int kPer = 4;                 // requests per lane per scan step
+constexpr int kScan = 32 * kPer;        // requests per scan step
+constexpr int kStagedCache = 16;        // staged row entries cached in smem per request
 
 __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
   __shared__ int64_t s_free[kMaxSeqCand];
@@ -231,26 +278,29 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
   __shared__ double s_ba[kMaxSeqCand];
   __shared__ int32_t s_rid[kMaxSeqCand];
   __shared__ int32_t s_node[kMaxSeqCand];
+  __shared__ int32_t s_cnt[kMaxSeqCand];
+  __shared__ __align__(16) int32_t s_stg[kScan][kStagedCache];
   const int g = blockIdx.x;
   const int lane = threadIdx.x;
   const int c0 = A.cand_off[g], nc = min(A.cand_off[g + 1] - c0, kMaxSeqCand);
   const GroupStat st = A.gs[g];
-  const int i0 = st.start, i1 = st.end;
-  if (i1 <= i0) return;
+  if (st.count == 0) return;
   for (int j = lane; j < nc; j += 32) {
     const int n = A.cand[c0 + j];
     s_node[j] = n;
     s_free[j] = A.ns.free_[n];
     s_b0[j] = A.ns.b0[n];
     s_rid[j] = A.nodes.replica_id[n];
+    s_cnt[j] = 0;
   }
   __syncwarp();
   const bool have_star = st.first_nz != INT32_MAX;
-  const double astar = have_star ? A.in[st.first_nz].alpha : 0.0;
+  const double astar = have_star ? A.req[st.first_nz].alpha : 0.0;
   if (have_star) {
     for (int j = lane; j < nc; j += 32) s_ba[j] = bound_loop(A.nodes, A.ns, s_node[j], astar);
     __syncwarp();
   }
+  const bool cache_staged = A.max_cand <= kStagedCache && (A.max_cand % 4) == 0;
   int64_t F0 = INT64_MIN, Fa = INT64_MIN;
   auto refresh = [&]() {
     int64_t f0 = INT64_MIN, fa = INT64_MIN;
@@ -258,108 +308,217 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
       if (!(s_b0[j] > A.eps)) f0 = max(f0, s_free[j]);
       if (have_star && !(s_ba[j] > A.eps)) fa = max(fa, s_free[j]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      f0 = max(f0, __shfl_xor_sync(kFull, f0, o));
-      fa = max(fa, __shfl_xor_sync(kFull, fa, o));
-    }
-    F0 = f0;
-    Fa = fa;
+    F0 = redux_max_i64(f0);
+    Fa = redux_max_i64(fa);
   };
   refresh();
-  // bound of node slot j for request alpha al (class 0: +0.0, 1: a*, 2: other)
   auto bound_of = [&](int j, int cls, double al) -> double {
     if (cls == 0) return s_b0[j];
     if (cls == 1) return s_ba[j];
     return bound_loop(A.nodes, A.ns, s_node[j], al);
   };
-  // once no remaining request of any class can fit anywhere, the rest wait
-  auto saturated = [&]() {
-    return st.n_other == 0 && F0 < st.min_t0 && (!have_star || Fa < st.min_t1);
-  };
-  constexpr int kPer = 4;
-  for (int base = i0; base < i1 && !saturated(); base += 32 * kPer) {
-    SeqIn v[kPer];
-    int cls[kPer];
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int i = base + lane * kPer + u;
-      v[u] = i < i1 ? A.in[i] : SeqIn{INT64_MAX, 0.0};
+  int32_t nplaced = 0;
+  const int32_t lbase = A.goff[g];
+  const int nchunks = (A.R + kScan - 1) / kScan;
+  int next = 0;
+  for (;;) {
+    // next chunk that can hold a placement under the current state: level-2 summaries
+    // (32 chunks each) first, then the 32 chunks of the first promising super-chunk
+    int found = -1;
+    auto pot = [&](const int64_t* m0, const int64_t* m1, const int32_t* ot, size_t e) {
+      return ot[e] > 0 || m0[e] <= F0 || (have_star && m1[e] <= Fa);
+    };
+    const int nsup = (nchunks + 31) / 32;
+    for (int sb = next / 32; sb < nsup && found < 0; sb += 32) {
+      const int k2 = sb + lane;
+      const bool p2 = k2 < nsup && pot(A.smin0, A.smin1, A.sother, static_cast<size_t>(k2) * A.G + g);
+      unsigned m2 = __ballot_sync(kFull, p2);
+      while (m2 && found < 0) {
+        const int sc = sb + __ffs(m2) - 1;
+        m2 &= m2 - 1;
+        const int k = sc * 32 + lane;
+        const bool p = k >= next && k < nchunks &&
+                       pot(A.cmin0, A.cmin1, A.cother, static_cast<size_t>(k) * A.G + g);
+        const unsigned m = __ballot_sync(kFull, p);
+        if (m) found = sc * 32 + __ffs(m) - 1;
+      }
     }
-    int done = base - 1;  // positions <= done are decided
+    if (found < 0) break;  // no later request of this group can be placed: all wait
+    next = found + 1;
+    const int base = found * kScan;
+    int64_t t[kPer];
+    bool mine[kPer];
+    int cl4[kPer];
+    {
+      const int r0 = base + lane * kPer;
+      int32_t cc[kPer];
+      int64_t tt4[kPer];
+      if (r0 + kPer <= A.R) {
+        const int4 c4 = *reinterpret_cast<const int4*>(A.rcls + r0);
+        const longlong2 ta = *reinterpret_cast<const longlong2*>(A.rt + r0);
+        const longlong2 tb = *reinterpret_cast<const longlong2*>(A.rt + r0 + 2);
+        cc[0] = c4.x; cc[1] = c4.y; cc[2] = c4.z; cc[3] = c4.w;
+        tt4[0] = ta.x; tt4[1] = ta.y; tt4[2] = tb.x; tt4[3] = tb.y;
+      } else {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          cc[u] = r0 + u < A.R ? A.rcls[r0 + u] : -1;
+          tt4[u] = r0 + u < A.R ? A.rt[r0 + u] : INT64_MAX;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        mine[u] = cc[u] >= 0 && (cc[u] >> 2) == g;
+        cl4[u] = cc[u] & 3;
+        t[u] = mine[u] ? tt4[u] : INT64_MAX;
+      }
+    }
+    if (cache_staged) {  // stage the chunk's staged rows (16 B vectors) into shared memory
+      for (int e = lane; e < kScan * (kStagedCache / 4); e += 32) {
+        const int rr = e / (kStagedCache / 4), v4 = e % (kStagedCache / 4);
+        const int r = base + rr;
+        int4 x = make_int4(0, 0, 0, 0);
+        if (r < A.R && 4 * v4 < A.max_cand)
+          x = *reinterpret_cast<const int4*>(A.staged + static_cast<int64_t>(r) * A.max_cand + 4 * v4);
+        *reinterpret_cast<int4*>(&s_stg[rr][4 * v4]) = x;
+      }
+      __syncwarp();
+    }
+    int done = base - 1;
     for (;;) {
-      // first position > done whose request could be placed under the current state
       int first = INT32_MAX;
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int i = base + lane * kPer + u;
-        if (i <= done || i >= i1) continue;
-        const bool nz = !same_bits(v[u].alpha, 0.0);
-        cls[u] = !nz ? 0 : (same_bits(v[u].alpha, astar) ? 1 : 2);
-        const bool could = cls[u] == 0 ? v[u].t <= F0 : (cls[u] == 1 ? v[u].t <= Fa : true);
-        if (could) first = min(first, i);
+        const int r = base + lane * kPer + u;
+        if (!mine[u] || r <= done) continue;
+        const int cls = cl4[u];
+        const bool could = cls == 0 ? t[u] <= F0 : (cls == 1 ? t[u] <= Fa : true);
+        if (could) first = min(first, r);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(kFull, first, o));
+      first = __reduce_min_sync(kFull, first);
       if (first == INT32_MAX) break;
-      // fetch the request at `first`
       const int owner = (first - base) / kPer, uu = (first - base) % kPer;
-      int64_t t = 0;
-      double al = 0.0;
+      int64_t tt = 0;
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        if (u == uu) {
-          t = __shfl_sync(kFull, v[u].t, owner);
-          al = __shfl_sync(kFull, v[u].alpha, owner);
-        }
-      }
-      const int cl = same_bits(al, 0.0) ? 0 : (same_bits(al, astar) ? 1 : 2);
-      const int r = A.order[first];
-      // full sched::route over the group's candidates (router.cpp:24-43)
+      for (int u = 0; u < kPer; ++u)
+        if (u == uu) tt = __shfl_sync(kFull, t[u], owner);
+      int cl = 0;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (u == uu) cl = __shfl_sync(kFull, cl4[u], owner);
+      // classes 0 / 1 are bit-identical to +0.0 / a*; only "other" alphas are fetched
+      const double a = cl == 0 ? 0.0 : (cl == 1 ? astar : A.req[first].alpha);
+      auto staged_of = [&](int j) -> int32_t {
+        return cache_staged ? s_stg[first - base][j]
+                            : A.staged[static_cast<int64_t>(first) * A.max_cand + j];
+      };
+      // full sched::route over the group's candidates (router.cpp:24-43): the
+      // reference's strict lexicographic running max on (headroom, staged, -replica_id) in
+      // input order == argmax of (h, s, -id, -pos); tiebreak <=> first position with
+      // headroom H precedes the first with (H, S)
       RouteAcc best{0, 0, 0, -1};
       for (int j = lane; j < nc; j += 32) {
         const int64_t fr = s_free[j];
-        if (t > fr) continue;
-        if (bound_of(j, cl, al) > A.eps) continue;
-        RouteAcc a{fr - t, A.staged[static_cast<int64_t>(r) * A.max_cand + j], s_rid[j], j};
-        if (acc_better(a, best)) best = a;
+        if (tt > fr) continue;
+        if (bound_of(j, cl, a) > A.eps) continue;
+        RouteAcc x{fr - tt, staged_of(j), s_rid[j], j};
+        if (acc_better(x, best)) best = x;
       }
-      best = warp_best(best);
+      const int64_t H = redux_max_i64(best.pos >= 0 ? best.h : INT64_MIN);
+      if (H != INT64_MIN) {
+        const bool onH = best.pos >= 0 && best.h == H;
+        const int64_t S = redux_max_i64(onH ? best.s : INT64_MIN);
+        const bool onS = onH && best.s == S;
+        const int32_t ID = __reduce_min_sync(kFull, onS ? best.id : INT32_MAX);
+        const int32_t POS = __reduce_min_sync(kFull, onS && best.id == ID ? best.pos : INT32_MAX);
+        best = RouteAcc{H, S, ID, POS};
+      } else {
+        best.pos = -1;
+      }
       if (best.pos >= 0) {
         int32_t p1 = 0x7fffffff, p2 = 0x7fffffff;
         for (int j = lane; j < nc; j += 32) {
           const int64_t fr = s_free[j];
-          if (t > fr || fr - t != best.h) continue;
-          if (bound_of(j, cl, al) > A.eps) continue;
+          if (tt > fr || fr - tt != best.h) continue;
+          if (bound_of(j, cl, a) > A.eps) continue;
           p1 = min(p1, j);
-          if (A.staged[static_cast<int64_t>(r) * A.max_cand + j] == best.s) p2 = min(p2, j);
+          if (staged_of(j) == best.s) p2 = min(p2, j);
         }
-        p1 = warp_min_i32(p1);
-        p2 = warp_min_i32(p2);
+        p1 = __reduce_min_sync(kFull, p1);
+        p2 = __reduce_min_sync(kFull, p2);
         const int w = best.pos;
         if (lane == 0) {
-          A.out[r] = pyg_decision{best.id, p1 < p2 ? 1 : 0, best.h, bound_of(w, cl, al)};
+          A.out[first] = pyg_decision{best.id, p1 < p2 ? 1 : 0, best.h, bound_of(w, cl, a)};
           const int n = s_node[w];
-          A.t_idx[r] = n;
-          // commit: the placement joins the node's pool (engine.cpp:686); oom_bound appends its
-          // alpha last (router.cpp:15)
-          s_free[w] -= t;
-          s_b0[w] += al;
-          if (have_star) s_ba[w] += al;
-          A.ns.app_alpha[first] = al;
-          A.ns.app_next[first] = -1;
-          if (A.ns.tail[n] >= 0)
-            A.ns.app_next[A.ns.tail[n]] = first;
-          else
-            A.ns.head[n] = first;
-          A.ns.tail[n] = first;
+          A.t_idx[first] = n;
+          A.glist[lbase + nplaced] = first;
+          s_cnt[w] += 1;
+          // commit: the placement joins the node's pool (engine.cpp:686); oom_bound appends
+          // its alpha last (router.cpp:15)
+          s_free[w] -= tt;
+          s_b0[w] += a;
+          if (have_star) s_ba[w] += a;
+          if (st.n_other) {  // "other" alphas need the full ordered list
+            A.ns.app_alpha[first] = a;
+            A.ns.app_next[first] = -1;
+            if (A.ns.tail[n] >= 0)
+              A.ns.app_next[A.ns.tail[n]] = first;
+            else
+              A.ns.head[n] = first;
+            A.ns.tail[n] = first;
+          }
         }
+        ++nplaced;
         __syncwarp();
         __threadfence_block();
         refresh();
       }
       done = first;
     }
+    __syncwarp();
+  }
+  __syncwarp();
+  for (int j = lane; j < nc; j += 32) A.rcount[s_node[j]] = s_cnt[j];
+  if (lane == 0) A.gs[g].nplaced = nplaced;
+}
+
+// placed_off = exclusive scan of per-replica placement counts (one CTA)
+__global__ void k_rep_off(const int32_t* rcount, int n, int32_t* off) {
+  __shared__ int64_t sm[64];
+  int64_t carry = 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int64_t v = i < n ? rcount[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_exscan(v, sm, &tot);
+    if (i < n) off[i] = static_cast<int32_t>(carry + ex);
+    carry += tot;
+  }
+  if (threadIdx.x == 0) off[n] = static_cast<int32_t>(carry);
+}
+
+// per-replica lists in placement (= request) order, from each group's list; one warp per group
+__global__ void k_rep_fill(const GroupStat* gs, const int32_t* goff, const int32_t* glist,
+                           const int32_t* t_idx, const int32_t* off, int32_t* rcur,
+                           int32_t* placed) {
+  const int g = blockIdx.x, lane = threadIdx.x;
+  const int np = gs[g].nplaced;
+  for (int b = 0; b < np; b += 32) {
+    const int k = b + lane;
+    const bool ok = k < np;
+    const int r = ok ? glist[goff[g] + k] : 0;
+    const int n = ok ? t_idx[r] : -1;
+    const unsigned act = __ballot_sync(kFull, ok);
+    const unsigned grp = __match_any_sync(kFull, n) & act;
+    const int rank = __popc(grp & lanemask_lt());
+    int pos = 0;
+    if (ok) pos = off[n] + rcur[n] + rank;
+    __syncwarp();
+    if (ok) {
+      placed[pos] = r;
+      if (rank == 0) rcur[n] += __popc(grp);
+    }
+    __syncwarp();
   }
 }
 
@@ -426,14 +585,15 @@ extern "C" int pyg_route_batch_dev(pyg_ctx* c, int32_t mode, const pyg_nodes_dev
     set_error("SEQ_COMMIT supports at most 1024 candidates per group");
     return PYG_ENOTSUP;
   }
+  if (mode == PYG_ROUTE_SEQ_COMMIT && G > 1024) {
+    set_error("SEQ_COMMIT supports at most 1024 candidate groups");
+    return PYG_ENOTSUP;
+  }
+  const int nchunk = (std::max(R, 1) + kScan - 1) / kScan;
+  const int nsup = (nchunk + 31) / 32;
   const int n = c->n_rep;
-  size_t tmp1 = 0, tmp2 = 0;
-  const int gbits = bits_for(G), rbits = bits_for(n + 1);
-  PYG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp1, static_cast<uint32_t*>(nullptr),
-                                           static_cast<uint32_t*>(nullptr),
-                                           static_cast<int32_t*>(nullptr),
-                                           static_cast<int32_t*>(nullptr), R, 0, gbits,
-                                           c->stream));
+  size_t tmp2 = 0;
+  const int rbits = bits_for(n + 1);
   PYG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, static_cast<uint32_t*>(nullptr),
                                            static_cast<uint32_t*>(nullptr),
                                            static_cast<int32_t*>(nullptr),
@@ -441,9 +601,13 @@ extern "C" int pyg_route_batch_dev(pyg_ctx* c, int32_t mode, const pyg_nodes_dev
                                            c->stream));
   auto al = [](size_t x) { return (x + 255) & ~size_t{255}; };
   const size_t Rn = static_cast<size_t>(std::max(R, 1));
-  const size_t bytes = al(n * 8) + al(n * 8) + al(Rn * 8) + al(Rn * 4) + 2 * al(n * 4) +
-                       al(Rn * 4) + 4 * al(Rn * 4) + al(Rn * sizeof(SeqIn)) + al((G + 1) * sizeof(GroupStat)) +
-                       al(std::max(tmp1, tmp2)) + 256;
+  const size_t Nn = static_cast<size_t>(std::max(n, 1));
+  const size_t bytes = 2 * al(Nn * 8) + al(Rn * 8) + al(Rn * 4) + 4 * al(Nn * 4) + al(Rn * 4) +
+                       4 * al(Rn * 4) + al((G + 1) * sizeof(GroupStat)) + al((G + 1) * 4) +
+                       al(Rn * 4) + al(tmp2) + 2 * al(static_cast<size_t>(nchunk) * G * 8) +
+                       al(static_cast<size_t>(nchunk) * G * 4) +
+                       2 * al(static_cast<size_t>(nsup) * G * 8) + al(static_cast<size_t>(nsup) * G * 4) +
+                       al(Rn * 8) + al(Rn * 4) + 1024;
   void* sp;
   int rc = scratch(c, bytes, &sp);
   if (rc) return rc;
@@ -454,63 +618,86 @@ extern "C" int pyg_route_batch_dev(pyg_ctx* c, int32_t mode, const pyg_nodes_dev
     return q;
   };
   NodeScratch ns;
-  ns.free_ = reinterpret_cast<int64_t*>(take(n * 8));
-  ns.b0 = reinterpret_cast<double*>(take(n * 8));
+  ns.free_ = reinterpret_cast<int64_t*>(take(Nn * 8));
+  ns.b0 = reinterpret_cast<double*>(take(Nn * 8));
   ns.app_alpha = reinterpret_cast<double*>(take(Rn * 8));
   ns.app_next = reinterpret_cast<int32_t*>(take(Rn * 4));
-  ns.head = reinterpret_cast<int32_t*>(take(n * 4));
-  ns.tail = reinterpret_cast<int32_t*>(take(n * 4));
+  ns.head = reinterpret_cast<int32_t*>(take(Nn * 4));
+  ns.tail = reinterpret_cast<int32_t*>(take(Nn * 4));
+  auto* rcount = reinterpret_cast<int32_t*>(take(Nn * 4));
+  auto* rcur = reinterpret_cast<int32_t*>(take(Nn * 4));
   auto* t_idx = reinterpret_cast<int32_t*>(take(Rn * 4));
   auto* k_in = reinterpret_cast<uint32_t*>(take(Rn * 4));
   auto* k_out = reinterpret_cast<uint32_t*>(take(Rn * 4));
   auto* v_in = reinterpret_cast<int32_t*>(take(Rn * 4));
   auto* v_out = reinterpret_cast<int32_t*>(take(Rn * 4));
-  auto* sin = reinterpret_cast<SeqIn*>(take(Rn * sizeof(SeqIn)));
   auto* gs = reinterpret_cast<GroupStat*>(take((G + 1) * sizeof(GroupStat)));
-  void* d_tmp = take(std::max(tmp1, tmp2));
+  auto* goff = reinterpret_cast<int32_t*>(take((G + 1) * 4));
+  auto* glist = reinterpret_cast<int32_t*>(take(Rn * 4));
+  void* d_tmp = take(tmp2);
+  auto* cmin0 = reinterpret_cast<int64_t*>(take(static_cast<size_t>(nchunk) * G * 8));
+  auto* cmin1 = reinterpret_cast<int64_t*>(take(static_cast<size_t>(nchunk) * G * 8));
+  auto* cother = reinterpret_cast<int32_t*>(take(static_cast<size_t>(nchunk) * G * 4));
+  auto* smin0 = reinterpret_cast<int64_t*>(take(static_cast<size_t>(nsup) * G * 8));
+  auto* smin1 = reinterpret_cast<int64_t*>(take(static_cast<size_t>(nsup) * G * 8));
+  auto* sother = reinterpret_cast<int32_t*>(take(static_cast<size_t>(nsup) * G * 4));
+  auto* rt = reinterpret_cast<int64_t*>(take(Rn * 8));
+  auto* rcls = reinterpret_cast<int32_t*>(take(Rn * 4));
   if (n) {
     k_node_prep<<<(n + 127) / 128, 128, 0, c->stream>>>(n, *nodes, ns);
     PYG_LAUNCHED(c);
   }
-  if (R) {
-    if (mode == PYG_ROUTE_SNAPSHOT) {
+  if (mode == PYG_ROUTE_SNAPSHOT) {
+    if (R) {
       k_route_snapshot<<<(R + 7) / 8, 256, 0, c->stream>>>(*nodes, ns, d_cand_off, d_cand,
                                                            max_cand, d_staged, eps, d_req,
                                                            d_group, R, d_out, t_idx);
       PYG_LAUNCHED(c);
-    } else {
-      // stable partition by group
-      k_iota_key<<<(R + 255) / 256, 256, 0, c->stream>>>(d_group, R, 0, k_in, v_in);
-      PYG_LAUNCHED(c);
-      PYG_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp1, k_in, k_out, v_in, v_out, R, 0, gbits,
-                                               c->stream));
-      PYG_LAUNCHED(c);
-      k_gs_init<<<(G + 127) / 128, 128, 0, c->stream>>>(gs, G);
-      PYG_LAUNCHED(c);
-      k_seq_prep<<<(R + 255) / 256, 256, 0, c->stream>>>(d_req, v_out, k_out, R, sin, gs, d_out,
-                                                         t_idx);
-      PYG_LAUNCHED(c);
-      k_seq_classes<<<(R + 255) / 256, 256, 0, c->stream>>>(sin, k_out, R, gs);
-      PYG_LAUNCHED(c);
-      SeqArgs a{*nodes, ns, d_cand_off, d_cand, max_cand, d_staged, eps, v_out, sin, gs, d_out,
-                t_idx};
-      k_route_seq<<<G, 32, 0, c->stream>>>(a);
-      PYG_LAUNCHED(c);
     }
+    if (d_placed_off && d_placed && n) {
+      // stable per-replica lists: radix sort of (t_idx + 1) with values = request index
+      if (R) {
+        k_iota_key<<<(R + 255) / 256, 256, 0, c->stream>>>(t_idx, R, 1, k_in, v_in);
+        PYG_LAUNCHED(c);
+        PYG_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp2, k_in, k_out, v_in, v_out, R, 0,
+                                                 rbits, c->stream));
+        PYG_LAUNCHED(c);
+      }
+      k_placed_off<<<(n + 1 + 127) / 128, 128, 0, c->stream>>>(k_out, R, n, d_placed_off);
+      PYG_LAUNCHED(c);
+      if (R) {
+        k_placed_copy<<<(R + 255) / 256, 256, 0, c->stream>>>(k_out, v_out, R, d_placed);
+        PYG_LAUNCHED(c);
+      }
+    }
+    return PYG_OK;
+  }
+  // SEQ_COMMIT
+  const int ginit = std::max(G, n);
+  k_gs_init<<<(ginit + 127) / 128 + 1, 128, 0, c->stream>>>(gs, G, rcount, rcur, n);
+  PYG_LAUNCHED(c);
+  if (R) {
+    k_seq_stats1<<<(R + 255) / 256, 256, 2 * G * sizeof(int32_t), c->stream>>>(
+        d_req, d_group, R, G, gs, d_out, t_idx);
+    PYG_LAUNCHED(c);
+    k_super_init<<<(nsup * G + 255) / 256, 256, 0, c->stream>>>(smin0, smin1, sother, nsup * G);
+    PYG_LAUNCHED(c);
+    k_chunk_stats<<<nchunk, kScan, 2 * G * sizeof(int64_t) + G * sizeof(int32_t), c->stream>>>(
+        d_req, d_group, R, G, gs, cmin0, cmin1, cother, smin0, smin1, sother, rt, rcls);
+    PYG_LAUNCHED(c);
+    k_group_off<<<1, 1, 0, c->stream>>>(gs, G, goff);
+    PYG_LAUNCHED(c);
+    SeqArgs a{*nodes, ns,  d_cand_off, d_cand, max_cand, d_staged, eps,   d_req,  d_group, R,
+              gs,     goff, glist,     rcount, cmin0,    cmin1,    cother, smin0, smin1, sother,
+              rt,     rcls, G,         d_out,  t_idx};
+    k_route_seq<<<G, 32, 0, c->stream>>>(a);
+    PYG_LAUNCHED(c);
   }
   if (d_placed_off && d_placed && n) {
-    // stable per-replica lists: sort (t_idx + 1) with values = request index
-    if (R) {
-      k_iota_key<<<(R + 255) / 256, 256, 0, c->stream>>>(t_idx, R, 1, k_in, v_in);
-      PYG_LAUNCHED(c);
-      PYG_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp2, k_in, k_out, v_in, v_out, R, 0, rbits,
-                                               c->stream));
-      PYG_LAUNCHED(c);
-    }
-    k_placed_off<<<(n + 1 + 127) / 128, 128, 0, c->stream>>>(k_out, R, n, d_placed_off);
+    k_rep_off<<<1, 1024, 0, c->stream>>>(rcount, n, d_placed_off);
     PYG_LAUNCHED(c);
-    if (R) {
-      k_placed_copy<<<(R + 255) / 256, 256, 0, c->stream>>>(k_out, v_out, R, d_placed);
+    if (R && G) {
+      k_rep_fill<<<G, 32, 0, c->stream>>>(gs, goff, glist, t_idx, d_placed_off, rcur, d_placed);
       PYG_LAUNCHED(c);
     }
   }
