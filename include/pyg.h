@@ -182,12 +182,26 @@ int pyg_hash_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_
                        int32_t n_req, const int64_t* d_hash_off, uint64_t* d_hashes);
 
 /* K2: staged matrix.  For request r and its j-th candidate replica cand[cand_off[g_r]+j]
-   (g_r = d_group[r]), d_staged[r*max_cand + j] = tier(L2).matched_prefix(prompt_r)
-   == lookup(prompt, nullptr).l2 as node_view computes it (engine.cpp:646). */
+   (g_r = d_group[r] < n_groups), d_staged[r*max_cand + j] = tier(L2).matched_prefix(prompt_r)
+   == lookup(prompt, nullptr).l2 as node_view computes it (engine.cpp:640-648).  Computed with
+   one walk per request through the L2 directory (every candidate at once); candidates are
+   global replica indices (== this ctx's replica indices unless pyg_set_shard was called) and
+   must be distinct within a group.  A single-GPU ctx rebuilds a stale directory here. */
 int pyg_staged_matrix_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
                           const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t n_req,
-                          const int32_t* d_group, const int32_t* d_cand_off,
+                          const int32_t* d_group, int32_t n_groups, const int32_t* d_cand_off,
                           const int32_t* d_cand, int32_t max_cand, int32_t* d_staged);
+
+/* ------------------------------------------------------- L2 directory / shards */
+/* This ctx holds global replicas [rep_base, rep_base + n_replicas) of an n_global-replica
+   cluster whose replicas are spread over several ctxs (one per GPU). */
+int pyg_set_shard(pyg_ctx* ctx, int32_t rep_base, int32_t n_global);
+/* Records (40 B each: hash, parent, span_start, span_end, global replica, flags) of every
+   alive L2 block of this ctx; cap from pyg_dir_export_cap.  *n_out = count. */
+int64_t pyg_dir_export_cap(pyg_ctx* ctx);
+int pyg_dir_export_dev(pyg_ctx* ctx, void* d_records, int64_t cap, int64_t* n_out);
+/* (Re)build the directory from the records of every shard (their concatenation). */
+int pyg_dir_build_dev(pyg_ctx* ctx, const void* d_records, int64_t n);
 
 /* K2: lookup (l1,l2,l3 matches) of request r against replica d_replica[r] (-1 = skip). */
 int pyg_lookup_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,

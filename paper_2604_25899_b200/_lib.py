@@ -102,7 +102,11 @@ _sig("pyg_check_device_error", vp)
 # batched (device pointers)
 _sig("pyg_hash_offsets_dev", vp, vp, i32, vp, vp)
 _sig("pyg_hash_batch_dev", vp, vp, vp, i32, vp, vp)
-_sig("pyg_staged_matrix_dev", vp, vp, vp, vp, vp, i32, vp, vp, vp, i32, vp)
+_sig("pyg_staged_matrix_dev", vp, vp, vp, vp, vp, i32, vp, i32, vp, vp, i32, vp)
+_sig("pyg_set_shard", vp, i32, i32)
+_sig("pyg_dir_export_cap", vp, res=i64)
+_sig("pyg_dir_export_dev", vp, vp, i64, vp)
+_sig("pyg_dir_build_dev", vp, vp, i64)
 _sig("pyg_lookup_batch_dev", vp, vp, vp, vp, vp, i32, vp, i32, vp)
 _sig("pyg_route_batch_dev", vp, i32, C.POINTER(NodesDev), vp, i32, vp, i32, vp, vp, i32, vp,
      dbl, vp, vp, vp)

@@ -147,7 +147,7 @@ def hash_batch(ctx, b: DeviceBatch):
 def staged_matrix(ctx, b: DeviceBatch, nodes: DeviceNodes, out: StepOut):
     check(_lib._lib.pyg_staged_matrix_dev(ctx.h, _ptr(b.tokens), _ptr(b.tok_off),
                                           _ptr(b.hash_off), _ptr(b.hashes), b.R, _ptr(b.group),
-                                          _ptr(nodes.cand_off), _ptr(nodes.cand),
+                                          nodes.n_groups, _ptr(nodes.cand_off), _ptr(nodes.cand),
                                           nodes.max_cand, _ptr(out.staged)))
 
 

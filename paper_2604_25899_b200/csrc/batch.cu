@@ -20,34 +20,7 @@ using namespace pyg_host;
 namespace {
 
 // ------------------------------------------------------------------- K2
-// staged[r][j] = tier(L2 of candidate j).matched_prefix(prompt_r)
-// (node_view: rep.cache.lookup(r.prompt, nullptr).l2, engine.cpp:646).
-// One thread per (request, candidate).
-__global__ void k_staged(CtxDev c, const uint64_t* __restrict__ tokens,
-                         const int64_t* __restrict__ tok_off, const int64_t* __restrict__ hash_off,
-                         const uint64_t* __restrict__ hashes, int R, const int32_t* group,
-                         const int32_t* cand_off, const int32_t* cand, int max_cand,
-                         int32_t* staged) {
-  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= static_cast<int64_t>(R) * max_cand) return;
-  const int r = static_cast<int>(x / max_cand);
-  const int j = static_cast<int>(x % max_cand);
-  const int g = group[r];
-  const int nc = cand_off[g + 1] - cand_off[g];
-  if (j >= nc) {
-    staged[x] = 0;
-    return;
-  }
-  const int rep = cand[cand_off[g] + j];
-  const TierDev& t = c.tiers[2 * rep + 1];
-  const int64_t L = tok_off[r + 1] - tok_off[r];
-  const uint64_t* hs = hashes + hash_off[r];
-  const int64_t nh = hash_off[r + 1] - hash_off[r];
-  const int64_t kb = thread_walk(t, hs, nh);
-  const int64_t m = kb ? matched_from_blocks(kb, L, c.B) : 0;
-  staged[x] = static_cast<int32_t>(ragged_extend(t, t.log, tokens + tok_off[r], L, hs, m, c.B));
-}
-
+// (the staged matrix is k_dir.cu: one directory walk per request)
 // CacheHierarchy::lookup (hierarchy.cpp:109-117) of request r on replica rep[r].
 __global__ void k_lookup_batch(CtxDev c, const uint64_t* __restrict__ tokens,
                                const int64_t* __restrict__ tok_off,
@@ -96,7 +69,8 @@ __device__ int64_t block_walk(const TierDev& t, const uint64_t* hashes, int64_t 
 
 // Erase a present, unpinned block by key; safe under concurrent claims of the
 // same key (the slot CAS decides).  Returns the freed size (0 if not erased).
-__device__ __forceinline__ int64_t erase_claim(const TierDev& t, uint64_t key) {
+__device__ __forceinline__ int64_t erase_claim(const TierDev& t, uint64_t key,
+                                               int64_t* li = nullptr) {
   const int64_t sl = idx_find_slot(t, key);
   if (sl < 0) return -1;
   unsigned long long* pv = reinterpret_cast<unsigned long long*>(&t.idx[sl].val);
@@ -106,6 +80,7 @@ __device__ __forceinline__ int64_t erase_claim(const TierDev& t, uint64_t key) {
   if (b.pin > 0) return -1;
   if (atomicCAS(pv, v, static_cast<unsigned long long>(kTomb)) != v) return -1;
   b.flags &= ~kAlive;
+  if (li) *li = static_cast<int64_t>(v - 1);
   return b.e - b.s;
 }
 
@@ -200,10 +175,12 @@ __global__ void __launch_bounds__(512) k_admit(CtxDev c, AdmitArgs a) {
       for (int64_t i = threadIdx.x; i < nh; i += blockDim.x) {
         const int64_t e = min((i + 1) * c.B, L);
         if (e <= m[0] || e > m[0] + l2_part) continue;
-        const int64_t sz = erase_claim(t2, hs[i]);
+        int64_t li;
+        const int64_t sz = erase_claim(t2, hs[i], &li);
         if (sz >= 0) {
           freed += sz;
           cnt += 1;
+          dir_note_erase(c, t2.log[li], rep);
         }
       }
       int64_t ft, ct;
@@ -323,20 +300,6 @@ int pyg_check_device_error(pyg_ctx* c) {
   return PYG_OK;
 }
 
-int pyg_staged_matrix_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
-                          const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t R,
-                          const int32_t* d_group, const int32_t* d_cand_off,
-                          const int32_t* d_cand, int32_t max_cand, int32_t* d_staged) {
-  if (!c || R < 0 || max_cand < 0) return PYG_EINVAL;
-  const int64_t n = static_cast<int64_t>(R) * max_cand;
-  if (n == 0) return PYG_OK;
-  k_staged<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(
-      c->hd, d_tokens, d_tok_off, d_hash_off, d_hashes, R, d_group, d_cand_off, d_cand, max_cand,
-      d_staged);
-  PYG_LAUNCHED(c);
-  return PYG_OK;
-}
-
 int pyg_lookup_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
                          const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t R,
                          const int32_t* d_rep, int32_t with_l3, int64_t* d_match3) {
@@ -366,6 +329,7 @@ int pyg_admit_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_t
   const size_t smem = kSmemSortCap * 12;
   cudaFuncSetAttribute(k_admit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_admit<<<c->n_rep, 512, smem, c->stream>>>(c->hd, a);
+  c->dir_admits += 1;
   PYG_LAUNCHED(c);
   k_l3_erase<<<(R + 7) / 8, 256, 0, c->stream>>>(c->hd, d_tok_off, d_hash_off, d_hashes, R,
                                                  d_admitted, l3span);
@@ -463,7 +427,8 @@ extern "C" int pyg_step_host(pyg_ctx* c, const pyg_batch_host* b, const pyg_node
   auto* coff = reinterpret_cast<int32_t*>(d + o_coff);
   auto* cand = reinterpret_cast<int32_t*>(d + o_cand);
   auto* stg = reinterpret_cast<int32_t*>(d + o_stg);
-  if ((rc = pyg_staged_matrix_dev(c, tok, toff, hoff, hash, R, grp, coff, cand, max_cand, stg)))
+  if ((rc = pyg_staged_matrix_dev(c, tok, toff, hoff, hash, R, grp, G, coff, cand, max_cand,
+                                   stg)))
     return rc;
   pyg_nodes_dev ndv{reinterpret_cast<int32_t*>(d + o_rid), reinterpret_cast<int64_t*>(d + o_kv),
                     reinterpret_cast<int64_t*>(d + o_aoff),

@@ -262,6 +262,7 @@ void pyg_destroy(pyg_ctx* c) {
   cudaFree(c->hd.reg_mask);
   cudaFree(c->d_scratch);
   cudaFree(c->d_list);
+  cudaFree(c->dir_mem);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }

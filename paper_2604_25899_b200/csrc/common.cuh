@@ -80,6 +80,12 @@ struct CtxDev {
   int32_t B;
   int32_t pad;
   int32_t* error;       // device error flag
+  // L2 directory (dir.cuh); main == nullptr until built
+  uint64_t* dir_main;
+  uint64_t* dir_rver;
+  uint64_t dir_main_mask, dir_rver_mask;
+  int32_t dir_stride;
+  int32_t rep_base;     // global index of replica 0 of this ctx
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {

@@ -9,6 +9,7 @@
 
 #include "../../include/pyg.h"
 #include "common.cuh"
+#include "dir.cuh"
 
 struct TierHost {
   pyg::TierDev d;   // host mirror of the static fields (pointers, caps)
@@ -32,6 +33,15 @@ struct pyg_ctx {
   void* d_list = nullptr;
   size_t d_list_size = 0;
   int64_t launches = 0;
+  // L2 directory (dir.cuh)
+  pyg::DirDev dir{};
+  void* dir_mem = nullptr;
+  size_t dir_mem_size = 0;
+  bool dir_dirty = true;     // an L2 tier changed outside batched admission
+  bool sharded = false;      // pyg_set_shard called: the directory spans other GPUs' replicas
+  int32_t n_global = 0;      // replicas in the cluster
+  int32_t rep_base = 0;      // global index of this ctx's replica 0
+  int64_t dir_admits = 0;    // admission calls since the last build (cleared bits accumulate)
 };
 
 namespace pyg_host {
@@ -41,6 +51,7 @@ int tier_index(pyg_ctx* c, int32_t replica, int32_t tier, bool hierarchy_level, 
 int ensure_capacity(pyg_ctx* c, int ti, int64_t k_new);
 int read_tier(pyg_ctx* c, int ti, pyg::TierDev* out);
 int scratch(pyg_ctx* c, size_t bytes, void** out);
+inline void dir_touch(pyg_ctx* c) { c->dir_dirty = true; }
 inline void count_launch(pyg_ctx* c, int n = 1) { c->launches += n; }
 }  // namespace pyg_host
 

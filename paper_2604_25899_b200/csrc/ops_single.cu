@@ -417,6 +417,7 @@ int pyg_chain_hashes(pyg_ctx* c, const uint64_t* tokens, int64_t n, uint64_t* ou
 
 int pyg_tier_put(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t hash, int64_t s, int64_t e,
                  int32_t wf, int32_t role, double now, int32_t pin, uint64_t* out_id) {
+  if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
   if (rc) return rc;
@@ -438,6 +439,7 @@ int pyg_tier_put(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t hash, int64
 }
 
 int pyg_tier_erase(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t id) {
+  if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
   if (rc) return rc;
@@ -540,6 +542,7 @@ int pyg_lookup(pyg_ctx* c, int32_t replica, const uint64_t* tokens, int64_t n, i
 
 int pyg_insert_chain(pyg_ctx* c, int32_t replica, int32_t tier, const uint64_t* tokens, int64_t n,
                      int64_t upto, int32_t wf, int32_t role, double now, int32_t pin) {
+  if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, true, &ti);
   if (rc) return rc;
@@ -571,6 +574,7 @@ int pyg_unpin_chain(pyg_ctx* c, int32_t replica, const uint64_t* tokens, int64_t
 
 int pyg_erase_chain_span(pyg_ctx* c, int32_t replica, int32_t tier, const uint64_t* tokens,
                          int64_t n, int64_t from, int64_t to) {
+  if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
   if (rc) return rc;
@@ -653,6 +657,7 @@ int pyg_registry_drop(pyg_ctx* c, int32_t wf) {
 int pyg_evict_for_space(pyg_ctx* c, int32_t replica, int32_t tier, int64_t needed,
                         int32_t speculative, uint64_t* freed, int64_t cap, int64_t* n_freed,
                         int64_t* freed_tokens, int32_t* satisfied) {
+  if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, true, &ti);
   if (rc) return rc;
@@ -737,6 +742,7 @@ static int complete_reps(pyg_ctx* c, const std::vector<int32_t>& reps, int32_t w
 
 int pyg_complete(pyg_ctx* c, int32_t replica, int32_t wf, uint64_t future, int32_t profiled,
                  double now, int64_t* n_actions) {
+  if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   if (!c || replica < 0 || replica >= c->n_rep) return PYG_EINVAL;
   if (!profiled) {  // req.unprofiled() => no actions (manager.cpp:28)
     if (n_actions) *n_actions = 0;
@@ -754,6 +760,7 @@ int pyg_l3_dead_sweep(pyg_ctx* c, int32_t wf, uint64_t future) {
 }
 
 int pyg_completion_policy(pyg_ctx* c, int32_t wf, uint64_t future, double now) {
+  if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   if (!c || wf < 0) return PYG_EINVAL;
   int rc = pyg_registry_update(c, wf, future);  // engine.cpp:1064-1065
   if (rc) return rc;
