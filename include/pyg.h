@@ -250,6 +250,34 @@ int pyg_release_batch_dev(pyg_ctx* ctx, const int64_t* d_tok_off, const int64_t*
                           const uint64_t* d_hashes, int32_t n_req, const int32_t* d_placed_off,
                           const int32_t* d_placed, const int32_t* d_admitted);
 
+/* ------------------------------------------------------ sharded step (multi-GPU) */
+/* With pyg_set_shard, pyg_route_batch_dev routes over the WHOLE cluster: the node table,
+   candidate lists and placed CSR ([n_global+1]) use global replica indices, and every shard
+   runs the same route over the all-gathered batch (bit-identical decisions everywhere).
+   Admission then runs on the owner shard only, over a local batch of the requests placed on
+   its replicas (local replica indices).  pyg_admit_shard_dev is pyg_admit_batch_dev that
+   (a) exports the L2 blocks it erases (DirRecords, so other shards clear their directory
+   bits with pyg_dir_clear_dev) and (b) does NOT erase promoted L3 spans itself but lists
+   their chain hashes: the shared L3 (hierarchy.hpp:76-85) is replicated on every shard and
+   each shard applies the union with pyg_l3_erase_hashes_dev (erasures commute).
+   d_counts[0] = L2 records written, d_counts[1] = L3 hashes written. */
+int pyg_admit_shard_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                        const int64_t* d_hash_off, const uint64_t* d_hashes,
+                        const int32_t* d_wf, const int32_t* d_role, int32_t n_req,
+                        const int32_t* d_placed_off, const int32_t* d_placed, double now,
+                        int32_t speculative, int32_t* d_admitted, int64_t* d_match3,
+                        void* d_l2_erased, int64_t l2_cap, uint64_t* d_l3_hashes, int64_t l3_cap,
+                        int64_t* d_counts);
+/* n is an upper bound; d_count (device, optional) holds the actual count (no host sync) */
+int pyg_dir_clear_dev(pyg_ctx* ctx, const void* d_records, int64_t n, const int64_t* d_count);
+int pyg_l3_erase_hashes_dev(pyg_ctx* ctx, const uint64_t* d_hashes, int64_t n,
+                            const int64_t* d_count);
+/* dst segment k = src segment idx[k] of a uint64 CSR (packing tokens/hashes of placed
+   requests for their owner shard); dst_off is the exclusive scan of the segment lengths. */
+int pyg_gather_csr_dev(pyg_ctx* ctx, const uint64_t* d_src, const int64_t* d_src_off,
+                       const int64_t* d_idx, int64_t n_idx, const int64_t* d_dst_off,
+                       uint64_t* d_dst);
+
 /* ------------------------------------------------- host-buffer batch entry */
 /* The drop-in batch call for a C++ engine: host arrays in, host arrays out.  Copies the batch
    to the device (pinned host memory is fastest), runs K1..K5 exactly as the _dev sequence

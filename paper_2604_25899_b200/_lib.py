@@ -107,6 +107,11 @@ _sig("pyg_set_shard", vp, i32, i32)
 _sig("pyg_dir_export_cap", vp, res=i64)
 _sig("pyg_dir_export_dev", vp, vp, i64, vp)
 _sig("pyg_dir_build_dev", vp, vp, i64)
+_sig("pyg_admit_shard_dev", vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, dbl, i32, vp, vp, vp, i64, vp,
+     i64, vp)
+_sig("pyg_dir_clear_dev", vp, vp, i64, vp)
+_sig("pyg_l3_erase_hashes_dev", vp, vp, i64, vp)
+_sig("pyg_gather_csr_dev", vp, vp, vp, vp, i64, vp, vp)
 _sig("pyg_lookup_batch_dev", vp, vp, vp, vp, vp, i32, vp, i32, vp)
 _sig("pyg_route_batch_dev", vp, i32, C.POINTER(NodesDev), vp, i32, vp, i32, vp, vp, i32, vp,
      dbl, vp, vp, vp)

@@ -98,6 +98,10 @@ struct AdmitArgs {
   int32_t* admitted;
   int64_t* match3;
   int64_t* l3_span;  // [2R] deferred L3 erase span per request
+  // sharded step: L2 blocks erased here are exported so every shard's directory follows
+  DirRecord* l2_out;
+  int64_t l2_cap;
+  unsigned long long* l2_count;
 };
 
 struct ChainGetB {
@@ -180,7 +184,16 @@ __global__ void __launch_bounds__(512) k_admit(CtxDev c, AdmitArgs a) {
         if (sz >= 0) {
           freed += sz;
           cnt += 1;
-          dir_note_erase(c, t2.log[li], rep);
+          const Block& eb = t2.log[li];
+          dir_note_erase(c, eb, rep);
+          if (a.l2_out) {
+            const unsigned long long k = atomicAdd(a.l2_count, 1ULL);
+            if (static_cast<int64_t>(k) < a.l2_cap)
+              a.l2_out[k] = DirRecord{eb.hash, eb.parent, eb.s, eb.e, c.rep_base + rep,
+                                      eb.flags & kOrphan};
+            else
+              atomicExch(c.error, 4);
+          }
         }
       }
       int64_t ft, ct;
@@ -225,7 +238,8 @@ __global__ void __launch_bounds__(512) k_admit(CtxDev c, AdmitArgs a) {
 // parallel; the slot CAS makes each block's erase happen once.
 __global__ void k_l3_erase(CtxDev c, const int64_t* tok_off, const int64_t* hash_off,
                            const uint64_t* hashes, int R, const int32_t* admitted,
-                           const int64_t* l3_span) {
+                           const int64_t* l3_span, uint64_t* list, int64_t list_cap,
+                           unsigned long long* list_count) {
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= R || admitted[r] != 1) return;
@@ -240,6 +254,12 @@ __global__ void k_l3_erase(CtxDev c, const int64_t* tok_off, const int64_t* hash
   for (int64_t i = lane; i < nh; i += 32) {
     const int64_t e = min((i + 1) * c.B, L);
     if (e <= from || e > to) continue;
+    if (list) {  // sharded step: the shared L3 is replicated, every shard applies the union
+      const unsigned long long k = atomicAdd(list_count, 1ULL);
+      if (static_cast<int64_t>(k) < list_cap) list[k] = hs[i];
+      else atomicExch(c.error, 4);
+      continue;
+    }
     const int64_t sz = erase_claim(t, hs[i]);
     if (sz >= 0) {
       freed += sz;
@@ -283,6 +303,53 @@ __global__ void k_release(CtxDev c, const int64_t* tok_off, const int64_t* hash_
   }
 }
 
+// erase_claim of a list of L3 chain hashes (the union of every shard's promoted
+// L3 spans, engine.cpp:826-828); duplicates and absent/pinned blocks are no-ops.
+__global__ void k_l3_erase_list(CtxDev c, const uint64_t* list, int64_t n,
+                                const int64_t* d_count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (d_count) n = min(n, *d_count);
+  int64_t freed = 0, cnt = 0;
+  TierDev* tp = c.tiers + 2 * c.n_rep;
+  if (i < n) {
+    const int64_t sz = erase_claim(*tp, list[i]);
+    if (sz >= 0) {
+      freed = sz;
+      cnt = 1;
+    }
+  }
+  freed = warp_sum(freed);
+  cnt = warp_sum(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tp->occupancy),
+              static_cast<unsigned long long>(-freed));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tp->n_alive),
+              static_cast<unsigned long long>(-cnt));
+  }
+}
+
+// L2 blocks erased on other shards: clear their directory bits (idempotent)
+__global__ void k_dir_clear(CtxDev c, const DirRecord* rec, int64_t n, const int64_t* d_count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (d_count) n = min(n, *d_count);
+  if (i >= n || !c.dir_main) return;
+  const DirRecord r = rec[i];
+  dir_clear_bit(c.dir_main, c.dir_main_mask, c.dir_stride, dir_key(r.hash), r.replica);
+  if (r.s % c.B == 0 && r.e % c.B != 0 && r.e > r.s)
+    dir_clear_bit(c.dir_rver, c.dir_rver_mask, c.dir_stride, rver_key(r.hash, r.s, r.e),
+                  r.replica);
+}
+
+// dst segment k = src segment idx[k] (CSR gather of uint64 rows: tokens / hashes)
+__global__ void k_gather_csr(const uint64_t* src, const int64_t* src_off, const int64_t* idx,
+                             int64_t n_idx, const int64_t* dst_off, uint64_t* dst) {
+  const int64_t k = blockIdx.x;
+  if (k >= n_idx) return;
+  const int64_t r = idx[k];
+  const int64_t a = src_off[r], len = src_off[r + 1] - a, d = dst_off[k];
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) dst[d + i] = src[a + i];
+}
+
 }  // namespace
 
 // =================================================================== C-ABI
@@ -311,12 +378,14 @@ int pyg_lookup_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_
   return PYG_OK;
 }
 
-int pyg_admit_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
-                        const int64_t* d_hash_off, const uint64_t* d_hashes, const int32_t* d_wf,
-                        const int32_t* d_role, int32_t R, const int32_t* d_placed_off,
-                        const int32_t* d_placed, double now, int32_t speculative,
-                        int32_t* d_admitted, int64_t* d_match3) {
+static int admit_impl(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                      const int64_t* d_hash_off, const uint64_t* d_hashes, const int32_t* d_wf,
+                      const int32_t* d_role, int32_t R, const int32_t* d_placed_off,
+                      const int32_t* d_placed, double now, int32_t speculative,
+                      int32_t* d_admitted, int64_t* d_match3, void* l2_out, int64_t l2_cap,
+                      uint64_t* l3_out, int64_t l3_cap, int64_t* d_counts) {
   if (!c || R < 0) return PYG_EINVAL;
+  if (d_counts) PYG_CUDA(cudaMemsetAsync(d_counts, 0, 16, c->stream));
   if (R == 0 || c->n_rep == 0) return PYG_OK;
   void* sp;
   int rc = scratch(c, static_cast<size_t>(R) * 16 + 64, &sp);
@@ -324,15 +393,72 @@ int pyg_admit_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_t
   auto* l3span = static_cast<int64_t*>(sp);
   PYG_CUDA(cudaMemsetAsync(d_admitted, 0, static_cast<size_t>(R) * 4, c->stream));
   PYG_CUDA(cudaMemsetAsync(d_match3, 0, static_cast<size_t>(R) * 24, c->stream));
+  auto* cnt = reinterpret_cast<unsigned long long*>(d_counts);
   AdmitArgs a{d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, d_placed_off, d_placed,
-              now, speculative, d_admitted, d_match3, l3span};
+              now, speculative, d_admitted, d_match3, l3span,
+              static_cast<DirRecord*>(l2_out), l2_cap, cnt};
   const size_t smem = kSmemSortCap * 12;
   cudaFuncSetAttribute(k_admit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_admit<<<c->n_rep, 512, smem, c->stream>>>(c->hd, a);
   c->dir_admits += 1;
   PYG_LAUNCHED(c);
   k_l3_erase<<<(R + 7) / 8, 256, 0, c->stream>>>(c->hd, d_tok_off, d_hash_off, d_hashes, R,
-                                                 d_admitted, l3span);
+                                                 d_admitted, l3span, l3_out, l3_cap,
+                                                 cnt ? cnt + 1 : nullptr);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_admit_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                        const int64_t* d_hash_off, const uint64_t* d_hashes, const int32_t* d_wf,
+                        const int32_t* d_role, int32_t R, const int32_t* d_placed_off,
+                        const int32_t* d_placed, double now, int32_t speculative,
+                        int32_t* d_admitted, int64_t* d_match3) {
+  return admit_impl(c, d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, R, d_placed_off,
+                    d_placed, now, speculative, d_admitted, d_match3, nullptr, 0, nullptr, 0,
+                    nullptr);
+}
+
+int pyg_admit_shard_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                        const int64_t* d_hash_off, const uint64_t* d_hashes, const int32_t* d_wf,
+                        const int32_t* d_role, int32_t R, const int32_t* d_placed_off,
+                        const int32_t* d_placed, double now, int32_t speculative,
+                        int32_t* d_admitted, int64_t* d_match3, void* d_l2_erased,
+                        int64_t l2_cap, uint64_t* d_l3_hashes, int64_t l3_cap,
+                        int64_t* d_counts) {
+  if (!d_counts || (l2_cap && !d_l2_erased) || (l3_cap && !d_l3_hashes)) return PYG_EINVAL;
+  return admit_impl(c, d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, R, d_placed_off,
+                    d_placed, now, speculative, d_admitted, d_match3, d_l2_erased, l2_cap,
+                    d_l3_hashes, l3_cap, d_counts);
+}
+
+int pyg_l3_erase_hashes_dev(pyg_ctx* c, const uint64_t* d_hashes, int64_t n,
+                            const int64_t* d_count) {
+  if (!c || n < 0) return PYG_EINVAL;
+  if (!n) return PYG_OK;
+  k_l3_erase_list<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(c->hd, d_hashes, n,
+                                                                                 d_count);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_dir_clear_dev(pyg_ctx* c, const void* d_records, int64_t n, const int64_t* d_count) {
+  if (!c || n < 0) return PYG_EINVAL;
+  if (!n) return PYG_OK;
+  k_dir_clear<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(
+      c->hd, static_cast<const DirRecord*>(d_records), n, d_count);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_gather_csr_dev(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_src_off,
+                       const int64_t* d_idx, int64_t n_idx, const int64_t* d_dst_off,
+                       uint64_t* d_dst) {
+  if (!c || n_idx < 0) return PYG_EINVAL;
+  if (!n_idx) return PYG_OK;
+  if (n_idx > 0x7fffffff) return PYG_EINVAL;
+  k_gather_csr<<<static_cast<unsigned>(n_idx), 128, 0, c->stream>>>(d_src, d_src_off, d_idx, n_idx,
+                                                                    d_dst_off, d_dst);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

@@ -591,7 +591,7 @@ extern "C" int pyg_route_batch_dev(pyg_ctx* c, int32_t mode, const pyg_nodes_dev
   }
   const int nchunk = (std::max(R, 1) + kScan - 1) / kScan;
   const int nsup = (nchunk + 31) / 32;
-  const int n = c->n_rep;
+  const int n = c->sharded ? c->n_global : c->n_rep;  // the node table is the whole cluster
   size_t tmp2 = 0;
   const int rbits = bits_for(n + 1);
   PYG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, static_cast<uint32_t*>(nullptr),

@@ -362,9 +362,15 @@ class Cluster:
     cand: np.ndarray              # int32
 
 
-def make_cluster(n_replicas, n_models, kv=100_000, l2=200_000, seed=0, max_bg=3, id_base=0):
+def make_cluster(n_replicas, n_models, kv=100_000, l2=200_000, seed=0, max_bg=3, id_base=0,
+                 interleave=False):
+    """n_replicas replicas of n_models models: contiguous blocks of replicas per model, or
+    (interleave) replica i serves model i % n_models."""
     rng = np.random.default_rng(seed)
-    model_of = (np.arange(n_replicas) * n_models // max(n_replicas, 1)).astype(np.int32)
+    if interleave:
+        model_of = (np.arange(n_replicas) % max(n_models, 1)).astype(np.int32)
+    else:
+        model_of = (np.arange(n_replicas) * n_models // max(n_replicas, 1)).astype(np.int32)
     asg, off = [], [0]
     for n in range(n_replicas):
         k = int(rng.integers(0, max_bg + 1))
