@@ -114,26 +114,37 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ workload
-def build_workload(args, rank, device):
+def build_workload(args, rank, ws, device):
+    """Rank `rank`'s burst and the GLOBAL cluster.  ws == 1: config 2 as stated (10k
+    workflows, 2 models x 16 replicas).  ws > 1 (weak scaling): every rank adds one config-2
+    unit -- 10k workflows with their own ids and two more models of 16 replicas, owned by
+    that rank; workflow w runs on model pair w % ws, so 1 - 1/ws of each rank's requests are
+    routed to and admitted on other GPUs."""
     from paper_2604_25899_b200 import workload as W
-    tr = W.deep_research(n_workflows=args.workflows, seed=1 + rank, device=device)
-    cl = W.make_cluster(args.replicas, 2, kv=args.kv, l2=args.l2, seed=rank,
-                        id_base=rank * args.replicas)
+    tr = W.deep_research(n_workflows=args.workflows, seed=1 + rank, device=device,
+                         wf_base=rank * args.workflows, model_stride=ws if ws > 1 else 0)
+    cl = W.make_cluster(args.replicas * ws, 2 * ws, kv=args.kv, l2=args.l2, seed=0)
     return tr, cl
 
 
-def warm_l2(ctx, tr, cl, rng, frac=0.01):
+def warm_l2(ctx, tr, cl, rng, frac=0.01, rep_base=0, n_local=None, n_workflows=None):
     """Stage a sample of prompts' prefixes into replicas' L2 (what forward staging does,
-    manager.cpp:60-100), so the staged matrix has real hits and tie-breaks."""
+    manager.cpp:60-100), so the staged matrix has real hits and tie-breaks.  Only this
+    ctx's replicas [rep_base, rep_base + n_local) are written."""
+    n_local = cl.n_replicas if n_local is None else n_local
+    mine = [r for r in range(tr.R)
+            if any(rep_base <= c < rep_base + n_local
+                   for c in cl.cand[cl.cand_off[tr.group[r]]:cl.cand_off[tr.group[r] + 1]])]
     n = max(1, int(tr.R * frac))
-    for r in rng.choice(tr.R, n, replace=False):
+    for r in rng.choice(mine, min(n, len(mine)), replace=False):
         g = int(tr.group[r])
-        cands = cl.cand[cl.cand_off[g]:cl.cand_off[g + 1]]
+        cands = [c for c in cl.cand[cl.cand_off[g]:cl.cand_off[g + 1]]
+                 if rep_base <= c < rep_base + n_local]
         rep = int(rng.choice(cands))
         p = tr.prompt(int(r))
-        ctx.insert_chain(rep, 1, p, int(len(p) * rng.uniform(0.3, 1.0)), int(tr.wf[r]),
-                         int(tr.role[r]), 0.5, 0)
-    for w in range(0, int(tr.wf.max()) + 1):
+        ctx.insert_chain(rep - rep_base, 1, p, int(len(p) * rng.uniform(0.3, 1.0)),
+                         int(tr.wf[r]), int(tr.role[r]), 0.5, 0)
+    for w in range(0, n_workflows or int(tr.wf.max()) + 1):
         ctx.registry_update(w, 0x3E)  # every workflow still expects roles 1..5
 
 
@@ -250,7 +261,9 @@ def run_ours(args):
     from paper_2604_25899_b200 import Context
     from paper_2604_25899_b200 import batch as PB
 
-    tr, cl = build_workload(args, rank, dev)
+    if ws > 1:
+        return run_sharded(args, ws, rank, local, dev)
+    tr, cl = build_workload(args, rank, ws, dev)
     ctx = Context(cl.n_replicas, cl.kv_capacity, cl.l2_capacity, args.block, device=local)
     PB.bind_current_stream(ctx)
     rng = np.random.default_rng(rank)
@@ -399,6 +412,154 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_sharded(args, ws, rank, local, dev):
+    """N > 1: the sharded step (paper_2604_25899_b200/shard.py) -- replicas partitioned over
+    the GPUs, route inputs all-gathered, placed requests dispatched to their owner GPU."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_25899_b200 import Context
+    from paper_2604_25899_b200 import batch as PB
+    from paper_2604_25899_b200.shard import ShardPlan, ShardedStep
+
+    tr, cl = build_workload(args, rank, ws, dev)
+    n_loc = args.replicas
+    base = rank * n_loc
+    counts = torch.tensor([tr.R], dtype=torch.int64, device=dev)
+    allc = [torch.zeros_like(counts) for _ in range(ws)]
+    dist.all_gather(allc, counts)
+    plan = ShardPlan([n_loc] * ws, [int(x.item()) for x in allc], rank, args.block)
+    ctx = Context(n_loc, cl.kv_capacity[base:base + n_loc], cl.l2_capacity[base:base + n_loc],
+                  args.block, device=local)
+    PB.bind_current_stream(ctx)
+    rng = np.random.default_rng(rank)
+    warm_l2(ctx, tr, cl, rng, rep_base=base, n_local=n_loc, n_workflows=ws * args.workflows)
+    db = PB.DeviceBatch(tr.R, tr.tokens, torch.from_numpy(tr.tok_off).to(dev), None, None,
+                        torch.from_numpy(tr.res.view(np.int64).reshape(tr.R, 4).copy()).to(dev),
+                        torch.from_numpy(tr.group).to(dev), torch.from_numpy(tr.wf).to(dev),
+                        torch.from_numpy(tr.role).to(dev), 0, tr.n_tokens)
+    nb = (np.diff(tr.tok_off) + args.block - 1) // args.block
+    hoff = np.zeros(tr.R + 1, np.int64)
+    np.cumsum(nb, out=hoff[1:])
+    db.hash_off = torch.from_numpy(hoff).to(dev)
+    db.hashes = torch.empty(int(hoff[-1]), dtype=torch.int64, device=dev)
+    dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand,
+                         device=dev)
+    st = ShardedStep(ctx, plan, db, dn, dev)
+    st.build_directory()
+    now = [1.0]
+    for _ in range(args.warmup):
+        st.step(now[0])
+        now[0] += 1.0
+    torch.cuda.synchronize()
+    ctx.check_device_error()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = ctx.kernel_launches()
+    evh = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t0e = torch.cuda.Event(enable_timing=True)
+    t1e = torch.cuda.Event(enable_timing=True)
+    t0e.record()
+    n_here = 0
+    for s_ in range(args.steps):
+        out = st.step(now[0], ev_hash=evh[s_])
+        n_here += out["n_placed_here"]
+        now[0] += 1.0
+    t1e.record()
+    torch.cuda.synchronize()
+    launches = ctx.kernel_launches() - launches0
+    clk = clocks.stop()
+    ctx.check_device_error()
+    ms = t0e.elapsed_time(t1e)
+    hash_ms = sum(a.elapsed_time(b) for a, b in evh) / args.steps
+    t = torch.tensor([ms, hash_ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, hash_ms_max = float(t[0].item()), float(t[1].item())
+    ms_step = ms / args.steps
+    value = plan.R_total * args.steps / (ms / 1000.0)
+    peak, peak_src = peaks()
+    L = np.diff(tr.tok_off)
+    hash_bytes = 8 * int(L.sum()) + 8 * int(nb.sum()) + 16 * (tr.R + 1)
+    hash_gbs = hash_bytes / (hash_ms / 1000.0) / 1e9
+
+    # e2e: pinned host inputs copied in and results copied out every step
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        h_tok = tr.tokens.cpu().pin_memory()
+        h_off, h_res = pin(tr.tok_off), pin(tr.res.view(np.int64).reshape(tr.R, 4))
+        h_grp, h_wf, h_role = pin(tr.group), pin(tr.wf), pin(tr.role)
+        h_dec = torch.empty((plan.R_local, 3), dtype=torch.int64).pin_memory()
+        h_adm = torch.empty(plan.R_local, dtype=torch.int32).pin_memory()
+        h_m3 = torch.empty((plan.R_local, 3), dtype=torch.int64).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in (h_tok, h_off, h_res, h_grp, h_wf, h_role))
+        d2h = sum(x.numel() * x.element_size() for x in (h_dec, h_adm, h_m3))
+
+        def e2e_step():
+            db.tokens.copy_(h_tok, non_blocking=True)
+            db.tok_off.copy_(h_off, non_blocking=True)
+            db.res.copy_(h_res, non_blocking=True)
+            db.group.copy_(h_grp, non_blocking=True)
+            db.wf.copy_(h_wf, non_blocking=True)
+            db.role.copy_(h_role, non_blocking=True)
+            o = st.step(now[0])
+            now[0] += 1.0
+            a = plan.req_base
+            h_dec.copy_(o["decisions"][a:a + plan.R_local], non_blocking=True)
+            h_adm.copy_(o["admitted"], non_blocking=True)
+            h_m3.copy_(o["match3"], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        e2e_step()
+        dist.barrier()
+        e_steps = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        e_ms = (time.perf_counter() - t0) * 1000.0
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+        e2e = {"value": plan.R_total * e_steps / (e_ms / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d * ws), "d2h_bytes_per_step": int(d2h * ws),
+               "ms_per_step": e_ms / e_steps,
+               "via": "ShardedStep with pinned host inputs copied in / results copied out "
+                      "(bytes summed over ranks)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {
+                "workload": (f"config-2 deep_research burst per GPU: {args.workflows} workflows "
+                             f"(~{tr.R} requests) per GPU, 6 roles, {2 * ws} models x "
+                             f"{args.replicas // 2} replicas = {args.replicas * ws} replicas "
+                             f"sharded {args.replicas}/GPU, B={args.block}, kv={args.kv}, "
+                             f"l2={args.l2}"),
+                "route_mode": "seq_commit (whole burst, identical on every GPU)",
+                "requests_per_step": plan.R_total, "requests_per_step_per_gpu": tr.R,
+                "tokens_per_step_per_gpu": tr.n_tokens,
+                "placed_on_rank0_per_step": n_here // max(args.steps, 1),
+                "l2_flush": "none needed: step inputs (tokens %.2f GB/GPU) exceed the 126 MB L2"
+                            % (tr.n_tokens * 8 / 1e9),
+                "parallelism": (f"replica shards x{ws}: NCCL all-gather of route inputs, "
+                                f"all-to-all of placed requests to owner GPUs, all-gather of "
+                                f"L2-directory/L3 erase lists")},
+            "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1), rank 0",
+                         "achieved": hash_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": hash_gbs / peak, "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": hash_bytes, "avg_launch_ms": hash_ms,
+                         "max_over_ranks_launch_ms": hash_ms_max},
+            "clocks": clk, "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": None,
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():

@@ -223,21 +223,38 @@ class ShardedStep:
         check(_lib._lib.pyg_dir_build_dev(self.ctx.h, _ptr(allrec), int(allrec.shape[0])))
 
     # ---------------------------------------------------------------- the step
-    def step(self, now: float, speculative=True, release=True, mode=1):
+    def step(self, now: float, speculative=True, release=True, mode=1, ev_hash=None,
+             marks=None):
+        """marks: optional list; (name, cuda event, host time) appended at phase ends."""
         ctx, plan, b, nodes, PB = self.ctx, self.plan, self.b, self.nodes, self.PB
+
+        def mark(name):
+            if marks is not None:
+                import time
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                marks.append((name, e, time.perf_counter()))
+
+        mark("start")
         PB.bind_current_stream(ctx)
         lib = _lib._lib
         # 1-2: local hash + staged rows
+        if ev_hash:
+            ev_hash[0].record()
         PB.hash_batch(ctx, b)
+        if ev_hash:
+            ev_hash[1].record()
         check(lib.pyg_staged_matrix_dev(ctx.h, _ptr(b.tokens), _ptr(b.tok_off), _ptr(b.hash_off),
                                         _ptr(b.hashes), plan.R_local, _ptr(b.group),
                                         nodes.n_groups, _ptr(nodes.cand_off), _ptr(nodes.cand),
                                         nodes.max_cand, _ptr(self.staged)))
+        mark("hash+staged")
         # 3: all-gather route inputs
         pay = pack_payload(b.res[:plan.R_local], b.group[:plan.R_local], b.wf[:plan.R_local],
                            b.role[:plan.R_local], self.lens, self.staged[:plan.R_local])
         g_res, g_group, g_wf, g_role, g_lens, g_staged = unpack_payload(
             allgather_var(pay, self.req_counts))
+        mark("allgather")
         # 4: route the whole burst (identical on every rank)
         ns = nodes.struct()
         check(lib.pyg_route_batch_dev(ctx.h, mode, C.byref(ns), _ptr(g_res), plan.R_total,
@@ -246,6 +263,7 @@ class ShardedStep:
                                       _ptr(self.decisions), _ptr(self.placed_off),
                                       _ptr(self.placed)))
         target = self.decisions[:plan.R_total].view(torch.int32).reshape(-1, 6)[:, 0]
+        mark("route")
         # 5: placed requests' tokens and hashes to their owners
         dp = dispatch_plan(plan, target, g_lens)
         s_lens = self.lens[dp.send_idx]
@@ -259,6 +277,7 @@ class ShardedStep:
                                      dp.send_idx.numel(), _ptr(s_hoff), _ptr(s_hash)))
         r_tok = a2a(s_tok, dp.send_tok, dp.recv_tok)
         r_hash = a2a(s_hash, dp.send_hash, dp.recv_hash)
+        mark("dispatch")
         # 6: admission of the requests placed on my replicas
         n_in = dp.recv_gidx.numel()
         l_lens = g_lens[dp.recv_gidx]
@@ -278,6 +297,7 @@ class ShardedStep:
                                       _ptr(p_loc), now, int(bool(speculative)), _ptr(adm),
                                       _ptr(m3), _ptr(l2_out), cap, _ptr(l3_out), cap,
                                       _ptr(self.counts)))
+        mark("admit")
         # 7: every shard applies every shard's L2-directory clears and L3 erasures
         caps = [max(int(x), 1) for x in dp.hash_to]
         g_cnt = allgather_cat(self.counts.reshape(1, 2))
@@ -293,6 +313,7 @@ class ShardedStep:
             if k != plan.rank:
                 check(lib.pyg_dir_clear_dev(ctx.h, _ptr(l2k), cmax, _ptr(g_cnt[k, 0:1])))
             check(lib.pyg_l3_erase_hashes_dev(ctx.h, _ptr(l3k), cmax, _ptr(g_cnt[k, 1:2])))
+        mark("l2l3_lists")
         # 8: release, results back to the origins
         if release and n_in:
             check(lib.pyg_release_batch_dev(ctx.h, _ptr(l_toff), _ptr(l_hoff), _ptr(r_hash), n_in,
@@ -304,6 +325,7 @@ class ShardedStep:
         if ret.shape[0]:
             out_adm[dp.send_idx] = ret[:, 0].to(torch.int32)
             out_m3[dp.send_idx] = ret[:, 1:]
+        mark("release+return")
         return {"decisions": self.decisions[:plan.R_total], "placed_off": self.placed_off,
                 "placed": self.placed, "admitted": out_adm[:plan.R_local],
                 "match3": out_m3[:plan.R_local], "staged": self.staged[:plan.R_local],

@@ -191,7 +191,8 @@ class _Builder:
 
 
 def deep_research(n_workflows=10_000, seed=1, device=None, unprofiled_frac=0.1,
-                  rounds=3, fanout=(2, 3), salt_tokens=4, task_tokens=256) -> Trace:
+                  rounds=3, fanout=(2, 3), salt_tokens=4, task_tokens=256, wf_base=0,
+                  model_stride=0) -> Trace:
     """Config 2 (BASELINE.json configs[1]): (decomposer -> researcher^{||2,3})^{3,3} ->
     summarizer -> critic -> writer -> verifier -> terminal; 6 roles on 2 models."""
     device = device or ("cuda" if torch.cuda.is_available() else "cpu")
@@ -202,8 +203,10 @@ def deep_research(n_workflows=10_000, seed=1, device=None, unprofiled_frac=0.1,
     b = _Builder()
     res, group, wfs, rls = [], [], [], []
     r = 0
-    for w in range(n_workflows):
+    for w in range(wf_base, wf_base + n_workflows):
         wid = f"w{w}"
+        # model_stride > 0: workflow w runs on model pair 2*(w % model_stride) (+0/+1 by role)
+        mbase = 2 * (w % model_stride) if model_stride else 0
         stages = []
         for _ in range(rounds):
             stages.append((0, 1))
@@ -230,14 +233,15 @@ def deep_research(n_workflows=10_000, seed=1, device=None, unprofiled_frac=0.1,
                     res.append((plen, GLOBAL_MAX_OUTPUT, 0.0, 0))
                 else:
                     res.append((plen, _p99(role.out_mean, role.out_cv), ALPHA, 0))
-                group.append(role.model)
+                group.append(role.model + mbase)
                 wfs.append(w)
                 rls.append(ro)
                 r += 1
             prev_first, prev_out = first_rid, int(outs[0])
     toks, tok_off = b.build(r, device)
     return Trace(toks, tok_off, np.array(res, RES_DTYPE), np.array(group, np.int32),
-                 np.array(wfs, np.int32), np.array(rls, np.int32), roles, 2, "deep_research")
+                 np.array(wfs, np.int32), np.array(rls, np.int32), roles,
+                 2 * max(model_stride, 1), "deep_research")
 
 
 def coding_assistant(n_workflows=1_000, seed=1, device=None, unprofiled_frac=0.0) -> Trace:
