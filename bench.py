@@ -446,7 +446,9 @@ def run_sharded(args, ws, rank, local, dev):
     db.hashes = torch.empty(int(hoff[-1]), dtype=torch.int64, device=dev)
     dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand,
                          device=dev)
-    st = ShardedStep(ctx, plan, db, dn, dev)
+    tt = torch.tensor([tr.n_tokens], dtype=torch.int64, device=dev)
+    dist.all_reduce(tt)
+    st = ShardedStep(ctx, plan, db, dn, dev, cl.kv_capacity[base:base + n_loc], int(tt.item()))
     st.build_directory()
     now = [1.0]
     for _ in range(args.warmup):
@@ -468,7 +470,6 @@ def run_sharded(args, ws, rank, local, dev):
     n_here = 0
     for s_ in range(args.steps):
         out = st.step(now[0], ev_hash=evh[s_])
-        n_here += out["n_placed_here"]
         now[0] += 1.0
     t1e.record()
     torch.cuda.synchronize()
@@ -544,12 +545,13 @@ def run_sharded(args, ws, rank, local, dev):
                 "route_mode": "seq_commit (whole burst, identical on every GPU)",
                 "requests_per_step": plan.R_total, "requests_per_step_per_gpu": tr.R,
                 "tokens_per_step_per_gpu": tr.n_tokens,
-                "placed_on_rank0_per_step": n_here // max(args.steps, 1),
+                "placed_on_rank0_per_step": int(out["recv_count"].item()),
                 "l2_flush": "none needed: step inputs (tokens %.2f GB/GPU) exceed the 126 MB L2"
                             % (tr.n_tokens * 8 / 1e9),
-                "parallelism": (f"replica shards x{ws}: NCCL all-gather of route inputs, "
-                                f"all-to-all of placed requests to owner GPUs, all-gather of "
-                                f"L2-directory/L3 erase lists")},
+                "parallelism": (f"replica shards x{ws}: NCCL all-gather of route inputs; owner "
+                                f"GPUs pull placed requests' tokens/hashes and peers' L2/L3 "
+                                f"erase lists and results over NVLink P2P (CUDA IPC); one "
+                                f"NCCL stream barrier; no host sync in the step")},
             "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1), rank 0",
                          "achieved": hash_gbs, "peak": peak, "unit": "GB/s",
                          "frac": hash_gbs / peak, "traffic": None, "peak_source": peak_src,

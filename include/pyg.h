@@ -278,6 +278,58 @@ int pyg_gather_csr_dev(pyg_ctx* ctx, const uint64_t* d_src, const int64_t* d_src
                        const int64_t* d_idx, int64_t n_idx, const int64_t* d_dst_off,
                        uint64_t* d_dst);
 
+/* ------------------------------------------- peer-memory exchange (NVLink P2P) */
+/* One shard's exchange window as seen by the importing process (pointers obtained with
+   pyg_ipc_import from the owner's pyg_ipc_export handles).  Inputs of its requests (tokens,
+   boundary hashes and their CSR offsets), its receive list (global request indices placed on
+   its replicas, ascending, with device count), its admission results in receive order, and its
+   exported erase lists (L2 DirRecords, L3 chain hashes; list_counts[0..1]). */
+typedef struct {
+  const uint64_t* tokens;
+  const int64_t* tok_off;
+  const uint64_t* hashes;
+  const int64_t* hash_off;
+  const int32_t* recv_gidx;
+  const int64_t* recv_count;
+  const int32_t* admitted;
+  const int64_t* match3;
+  const void* l2_list;
+  const uint64_t* l3_list;
+  const int64_t* list_counts;
+} pyg_peer;
+
+/* CUDA IPC: handle (64 bytes) + offset of the allocation holding d_ptr; import maps it into this
+   process once (cached) and returns the device pointer. */
+int pyg_ipc_export(const void* d_ptr, void* handle_out, int64_t* offset_out);
+int pyg_ipc_import(pyg_ctx* ctx, const void* handle, int64_t offset, void** d_ptr_out);
+
+/* Requests of the burst routed to this shard's replicas (ascending global index) with their
+   token / hash offsets in the receive buffers; count stays on the device.  cap bounds the
+   count (the prompt tokens placed on a replica never exceed its kv_capacity).  Lineage
+   (workflow, role) of the received requests is gathered from the burst-wide arrays. */
+int pyg_shard_recv_plan_dev(pyg_ctx* ctx, int32_t R_total, const pyg_decision* d_dec,
+                            const int64_t* d_lens, const int32_t* d_wf, const int32_t* d_role,
+                            int64_t cap, int32_t* d_recv_gidx, int64_t* d_recv_count,
+                            int64_t* d_recv_toff, int64_t* d_recv_hoff, int32_t* d_recv_wf,
+                            int32_t* d_recv_role);
+/* Pull the received requests' tokens and hashes from their origin shards (peer loads). */
+int pyg_shard_pull_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world,
+                       const int64_t* d_req_off, const int32_t* d_recv_gidx,
+                       const int64_t* d_recv_count, const int64_t* d_recv_toff,
+                       const int64_t* d_recv_hoff, uint64_t* d_tok_out, int64_t tok_cap,
+                       uint64_t* d_hash_out, int64_t hash_cap);
+/* Global per-replica placed CSR -> this shard's per-local-replica lists of receive positions. */
+int pyg_shard_local_placed_dev(pyg_ctx* ctx, const int32_t* d_placed_off, const int32_t* d_placed,
+                               const int32_t* d_recv_gidx, const int64_t* d_recv_count,
+                               int32_t* d_p_off, int32_t* d_p_loc);
+/* After a cross-GPU barrier: erase every shard's listed L3 hashes from this shard's L3 replica
+   and clear the other shards' erased L2 blocks from the directory. */
+int pyg_shard_apply_lists_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world, int32_t me);
+/* Admission results of this shard's own requests, read from their owner shards. */
+int pyg_shard_results_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world,
+                          const int64_t* d_rep_off, const pyg_decision* d_dec, int64_t req_base,
+                          int32_t R_local, int32_t* d_admitted, int64_t* d_match3);
+
 /* ------------------------------------------------- host-buffer batch entry */
 /* The drop-in batch call for a C++ engine: host arrays in, host arrays out.  Copies the batch
    to the device (pinned host memory is fastest), runs K1..K5 exactly as the _dev sequence

@@ -112,6 +112,13 @@ _sig("pyg_admit_shard_dev", vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, dbl, i32, v
 _sig("pyg_dir_clear_dev", vp, vp, i64, vp)
 _sig("pyg_l3_erase_hashes_dev", vp, vp, i64, vp)
 _sig("pyg_gather_csr_dev", vp, vp, vp, vp, i64, vp, vp)
+_sig("pyg_ipc_export", vp, vp, vp)
+_sig("pyg_ipc_import", vp, vp, i64, vp)
+_sig("pyg_shard_recv_plan_dev", vp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp)
+_sig("pyg_shard_pull_dev", vp, vp, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64)
+_sig("pyg_shard_local_placed_dev", vp, vp, vp, vp, vp, vp, vp)
+_sig("pyg_shard_apply_lists_dev", vp, vp, i32, i32)
+_sig("pyg_shard_results_dev", vp, vp, i32, vp, vp, i64, i32, vp, vp)
 _sig("pyg_lookup_batch_dev", vp, vp, vp, vp, vp, i32, vp, i32, vp)
 _sig("pyg_route_batch_dev", vp, i32, C.POINTER(NodesDev), vp, i32, vp, i32, vp, vp, i32, vp,
      dbl, vp, vp, vp)

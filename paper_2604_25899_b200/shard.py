@@ -12,14 +12,17 @@ the burst (global issue order = rank order, then index).  One step:
          lineage, staged row) -> every rank holds the whole burst's K3 inputs
   4. K3  sequential-commit route of the whole burst over the global node table,
          identically on every rank (engine.cpp:650-692 order; decisions bit-equal)
-  5. NCCL all-to-all: each placed request's tokens and boundary hashes travel from
-         its origin rank to the rank owning its target replica
+  5. the owner of each target replica PULLS the placed requests' tokens and boundary
+         hashes out of the origin GPU's HBM over NVLink (CUDA IPC peer mappings set up
+         once; csrc/k_shard.cu) -- sizes bounded by capacity_holds, counts on device
   6. K4/K5 admission on the owner, per replica in global placement order
          (engine.cpp:799-829); it exports the L2 blocks it erases and the L3 chain
          hashes it promotes
-  7. NCCL all-gather of those lists: every rank clears the directory bits and
-         erases the union from its replica of the shared L3 (erasures commute)
-  8. release (unpin) on the owner; admission results return to the origin (all-to-all)
+  7. one NCCL stream barrier, then every rank reads every peer's lists in place:
+         clears the directory bits and erases the union from its replica of the
+         shared L3 (erasures commute)
+  8. release (unpin) on the owner; each origin reads its requests' admission results
+         from the owners (peer loads).  No host synchronisation inside the step.
 
 Every collective carries data whose order is fixed by the global request order,
 so the result is bit-identical to one GPU holding the whole cluster (and to the
@@ -121,94 +124,102 @@ def unpack_payload(p: torch.Tensor):
             p[:, _PAYLOAD_FIXED:].contiguous())
 
 
-@dataclass
-class Dispatch:
-    """Who sends which placed request where (all derived from the global decisions)."""
-    send_idx: torch.Tensor      # int64 local request indices, destination-major, ascending
-    send_counts: list           # requests per destination
-    send_tok: list              # tokens per destination
-    send_hash: list             # boundary hashes per destination
-    recv_gidx: torch.Tensor     # int64 global indices of requests placed on my replicas, ascending
-    recv_counts: list
-    recv_tok: list
-    recv_hash: list
-    hash_to: list               # boundary hashes received by each rank (bounds its erase lists)
-
-
-def dispatch_plan(plan: ShardPlan, target: torch.Tensor, lens: torch.Tensor) -> Dispatch:
-    """target/lens over the whole burst (global order).  One device->host copy (G x G x 3)."""
-    G, B = plan.world, plan.B
-    dev = target.device
-    owner = plan.owner(target.to(torch.int64))
-    src = torch.bucketize(torch.arange(plan.R_total, device=dev),
-                          torch.as_tensor(plan.req_off[1:-1], device=dev), right=True)
-    ok = owner >= 0
-    pair = (src * G + owner)[ok]
-    nb = (lens + B - 1) // B
-    cnt = torch.bincount(pair, minlength=G * G)
-    tok = torch.bincount(pair, weights=lens[ok].to(torch.float64), minlength=G * G)
-    hsh = torch.bincount(pair, weights=nb[ok].to(torch.float64), minlength=G * G)
-    m = torch.stack([cnt.to(torch.float64), tok, hsh]).cpu().numpy().round().astype(np.int64)
-    m = m.reshape(3, G, G)
-    me = plan.rank
-    lo, hi = plan.req_base, plan.req_base + plan.R_local
-    own_l = owner[lo:hi]
-    sel = torch.nonzero(own_l >= 0).flatten()
-    order = torch.argsort(own_l[sel], stable=True)
-    send_idx = sel[order]
-    recv_gidx = torch.nonzero(owner == me).flatten()
-    return Dispatch(send_idx, m[0, me].tolist(), m[1, me].tolist(), m[2, me].tolist(), recv_gidx,
-                    m[0, :, me].tolist(), m[1, :, me].tolist(), m[2, :, me].tolist(),
-                    m[2].sum(axis=0).tolist())
-
-
-def local_placed(plan: ShardPlan, placed_off: torch.Tensor, placed: torch.Tensor,
-                 recv_gidx: torch.Tensor):
-    """Global per-replica placed lists (global request indices, placement order) -> the
-    owner's per-local-replica lists of local batch indices."""
-    a, b = plan.rep_base, plan.rep_base + plan.n_local
-    off = placed_off[a:b + 1].to(torch.int64)
-    vals = placed[int(off[0]):int(off[-1])].to(torch.int64) if off.numel() else placed[:0]
-    loc = torch.searchsorted(recv_gidx, vals)
-    return (off - off[0]).to(torch.int32), loc.to(torch.int32)
-
-
-def a2a(send: torch.Tensor, send_counts, recv_counts) -> torch.Tensor:
-    out = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype,
-                      device=send.device)
-    send = send[:sum(send_counts)]
-    if dist.get_world_size() == 1:
-        out.copy_(send)
-        return out
-    dist.all_to_all_single(out, send.contiguous(), recv_counts, send_counts)
-    return out
-
-
 def csr_offsets(lens: torch.Tensor) -> torch.Tensor:
     off = torch.zeros(lens.numel() + 1, dtype=torch.int64, device=lens.device)
     torch.cumsum(lens.to(torch.int64), 0, out=off[1:])
     return off
 
 
+WINDOW_FIELDS = ("tokens", "tok_off", "hashes", "hash_off", "recv_gidx", "recv_count", "admitted",
+                 "match3", "l2_list", "l3_list", "list_counts")  # == pyg_peer (include/pyg.h)
+
+
+def exchange_windows(local_ptrs, export, import_):
+    """Every rank publishes its exchange window (IPC handle + offset per field, pyg_peer
+    order); returns, per rank, the field pointers valid in THIS process (own window: local
+    pointers; others: imported peer mappings)."""
+    mine = [export(p) for p in local_ptrs]
+    ws = dist.get_world_size() if dist.is_initialized() else 1
+    allw = [None] * ws
+    if ws > 1:
+        dist.all_gather_object(allw, mine)
+    else:
+        allw = [mine]
+    me = dist.get_rank() if ws > 1 else 0
+    return [list(local_ptrs) if k == me else [import_(h, o) for h, o in allw[k]]
+            for k in range(ws)]
+
+
+def barrier_on_stream(dev):
+    """Cross-GPU stream barrier: a one-element NCCL all-reduce completes on this stream only
+    after every rank's stream has reached it."""
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(torch.zeros(1, dtype=torch.int32, device=dev))
+
+
 class ShardedStep:
     """One rank's side of the multi-GPU step (see module doc).  `nodes` is the global node
     table (every replica of the cluster, global candidate ids); `batch` holds this rank's
-    requests."""
+    requests.  Buffers other ranks read (inputs, receive lists, results, erase lists) are
+    mapped into every peer with CUDA IPC once, here."""
 
-    def __init__(self, ctx, plan: ShardPlan, batch, nodes, device):
+    def __init__(self, ctx, plan: ShardPlan, batch, nodes, device, kv_capacity_local,
+                 tokens_total=None):
         from . import batch as PB
         self.PB = PB
         self.ctx, self.plan, self.b, self.nodes, self.dev = ctx, plan, batch, nodes, device
         check(_lib._lib.pyg_set_shard(ctx.h, plan.rep_base, plan.n_global))
-        R, Rt, mc = plan.R_local, plan.R_total, max(nodes.max_cand, 1)
-        self.staged = torch.zeros((max(R, 1), mc), dtype=torch.int32, device=device)
-        self.decisions = torch.zeros((max(Rt, 1), 3), dtype=torch.int64, device=device)
-        self.placed_off = torch.zeros(plan.n_global + 1, dtype=torch.int32, device=device)
-        self.placed = torch.zeros(max(Rt, 1), dtype=torch.int32, device=device)
-        self.counts = torch.zeros(2, dtype=torch.int64, device=device)
+        R, Rt, mc, B = plan.R_local, plan.R_total, max(nodes.max_cand, 1), plan.B
+        i32, i64 = torch.int32, torch.int64
+        z = lambda *sh, dt=i64: torch.zeros(sh, dtype=dt, device=device)  # noqa: E731
+        self.staged = z(max(R, 1), mc, dt=i32)
+        self.decisions = z(max(Rt, 1), 3)
+        self.placed_off = z(plan.n_global + 1, dt=i32)
+        self.placed = z(max(Rt, 1), dt=i32)
         self.lens = (batch.tok_off[1:] - batch.tok_off[:-1]).contiguous()
         self.req_counts = np.diff(plan.req_off).tolist()
-        self.launches = 0
+        # receive-side bounds: placed prompt tokens on a replica <= its kv_capacity
+        kv = int(np.sum(kv_capacity_local))
+        tt = int(tokens_total) if tokens_total is not None else kv + 1
+        self.cap_req = max(1, min(Rt, kv))
+        self.cap_tok = max(1, min(tt, kv + 1))
+        self.cap_hash = self.cap_tok // B + self.cap_req + 1
+        self.recv_gidx = z(self.cap_req, dt=i32)
+        self.recv_count = z(1)
+        self.recv_wf = z(self.cap_req, dt=i32)
+        self.recv_role = z(self.cap_req, dt=i32)
+        self.recv_toff = z(self.cap_req + 1)
+        self.recv_hoff = z(self.cap_req + 1)
+        self.r_tok = z(self.cap_tok)
+        self.r_hash = z(self.cap_hash)
+        self.adm = z(self.cap_req, dt=i32)
+        self.m3 = z(self.cap_req, 3)
+        self.l2_list = z(self.cap_hash, 5)
+        self.l3_list = z(self.cap_hash)
+        self.counts = z(2)
+        self.p_off = z(plan.n_local + 1, dt=i32)
+        self.p_loc = z(self.cap_req, dt=i32)
+        self.out_adm = z(max(R, 1), dt=i32)
+        self.out_m3 = z(max(R, 1), 3)
+        self.rep_off_d = torch.as_tensor(plan.rep_off, dtype=i64, device=device)
+        self.req_off_d = torch.as_tensor(plan.req_off, dtype=i64, device=device)
+        local = [batch.tokens, batch.tok_off, batch.hashes, batch.hash_off, self.recv_gidx,
+                 self.recv_count, self.adm, self.m3, self.l2_list, self.l3_list, self.counts]
+        lib = _lib._lib
+
+        def export(t):
+            h = (C.c_char * 64)()
+            off = C.c_int64()
+            check(lib.pyg_ipc_export(C.c_void_p(t), h, C.byref(off)))
+            return bytes(h), off.value
+
+        def import_(h, off):
+            p = C.c_void_p()
+            check(lib.pyg_ipc_import(ctx.h, h, off, C.byref(p)))
+            return p.value
+
+        wins = exchange_windows([t.data_ptr() for t in local], export, import_)
+        self.peers = torch.tensor(wins, dtype=torch.int64, device=device)  # [world, 11]
 
     # ---------------------------------------------------------------- directory
     def build_directory(self):
@@ -218,8 +229,8 @@ class ShardedStep:
         n = C.c_int64()
         check(_lib._lib.pyg_dir_export_dev(self.ctx.h, _ptr(rec), cap, C.byref(n)))
         nt = torch.tensor([n.value], dtype=torch.int64, device=self.dev)
-        counts = allgather_cat(nt).cpu().tolist()
-        allrec = allgather_var(rec, counts)
+        counts = allgather_cat(nt).cpu().tolist() if dist.is_initialized() else [n.value]
+        allrec = allgather_var(rec, counts) if dist.is_initialized() else rec[:n.value]
         check(_lib._lib.pyg_dir_build_dev(self.ctx.h, _ptr(allrec), int(allrec.shape[0])))
 
     # ---------------------------------------------------------------- the step
@@ -238,6 +249,7 @@ class ShardedStep:
         mark("start")
         PB.bind_current_stream(ctx)
         lib = _lib._lib
+        W = plan.world
         # 1-2: local hash + staged rows
         if ev_hash:
             ev_hash[0].record()
@@ -249,11 +261,11 @@ class ShardedStep:
                                         nodes.n_groups, _ptr(nodes.cand_off), _ptr(nodes.cand),
                                         nodes.max_cand, _ptr(self.staged)))
         mark("hash+staged")
-        # 3: all-gather route inputs
+        # 3: all-gather route inputs (also the barrier that frees last step's shared buffers)
         pay = pack_payload(b.res[:plan.R_local], b.group[:plan.R_local], b.wf[:plan.R_local],
                            b.role[:plan.R_local], self.lens, self.staged[:plan.R_local])
         g_res, g_group, g_wf, g_role, g_lens, g_staged = unpack_payload(
-            allgather_var(pay, self.req_counts))
+            allgather_var(pay, self.req_counts) if dist.is_initialized() else pay)
         mark("allgather")
         # 4: route the whole burst (identical on every rank)
         ns = nodes.struct()
@@ -262,74 +274,47 @@ class ShardedStep:
                                       _ptr(nodes.cand), nodes.max_cand, _ptr(g_staged), 0.05,
                                       _ptr(self.decisions), _ptr(self.placed_off),
                                       _ptr(self.placed)))
-        target = self.decisions[:plan.R_total].view(torch.int32).reshape(-1, 6)[:, 0]
         mark("route")
-        # 5: placed requests' tokens and hashes to their owners
-        dp = dispatch_plan(plan, target, g_lens)
-        s_lens = self.lens[dp.send_idx]
-        s_nb = (s_lens + plan.B - 1) // plan.B
-        s_toff, s_hoff = csr_offsets(s_lens), csr_offsets(s_nb)
-        s_tok = torch.empty(max(int(sum(dp.send_tok)), 1), dtype=torch.int64, device=self.dev)
-        s_hash = torch.empty(max(int(sum(dp.send_hash)), 1), dtype=torch.int64, device=self.dev)
-        check(lib.pyg_gather_csr_dev(ctx.h, _ptr(b.tokens), _ptr(b.tok_off), _ptr(dp.send_idx),
-                                     dp.send_idx.numel(), _ptr(s_toff), _ptr(s_tok)))
-        check(lib.pyg_gather_csr_dev(ctx.h, _ptr(b.hashes), _ptr(b.hash_off), _ptr(dp.send_idx),
-                                     dp.send_idx.numel(), _ptr(s_hoff), _ptr(s_hash)))
-        r_tok = a2a(s_tok, dp.send_tok, dp.recv_tok)
-        r_hash = a2a(s_hash, dp.send_hash, dp.recv_hash)
+        # 5: requests placed on my replicas: plan, pull their tokens/hashes from the origins
+        check(lib.pyg_shard_recv_plan_dev(ctx.h, plan.R_total, _ptr(self.decisions), _ptr(g_lens),
+                                          _ptr(g_wf), _ptr(g_role), self.cap_req,
+                                          _ptr(self.recv_gidx), _ptr(self.recv_count),
+                                          _ptr(self.recv_toff), _ptr(self.recv_hoff),
+                                          _ptr(self.recv_wf), _ptr(self.recv_role)))
+        check(lib.pyg_shard_pull_dev(ctx.h, _ptr(self.peers), W, _ptr(self.req_off_d),
+                                     _ptr(self.recv_gidx), _ptr(self.recv_count),
+                                     _ptr(self.recv_toff), _ptr(self.recv_hoff), _ptr(self.r_tok),
+                                     self.cap_tok, _ptr(self.r_hash), self.cap_hash))
+        check(lib.pyg_shard_local_placed_dev(ctx.h, _ptr(self.placed_off), _ptr(self.placed),
+                                             _ptr(self.recv_gidx), _ptr(self.recv_count),
+                                             _ptr(self.p_off), _ptr(self.p_loc)))
         mark("dispatch")
-        # 6: admission of the requests placed on my replicas
-        n_in = dp.recv_gidx.numel()
-        l_lens = g_lens[dp.recv_gidx]
-        l_toff = csr_offsets(l_lens)
-        l_hoff = csr_offsets((l_lens + plan.B - 1) // plan.B)
-        l_wf = g_wf[dp.recv_gidx].contiguous()
-        l_role = g_role[dp.recv_gidx].contiguous()
-        p_off, p_loc = local_placed(plan, self.placed_off, self.placed, dp.recv_gidx)
-        adm = torch.zeros(max(n_in, 1), dtype=torch.int32, device=self.dev)
-        m3 = torch.zeros((max(n_in, 1), 3), dtype=torch.int64, device=self.dev)
-        cap = max(int(sum(dp.recv_hash)), 1)
-        l2_out = torch.empty((cap, 5), dtype=torch.int64, device=self.dev)
-        l3_out = torch.empty(cap, dtype=torch.int64, device=self.dev)
-        p_loc = p_loc if p_loc.numel() else torch.zeros(1, dtype=torch.int32, device=self.dev)
-        check(lib.pyg_admit_shard_dev(ctx.h, _ptr(r_tok), _ptr(l_toff), _ptr(l_hoff),
-                                      _ptr(r_hash), _ptr(l_wf), _ptr(l_role), n_in, _ptr(p_off),
-                                      _ptr(p_loc), now, int(bool(speculative)), _ptr(adm),
-                                      _ptr(m3), _ptr(l2_out), cap, _ptr(l3_out), cap,
+        # 6: admission on the owner (bounded sizes; the real count lives on the device)
+        check(lib.pyg_admit_shard_dev(ctx.h, _ptr(self.r_tok), _ptr(self.recv_toff),
+                                      _ptr(self.recv_hoff), _ptr(self.r_hash), _ptr(self.recv_wf),
+                                      _ptr(self.recv_role), self.cap_req, _ptr(self.p_off),
+                                      _ptr(self.p_loc), now, int(bool(speculative)),
+                                      _ptr(self.adm), _ptr(self.m3), _ptr(self.l2_list),
+                                      self.cap_hash, _ptr(self.l3_list), self.cap_hash,
                                       _ptr(self.counts)))
         mark("admit")
-        # 7: every shard applies every shard's L2-directory clears and L3 erasures
-        caps = [max(int(x), 1) for x in dp.hash_to]
-        g_cnt = allgather_cat(self.counts.reshape(1, 2))
-        cmax = max(caps)
-        buf = torch.zeros((cmax, 6), dtype=torch.int64, device=self.dev)
-        buf[:cap, :5] = l2_out
-        buf[:cap, 5] = l3_out
-        g_buf = allgather_cat(buf)
-        for k in range(plan.world):
-            blk = g_buf[k * cmax:(k + 1) * cmax]
-            l2k = blk[:, :5].contiguous()
-            l3k = blk[:, 5].contiguous()
-            if k != plan.rank:
-                check(lib.pyg_dir_clear_dev(ctx.h, _ptr(l2k), cmax, _ptr(g_cnt[k, 0:1])))
-            check(lib.pyg_l3_erase_hashes_dev(ctx.h, _ptr(l3k), cmax, _ptr(g_cnt[k, 1:2])))
+        # 7: every shard applies every shard's L3 erasures and L2-directory clears
+        barrier_on_stream(self.dev)
+        check(lib.pyg_shard_apply_lists_dev(ctx.h, _ptr(self.peers), W, plan.rank))
         mark("l2l3_lists")
-        # 8: release, results back to the origins
-        if release and n_in:
-            check(lib.pyg_release_batch_dev(ctx.h, _ptr(l_toff), _ptr(l_hoff), _ptr(r_hash), n_in,
-                                            _ptr(p_off), _ptr(p_loc), _ptr(adm)))
-        back = torch.cat([adm[:n_in].to(torch.int64).reshape(-1, 1), m3[:n_in]], dim=1)
-        ret = a2a(back.contiguous(), dp.recv_counts, dp.send_counts)
-        out_adm = torch.zeros(max(plan.R_local, 1), dtype=torch.int32, device=self.dev)
-        out_m3 = torch.zeros((max(plan.R_local, 1), 3), dtype=torch.int64, device=self.dev)
-        if ret.shape[0]:
-            out_adm[dp.send_idx] = ret[:, 0].to(torch.int32)
-            out_m3[dp.send_idx] = ret[:, 1:]
+        # 8: release on the owner; results of my requests from their owners
+        if release:
+            check(lib.pyg_release_batch_dev(ctx.h, _ptr(self.recv_toff), _ptr(self.recv_hoff),
+                                            _ptr(self.r_hash), self.cap_req, _ptr(self.p_off),
+                                            _ptr(self.p_loc), _ptr(self.adm)))
+        check(lib.pyg_shard_results_dev(ctx.h, _ptr(self.peers), W, _ptr(self.rep_off_d),
+                                        _ptr(self.decisions), plan.req_base, plan.R_local,
+                                        _ptr(self.out_adm), _ptr(self.out_m3)))
         mark("release+return")
         return {"decisions": self.decisions[:plan.R_total], "placed_off": self.placed_off,
-                "placed": self.placed, "admitted": out_adm[:plan.R_local],
-                "match3": out_m3[:plan.R_local], "staged": self.staged[:plan.R_local],
-                "n_placed_here": n_in}
+                "placed": self.placed, "admitted": self.out_adm[:plan.R_local],
+                "match3": self.out_m3[:plan.R_local], "staged": self.staged[:plan.R_local],
+                "recv_count": self.recv_count}
 
 
 def decisions_host(dec: torch.Tensor) -> np.ndarray:

@@ -78,7 +78,7 @@ def run(rank, world, B=16, steps=3, n_wf=20, n_rep=8, n_models=2, interleave=Tru
                          device=dev)
     dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand,
                          device=dev)
-    st = ShardedStep(ctx, plan, db, dn, dev)
+    st = ShardedStep(ctx, plan, db, dn, dev, cl.kv_capacity[lo:lo + plan.n_local], tr.n_tokens)
     st.build_directory()
     placed_total = 0
     for s in range(steps):

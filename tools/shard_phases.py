@@ -34,7 +34,7 @@ def main():
                   n_workflows=ws * args.workflows)
     db = PB.upload_batch(ctx, tr.tokens_np(), tr.tok_off, tr.res, tr.group, tr.wf, tr.role, device=dev)
     dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand, device=dev)
-    st = ShardedStep(ctx, plan, db, dn, dev)
+    st = ShardedStep(ctx, plan, db, dn, dev, cl.kv_capacity[base:base + n_loc])
     st.build_directory()
     for i in range(3):
         st.step(1.0 + i)
