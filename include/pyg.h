@@ -330,6 +330,38 @@ int pyg_shard_results_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world,
                           const int64_t* d_rep_off, const pyg_decision* d_dec, int64_t req_base,
                           int32_t R_local, int32_t* d_admitted, int64_t* d_match3);
 
+/* ------------------------------------------------ K6: next-use from the workflow DAG */
+/* One node of a flattened path expression (PathNode, path_expr.hpp:21-38), preorder: every
+   node's descendants follow it.  kind: 0 Atom, 1 Seq, 2 Repeat, 3 ParallelFanout,
+   4 Optional, 5 Terminal (PathKind order).  Seq children are ch_list[ch_begin..ch_end). */
+typedef struct {
+  int32_t kind, role, min, max;
+  double p_continue, p;
+  int32_t child, ch_begin, ch_end, pad;
+} pyg_path_node;
+
+/* expected_distance_to(cursor, role) (path_analysis.cpp:553-557) for every cursor and role
+   < n_roles, and future_roles(cursor) (path_analysis.cpp:547-551) as role masks.  Cursors are
+   PathCursor::frames() as a CSR: frames [d_frame_off[c], d_frame_off[c+1]) of (node id,
+   progress), root frame first, atom frame last.  d_dist[c*n_roles + role] = NaN for nullopt.
+   Bit-exact FP64 (no contraction). */
+int pyg_next_use_dev(pyg_ctx* ctx, const pyg_path_node* d_nodes, int32_t n_nodes,
+                     const int32_t* d_ch_list, int32_t n_cursors, const int32_t* d_frame_off,
+                     const int32_t* d_frame_node, const int32_t* d_frame_prog, int32_t n_roles,
+                     double* d_dist, uint64_t* d_future);
+/* Predicted next use of every block of a tier in id order (the pyg_tier_dump order):
+   d_dist[d_wf_cursor[block.workflow]*n_roles + block.role], NaN when the workflow has no
+   cursor (-1) or the role has no future occurrence.  *d_count = number of blocks. */
+int pyg_block_next_use_dev(pyg_ctx* ctx, int32_t replica, int32_t tier, const int32_t* d_wf_cursor,
+                           int32_t n_wf, const double* d_dist, int32_t n_roles, double* d_out,
+                           int64_t cap, int64_t* d_count);
+/* FutureRegistry::update from cursors (engine.cpp:605-609 at issue: future_roles plus the
+   current role; engine.cpp:1064-1065 at completion: d_current_role = NULL).  d_cursor[i] = -1
+   registers an empty set.  max_wf bounds the workflow ids (registry capacity). */
+int pyg_registry_from_cursors_dev(pyg_ctx* ctx, int32_t n, int32_t max_wf, const int32_t* d_wf,
+                                  const int32_t* d_cursor, const uint64_t* d_future,
+                                  const int32_t* d_current_role);
+
 /* ------------------------------------------------- host-buffer batch entry */
 /* The drop-in batch call for a C++ engine: host arrays in, host arrays out.  Copies the batch
    to the device (pinned host memory is fastest), runs K1..K5 exactly as the _dev sequence

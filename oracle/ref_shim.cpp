@@ -15,7 +15,9 @@
 
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -431,4 +433,100 @@ int64_t pref_step(void** caches, int32_t n_rep, void* l3v, void* regv, int32_t s
   return n_placed;
 }
 
+// ---- path analysis over a flattened tree (preorder node arrays, the layout of
+// pyg_path_node in include/pyg.h): builds the reference PathExpr, locates a history
+// with locate_position (path_analysis.cpp), and evaluates expected_distance_to /
+// future_roles there.  Frames come back as preorder node ids.
+struct pref_path_node {
+  int32_t kind, role, min, max;
+  double p_continue, p;
+  int32_t child, ch_begin, ch_end, pad;
+};
+
+namespace {
+workflow::PathNodePtr build_node(const pref_path_node* n, const int32_t* ch, int32_t i) {
+  const pref_path_node& x = n[i];
+  switch (x.kind) {
+    case 0: return workflow::PathNode::atom(role_name(x.role));
+    case 1: {
+      std::vector<workflow::PathNodePtr> kids;
+      for (int32_t k = x.ch_begin; k < x.ch_end; ++k) kids.push_back(build_node(n, ch, ch[k]));
+      return workflow::PathNode::seq(std::move(kids));
+    }
+    case 2: return workflow::PathNode::repeat(build_node(n, ch, x.child), x.min, x.max, x.p_continue);
+    case 3: return workflow::PathNode::fanout(build_node(n, ch, x.child), x.min, x.max);
+    case 4: return workflow::PathNode::optional(build_node(n, ch, x.child), x.p);
+    default: return workflow::PathNode::terminal();
+  }
+}
+
+void preorder_ids(const workflow::PathNode* node, std::map<const workflow::PathNode*, int32_t>& ids) {
+  const int32_t id = static_cast<int32_t>(ids.size());
+  ids[node] = id;
+  if (node->kind == workflow::PathKind::Seq) {
+    for (const auto& c : node->children) preorder_ids(c.get(), ids);
+  } else if (node->child) {
+    preorder_ids(node->child.get(), ids);
+  }
+}
+
+std::vector<std::string> history_of(const int32_t* h, int32_t n) {
+  std::vector<std::string> out;
+  for (int32_t i = 0; i < n; ++i) out.push_back(role_name(h[i]));
+  return out;
+}
+}  // namespace
+
+extern "C" {
+
+void* pref_path_build(const pref_path_node* nodes, const int32_t* ch_list, int32_t root) {
+  try {
+    return new workflow::PathExpr(build_node(nodes, ch_list, root));
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+void pref_path_free(void* e) { delete static_cast<workflow::PathExpr*>(e); }
+
+// Frames of locate_position(history) as (preorder id, progress); returns the frame count,
+// -1 if the history cannot be located.
+int32_t pref_path_locate(void* e, const int32_t* hist, int32_t n_hist, int32_t* frame_node,
+                         int32_t* frame_prog, int32_t cap) {
+  auto* ex = static_cast<workflow::PathExpr*>(e);
+  auto pos = workflow::locate_position(*ex, history_of(hist, n_hist));
+  if (!pos) return -1;
+  std::map<const workflow::PathNode*, int32_t> ids;
+  preorder_ids(ex->root().get(), ids);
+  const auto& fr = pos->frames();
+  const int32_t nf = static_cast<int32_t>(fr.size());
+  for (int32_t i = 0; i < nf && i < cap; ++i) {
+    frame_node[i] = ids.at(fr[i].node);
+    frame_prog[i] = fr[i].progress;
+  }
+  return nf;
+}
+
+// expected_distance_to at the located position: 0 = value written, 1 = nullopt, -1 = history
+// not locatable.  *future_mask = future_roles as a role bitmask.
+int32_t pref_path_distance(void* e, const int32_t* hist, int32_t n_hist, int32_t role,
+                           double* out, uint64_t* future_mask) {
+  auto* ex = static_cast<workflow::PathExpr*>(e);
+  auto pos = workflow::locate_position(*ex, history_of(hist, n_hist));
+  if (!pos) return -1;
+  if (future_mask) {
+    uint64_t m = 0;
+    for (const auto& r : workflow::future_roles(*pos)) {
+      int32_t k = parse_int(r);
+      if (k >= 0 && k < 64) m |= uint64_t{1} << k;
+    }
+    *future_mask = m;
+  }
+  auto d = workflow::expected_distance_to(*pos, role_name(role));
+  if (!d) return 1;
+  *out = *d;
+  return 0;
+}
+
+}  // extern "C"
 }  // extern "C"

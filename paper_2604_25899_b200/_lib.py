@@ -113,6 +113,9 @@ _sig("pyg_dir_clear_dev", vp, vp, i64, vp)
 _sig("pyg_l3_erase_hashes_dev", vp, vp, i64, vp)
 _sig("pyg_gather_csr_dev", vp, vp, vp, vp, i64, vp, vp)
 _sig("pyg_ipc_export", vp, vp, vp)
+_sig("pyg_next_use_dev", vp, vp, i32, vp, i32, vp, vp, vp, i32, vp, vp)
+_sig("pyg_block_next_use_dev", vp, i32, i32, vp, i32, vp, i32, vp, i64, vp)
+_sig("pyg_registry_from_cursors_dev", vp, i32, i32, vp, vp, vp, vp)
 _sig("pyg_ipc_import", vp, vp, i64, vp)
 _sig("pyg_shard_recv_plan_dev", vp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp)
 _sig("pyg_shard_pull_dev", vp, vp, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64)

@@ -637,6 +637,7 @@ static int reg_grow(pyg_ctx* c, int32_t wf) {
   return PYG_OK;
 }
 
+
 int pyg_registry_update(pyg_ctx* c, int32_t wf, uint64_t mask) {
   if (!c || wf < 0) return PYG_EINVAL;
   int rc = reg_grow(c, wf);
@@ -826,3 +827,7 @@ int pyg_route_least_outstanding(pyg_ctx* c, int32_t nn, const int32_t* rid, cons
 }
 
 }  // extern "C"
+
+namespace pyg_host {
+int reg_ensure(pyg_ctx* c, int32_t max_wf) { return reg_grow(c, max_wf); }
+}  // namespace pyg_host
