@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="deep_research", choices=["deep_research", "bursty"],
+                    help="deep_research = config 2 (default); bursty = config 4 (per-GPU slice)")
+    ap.add_argument("--requests", type=int, default=125_000, help="bursty: requests per GPU")
     ap.add_argument("--workflows", type=int, default=10_000)
     ap.add_argument("--replicas", type=int, default=32)
     ap.add_argument("--block", type=int, default=16)
@@ -121,10 +124,40 @@ def build_workload(args, rank, ws, device):
     that rank; workflow w runs on model pair w % ws, so 1 - 1/ws of each rank's requests are
     routed to and admitted on other GPUs."""
     from paper_2604_25899_b200 import workload as W
+    if args.workload == "bursty":
+        # config 4: 1M requests over 4 models x 64 replicas at 8 GPUs = 125k requests and
+        # 32 replicas (8 per model, interleaved) per GPU
+        tr = W.bursty(n_requests=args.requests, seed=1 + rank, device=device,
+                      r_base=rank * args.requests)
+        cl = W.make_cluster(args.replicas * ws, 4, kv=args.kv, l2=args.l2, seed=0,
+                            interleave=True)
+        return tr, cl
     tr = W.deep_research(n_workflows=args.workflows, seed=1 + rank, device=device,
                          wf_base=rank * args.workflows, model_stride=ws if ws > 1 else 0)
     cl = W.make_cluster(args.replicas * ws, 2 * ws, kv=args.kv, l2=args.l2, seed=0)
     return tr, cl
+
+
+def n_workflows_total(args, ws, tr):
+    if args.workload == "bursty":
+        return (ws * args.requests) // 8 + 1
+    return ws * args.workflows
+
+
+def describe(args, tr, ws):
+    if args.workload == "bursty":
+        return (f"config-4 bursty multi-LLM slice: {args.requests} requests/GPU "
+                f"({ws * args.requests} total), L~lognormal(2048,1.0) in [64,32768], 4 models x "
+                f"{args.replicas * ws // 4} replicas = {args.replicas * ws} replicas "
+                f"({args.replicas}/GPU), B={args.block}, kv={args.kv}, l2={args.l2}")
+    if ws == 1:
+        return (f"config-2 deep_research burst: {args.workflows} workflows = {tr.R} requests/step, "
+                f"6 roles, 2 models x {args.replicas // 2} replicas, B={args.block}, kv={args.kv}, "
+                f"l2={args.l2}")
+    return (f"config-2 deep_research burst per GPU: {args.workflows} workflows (~{tr.R} requests) "
+            f"per GPU, 6 roles, {2 * ws} models x {args.replicas // 2} replicas = "
+            f"{args.replicas * ws} replicas sharded {args.replicas}/GPU, B={args.block}, "
+            f"kv={args.kv}, l2={args.l2}")
 
 
 def warm_l2(ctx, tr, cl, rng, frac=0.01, rep_base=0, n_local=None, n_workflows=None):
@@ -172,14 +205,18 @@ def algorithmic_bytes(tr, B, staged, max_cand, cl, placed, match3):
 # --------------------------------------------------------------- CPU baseline
 def _cpu_worker(payload):
     """Reference engine composition (oracle/_ref, unmodified sources) on one core."""
-    wf_count, seed, seconds, replicas, kv, l2, B, rank_base = payload
+    wf_count, seed, seconds, replicas, kv, l2, B, rank_base, workload = payload
     import torch  # noqa: F401
     from oracle.py_oracle import Reference
     from oracle.step import apply_warm_oracle, warm_ops
     from paper_2604_25899_b200 import workload as W
     ref = Reference(B)
-    tr = W.deep_research(n_workflows=wf_count, seed=seed, device="cpu")
-    cl = W.make_cluster(replicas, 2, kv=kv, l2=l2, seed=seed, id_base=rank_base)
+    if workload == "bursty":
+        tr = W.bursty(n_requests=wf_count * 8, seed=seed, device="cpu")
+        cl = W.make_cluster(replicas, 4, kv=kv, l2=l2, seed=seed, interleave=True)
+    else:
+        tr = W.deep_research(n_workflows=wf_count, seed=seed, device="cpu")
+        cl = W.make_cluster(replicas, 2, kv=kv, l2=l2, seed=seed, id_base=rank_base)
     caches = [ref.new_cache(int(cl.kv_capacity[n]), int(cl.l2_capacity[n])) for n in range(replicas)]
     l3, reg = ref.new_l3(), ref.new_registry()
     apply_warm_oracle(ref, caches, l3, reg, tr, warm_ops(tr, cl, seed, n_chains=4))
@@ -205,8 +242,8 @@ def cpu_baseline(args, cores, seconds):
     if not reference_available(args.block):
         return None
     wf = max(40, min(args.workflows, 400))
-    payloads = [(wf, 100 + i, seconds, args.replicas, args.kv, args.l2, args.block, 0)
-                for i in range(cores)]
+    payloads = [(wf, 100 + i, seconds, args.replicas, args.kv, args.l2, args.block, 0,
+                 args.workload) for i in range(cores)]
     if cores == 1:
         res = [_cpu_worker(payloads[0])]
     else:
@@ -216,7 +253,8 @@ def cpu_baseline(args, cores, seconds):
     rate = sum(d / e for d, e, _ in res)
     n = sum(d for d, _, _ in res)
     return {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": (f"{n} config-2 requests (mean prompt {res[0][2]:.0f} tokens) routed through "
+            "sample": (f"{n} {'config-4' if args.workload == 'bursty' else 'config-2'} requests "
+                       f"(mean prompt {res[0][2]:.0f} tokens) routed through "
                        f"the unmodified reference (oracle/_ref/libpythia_ref{args.block}.so, "
                        f"pref_step: per-candidate lookup, route, admit, release) on "
                        f"{args.replicas} replicas, {cores} process(es) x {seconds:.0f}s")}
@@ -240,7 +278,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * el / max(args.steps, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "config-2 deep_research burst (bounded CPU sample)",
+            "config": {"workload": f"{args.workload} burst (bounded CPU sample)",
                        "replicas": args.replicas, "block_tokens": args.block,
                        "route_mode": "seq_commit"},
             "cpu_baseline": bl,
@@ -267,7 +305,7 @@ def run_ours(args):
     ctx = Context(cl.n_replicas, cl.kv_capacity, cl.l2_capacity, args.block, device=local)
     PB.bind_current_stream(ctx)
     rng = np.random.default_rng(rank)
-    warm_l2(ctx, tr, cl, rng)
+    warm_l2(ctx, tr, cl, rng, n_workflows=n_workflows_total(args, ws, tr))
     db = PB.DeviceBatch(tr.R, tr.tokens, torch.from_numpy(tr.tok_off).to(dev), None, None,
                         torch.from_numpy(tr.res.view(np.int64).reshape(tr.R, 4).copy()).to(dev),
                         torch.from_numpy(tr.group).to(dev), torch.from_numpy(tr.wf).to(dev),
@@ -386,9 +424,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {
-                "workload": (f"config-2 deep_research burst: {args.workflows} workflows = "
-                             f"{tr.R} requests/step/GPU, 6 roles, 2 models x {args.replicas // 2} "
-                             f"replicas, B={args.block}, kv={args.kv}, l2={args.l2}"),
+                "workload": describe(args, tr, ws),
                 "route_mode": "seq_commit" if mode == PB.SEQ_COMMIT else "snapshot",
                 "requests_per_step_per_gpu": tr.R, "tokens_per_step_per_gpu": tr.n_tokens,
                 "placed_per_step": n_placed, "admitted_per_step": n_admitted,
@@ -434,7 +470,8 @@ def run_sharded(args, ws, rank, local, dev):
                   args.block, device=local)
     PB.bind_current_stream(ctx)
     rng = np.random.default_rng(rank)
-    warm_l2(ctx, tr, cl, rng, rep_base=base, n_local=n_loc, n_workflows=ws * args.workflows)
+    warm_l2(ctx, tr, cl, rng, rep_base=base, n_local=n_loc,
+            n_workflows=n_workflows_total(args, ws, tr))
     db = PB.DeviceBatch(tr.R, tr.tokens, torch.from_numpy(tr.tok_off).to(dev), None, None,
                         torch.from_numpy(tr.res.view(np.int64).reshape(tr.R, 4).copy()).to(dev),
                         torch.from_numpy(tr.group).to(dev), torch.from_numpy(tr.wf).to(dev),
@@ -537,11 +574,7 @@ def run_sharded(args, ws, rank, local, dev):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {
-                "workload": (f"config-2 deep_research burst per GPU: {args.workflows} workflows "
-                             f"(~{tr.R} requests) per GPU, 6 roles, {2 * ws} models x "
-                             f"{args.replicas // 2} replicas = {args.replicas * ws} replicas "
-                             f"sharded {args.replicas}/GPU, B={args.block}, kv={args.kv}, "
-                             f"l2={args.l2}"),
+                "workload": describe(args, tr, ws),
                 "route_mode": "seq_commit (whole burst, identical on every GPU)",
                 "requests_per_step": plan.R_total, "requests_per_step_per_gpu": tr.R,
                 "tokens_per_step_per_gpu": tr.n_tokens,

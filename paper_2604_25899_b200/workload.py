@@ -325,9 +325,10 @@ def long_context(n_requests=100_000, seed=1, device=None, n_roles=8, steps=4,
 
 
 def bursty(n_requests=1_000_000, seed=1, device=None, n_models=4, mean_len=2048, cv=1.0,
-           n_prefixes=512) -> Trace:
+           n_prefixes=512, r_base=0) -> Trace:
     """Config 4: L ~ lognormal(2048, 1.0) clamped to [64, 32768] over 4 models; prompts share
-    one of n_prefixes system prefixes (shared across the model's workflows) + unique suffix."""
+    one of n_prefixes system prefixes (shared across the model's workflows) + unique suffix.
+    r_base offsets request / workflow ids (one GPU's slice of a larger burst)."""
     device = device or ("cuda" if torch.cuda.is_available() else "cpu")
     rng = np.random.default_rng(seed)
     s2 = math.log(1 + cv * cv)
@@ -342,13 +343,14 @@ def bursty(n_requests=1_000_000, seed=1, device=None, n_models=4, mean_len=2048,
     unprof = rng.random(n_requests) < 0.1
     for r in range(n_requests):
         b.add(r, "i", pkeys[pre[r]], 0, int(plen[r]))
-        b.add(r, "i", salt_key(f"b{r}"), 0, int(L[r] - plen[r]))
+        b.add(r, "i", salt_key(f"b{r_base + r}"), 0, int(L[r] - plen[r]))
     res = np.zeros(n_requests, RES_DTYPE)
     res["prompt_len"] = L
     res["upper"] = np.where(unprof, GLOBAL_MAX_OUTPUT, up)
     res["alpha"] = np.where(unprof, 0.0, ALPHA)
     toks, tok_off = b.build(n_requests, device)
-    return Trace(toks, tok_off, res, model, (np.arange(n_requests) // 8).astype(np.int32),
+    return Trace(toks, tok_off, res, model,
+                 ((r_base + np.arange(n_requests)) // 8).astype(np.int32),
                  (pre % 16).astype(np.int32), [], n_models, "bursty")
 
 
