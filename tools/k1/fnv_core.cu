@@ -106,27 +106,29 @@ int main() {
   uint64_t* d; cudaMalloc(&d, 8ull << 22);
   const int ntok = 4096;
   const char* names[] = {"fnv_token (product)", "plain u64 *= P", "split IMAD.HI + PRMT", "PRMT byte extract", "mad hi + LEA", "mad hi + shf + add"};
-  for (int blocks_per_sm : {4, 8}) {
-    const int grid = nsm * blocks_per_sm;
+  for (int blocks_per_sm : {0, 8}) {
+    const int grid = blocks_per_sm ? nsm * blocks_per_sm : nsm;  // 0: one warp per SM (latency)
+    const int threads = blocks_per_sm ? 256 : 32;
     uint64_t ref[6] = {0, 0, 0, 0, 0, 0};
     for (int V = 0; V < 6; ++V) {
       cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
       auto launch = [&]() {
-        if (V == 0) bench<0><<<grid, 256>>>(d, ntok, 7);
-        if (V == 1) bench<1><<<grid, 256>>>(d, ntok, 7);
-        if (V == 2) bench<2><<<grid, 256>>>(d, ntok, 7);
-        if (V == 3) bench<3><<<grid, 256>>>(d, ntok, 7);
-        if (V == 4) bench<4><<<grid, 256>>>(d, ntok, 7);
-        if (V == 5) bench<5><<<grid, 256>>>(d, ntok, 7);
+        if (V == 0) bench<0><<<grid, threads>>>(d, ntok, 7);
+        if (V == 1) bench<1><<<grid, threads>>>(d, ntok, 7);
+        if (V == 2) bench<2><<<grid, threads>>>(d, ntok, 7);
+        if (V == 3) bench<3><<<grid, threads>>>(d, ntok, 7);
+        if (V == 4) bench<4><<<grid, threads>>>(d, ntok, 7);
+        if (V == 5) bench<5><<<grid, threads>>>(d, ntok, 7);
       };
       launch();
       cudaEventRecord(a); launch(); cudaEventRecord(b); cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b);
       uint64_t x; cudaMemcpy(&x, d + 12345, 8, cudaMemcpyDeviceToHost);
       ref[V] = x;
-      const double toks = (double)grid * 256 * ntok;
-      printf("blocks/SM %d  %-24s %.3f ms  %.1f Gtok/s  = %.2f TB/s of token bytes  %s\n", blocks_per_sm,
-             names[V], ms, toks / ms / 1e6, toks * 8 / ms / 1e9, V && ref[V] != ref[0] ? "MISMATCH" : "");
+      const double toks = (double)grid * threads * ntok;
+      printf("blocks/SM %d  %-24s %.3f ms  %.1f Gtok/s  = %.2f TB/s  %.1f cycles/token/lane  %s\n", blocks_per_sm,
+             names[V], ms, toks / ms / 1e6, toks * 8 / ms / 1e9, ms * 1e-3 * 1.965e9 / ntok,
+             V && ref[V] != ref[0] ? "MISMATCH" : "");
     }
   }
   return 0;

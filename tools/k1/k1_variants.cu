@@ -24,14 +24,14 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 // ---------------- V0: the product kernel (1 chain per lane, 16-token chunks)
 namespace v0 {
 constexpr int kChunk = 16, kRowBytes = kChunk * 8 + 16, kStageBytes = 32 * kRowBytes;
-template <int kWarps, int kMinB>
+template <int kWarps, int kMinB, int kStages = 2>
 __global__ void __launch_bounds__(kWarps * 32, kMinB)
 k(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int R,
   const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
   uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbuf = smem + warp * 2 * kStageBytes;
+  unsigned char* wbuf = smem + warp * kStages * kStageBytes;
   const int ntasks = (R + 31) / 32;
   for (;;) {
     int task = 0;
@@ -51,7 +51,7 @@ k(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int 
     int cc = cpb;
     const int sub = lane >> 4, q = lane & 15;
     auto issue = [&](int c) {
-      unsigned char* st = wbuf + (c & 1) * kStageBytes;
+      unsigned char* st = wbuf + (c % kStages) * kStageBytes;
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
         const int jj = j + sub;
@@ -64,13 +64,16 @@ k(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int 
     };
     uint64_t h = kFnvOffset;
     int64_t kk = 0;
-    issue(0);
+#pragma unroll
+    for (int c0 = 0; c0 < kStages - 1; ++c0) {
+      if (c0 < maxch) issue(c0); else cp_commit();
+    }
     for (int c = 0; c < maxch; ++c) {
-      if (c + 1 < maxch) issue(c + 1); else cp_commit();
-      cp_wait1();
+      if (c + kStages - 1 < maxch) issue(c + kStages - 1); else cp_commit();
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kStages - 1));
       __syncwarp();
       if (c < nch) {
-        const unsigned char* row = wbuf + (c & 1) * kStageBytes + lane * kRowBytes;
+        const unsigned char* row = wbuf + (c % kStages) * kStageBytes + lane * kRowBytes;
         const int64_t rem = n - static_cast<int64_t>(c) * kChunk;
         if (rem >= kChunk) {
 #pragma unroll
@@ -205,12 +208,14 @@ __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
 
 int main(int argc, char** argv) {
-  const int R = 145000, B = 16;
+  const int R = argc > 1 ? atoi(argv[1]) : 145000, B = 16;
+  const double mean = argc > 2 ? atof(argv[2]) : 1100, cv = argc > 3 ? atof(argv[3]) : 0.6;
+  const int64_t lmax = argc > 4 ? atol(argv[4]) : 4096;
   std::mt19937_64 rng(1);
-  std::lognormal_distribution<double> ln(std::log(1100.0) - 0.5 * std::log(1 + 0.36), std::sqrt(std::log(1 + 0.36)));
+  std::lognormal_distribution<double> ln(std::log(mean) - 0.5 * std::log(1 + cv * cv), std::sqrt(std::log(1 + cv * cv)));
   std::vector<int64_t> off(R + 1, 0), hoff(R + 1, 0);
   for (int r = 0; r < R; ++r) {
-    int64_t L = std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t)ln(rng)));
+    int64_t L = std::max<int64_t>(1, std::min<int64_t>(lmax, (int64_t)ln(rng)));
     off[r + 1] = off[r] + L;
     hoff[r + 1] = hoff[r] + (L + B - 1) / B;
   }
@@ -262,9 +267,13 @@ int main(int argc, char** argv) {
   };
   run("v0 4w x4", v0::k<4, 4>, 4, 4, 4 * 2 * v0::kStageBytes, 32, d_h1); check("v0 4w");
   run("v0 8w x3", v0::k<8, 3>, 8, 3, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v0 8x3");
-  run("v2 8w x2 (2 chains, 8-tok chunks)", v2::k<8, 2>, 8, 2, 8 * 2 * v2::kStageBytes, 64, d_h1); check("v2 8x2");
-  run("v2 4w x4", v2::k<4, 4>, 4, 4, 4 * 2 * v2::kStageBytes, 64, d_h1); check("v2 4x4");
-  run("v2 8w x1", v2::k<8, 1>, 8, 1, 8 * 2 * v2::kStageBytes, 64, d_h1); check("v2 8x1");
-  run("v2 4w x3", v2::k<4, 3>, 4, 3, 4 * 2 * v2::kStageBytes, 64, d_h1); check("v2 4x3");
+  run("v0 8w x1", v0::k<8, 1>, 8, 1, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v0 8x1");
+  run("v0 8w x1 3 stages", v0::k<8, 1, 3>, 8, 1, 8 * 3 * v0::kStageBytes, 32, d_h1); check("v0 8x1s3");
+  run("v0 8w x1 4 stages", v0::k<8, 1, 4>, 8, 1, 8 * 4 * v0::kStageBytes, 32, d_h1); check("v0 8x1s4");
+  run("v0 12w x1 3 stages", v0::k<12, 1, 3>, 12, 1, 12 * 3 * v0::kStageBytes, 32, d_h1); check("v0 12x1s3");
+  run("v0 4w x2 4 stages", v0::k<4, 2, 4>, 4, 2, 4 * 4 * v0::kStageBytes, 32, d_h1); check("v0 4x2s4");
+  run("v0 4w x1 6 stages", v0::k<4, 1, 6>, 4, 1, 4 * 6 * v0::kStageBytes, 32, d_h1); check("v0 4x1s6");
+  run("v0 4w x2", v0::k<4, 2>, 4, 2, 4 * 2 * v0::kStageBytes, 32, d_h1); check("v0 4x2");
+  run("v0 4w x1", v0::k<4, 1>, 4, 1, 4 * 2 * v0::kStageBytes, 32, d_h1); check("v0 4x1");
   return 0;
 }
