@@ -129,3 +129,32 @@ def test_hash_batch_all_lengths(B):
     for r in range(len(lens)):
         want = o.chain_hashes(toks[off[r]:off[r + 1]])
         assert np.array_equal(got[hoff[r]:hoff[r + 1]], want), (r, lens[r])
+
+
+def test_batch_config4_bursty_shape():
+    """Config 4 shape: lognormal prompt lengths up to 32k, 4 models interleaved over the
+    replicas, 10% unprofiled (alpha 0) reservations."""
+    from paper_2604_25899_b200 import workload as W
+    tr = W.bursty(n_requests=160, seed=4, device="cpu", mean_len=1500)
+    cl = W.make_cluster(12, 4, kv=60_000, l2=60_000, seed=6, interleave=True)
+    placed = _run(tr, cl, 16, SEQ_COMMIT, steps=2)
+    assert placed > 10
+
+
+def test_batch_config3_long_context_pressure():
+    """Config 3 shape: 32,768-token prompts sharing a 28,672-token carried context,
+    kv_capacity ~4 reservations, so capacity_holds binds alongside k_max."""
+    from paper_2604_25899_b200 import workload as W
+    tr = W.long_context(n_requests=24, seed=2, device="cpu")
+    cl = W.make_cluster(6, 1, kv=141_000, l2=200_000, seed=7)
+    placed = _run(tr, cl, 16, SEQ_COMMIT, steps=2)
+    assert placed >= 6
+
+
+@pytest.mark.parametrize("n_rep", [300, 1024])
+def test_batch_config5_many_replicas(n_rep):
+    """Config 5 sweep corner: up to 1024 replicas (16-word directory masks)."""
+    from paper_2604_25899_b200 import workload as W
+    tr = W.deep_research(n_workflows=6, seed=8, device="cpu")
+    cl = W.make_cluster(n_rep, 2, kv=30_000, l2=30_000, seed=9, interleave=True, max_bg=1)
+    _run(tr, cl, 16, SEQ_COMMIT, steps=1)
