@@ -46,6 +46,8 @@ def parse():
                     help="deep_research = config 2 (default); bursty = config 4 (per-GPU slice)")
     ap.add_argument("--requests", type=int, default=125_000, help="bursty: requests per GPU")
     ap.add_argument("--workflows", type=int, default=10_000)
+    ap.add_argument("--model-stride", type=int, default=0,
+                    help="experiments: emulate the N-GPU burst's model groups on one GPU")
     ap.add_argument("--replicas", type=int, default=32)
     ap.add_argument("--block", type=int, default=16)
     ap.add_argument("--kv", type=int, default=100_000)
@@ -132,9 +134,10 @@ def build_workload(args, rank, ws, device):
         cl = W.make_cluster(args.replicas * ws, 4, kv=args.kv, l2=args.l2, seed=0,
                             interleave=True)
         return tr, cl
+    stride = ws if ws > 1 else args.model_stride
     tr = W.deep_research(n_workflows=args.workflows, seed=1 + rank, device=device,
-                         wf_base=rank * args.workflows, model_stride=ws if ws > 1 else 0)
-    cl = W.make_cluster(args.replicas * ws, 2 * ws, kv=args.kv, l2=args.l2, seed=0)
+                         wf_base=rank * args.workflows, model_stride=stride)
+    cl = W.make_cluster(args.replicas * ws, 2 * max(stride, 1), kv=args.kv, l2=args.l2, seed=0)
     return tr, cl
 
 

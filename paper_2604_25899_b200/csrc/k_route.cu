@@ -270,7 +270,6 @@ struct SeqArgs {
 
 constexpr int kPer = 4;                 // requests per lane per scan step
 constexpr int kScan = 32 * kPer;        // requests per scan step
-constexpr int kStagedCache = 16;        // staged row entries cached in smem per request
 
 __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
   __shared__ int64_t s_free[kMaxSeqCand];
@@ -279,7 +278,6 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
   __shared__ int32_t s_rid[kMaxSeqCand];
   __shared__ int32_t s_node[kMaxSeqCand];
   __shared__ int32_t s_cnt[kMaxSeqCand];
-  __shared__ __align__(16) int32_t s_stg[kScan][kStagedCache];
   const int g = blockIdx.x;
   const int lane = threadIdx.x;
   const int c0 = A.cand_off[g], nc = min(A.cand_off[g + 1] - c0, kMaxSeqCand);
@@ -300,7 +298,6 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
     for (int j = lane; j < nc; j += 32) s_ba[j] = bound_loop(A.nodes, A.ns, s_node[j], astar);
     __syncwarp();
   }
-  const bool cache_staged = A.max_cand <= kStagedCache && (A.max_cand % 4) == 0;
   int64_t F0 = INT64_MIN, Fa = INT64_MIN;
   auto refresh = [&]() {
     int64_t f0 = INT64_MIN, fa = INT64_MIN;
@@ -373,17 +370,6 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
         t[u] = mine[u] ? tt4[u] : INT64_MAX;
       }
     }
-    if (cache_staged) {  // stage the chunk's staged rows (16 B vectors) into shared memory
-      for (int e = lane; e < kScan * (kStagedCache / 4); e += 32) {
-        const int rr = e / (kStagedCache / 4), v4 = e % (kStagedCache / 4);
-        const int r = base + rr;
-        int4 x = make_int4(0, 0, 0, 0);
-        if (r < A.R && 4 * v4 < A.max_cand)
-          x = *reinterpret_cast<const int4*>(A.staged + static_cast<int64_t>(r) * A.max_cand + 4 * v4);
-        *reinterpret_cast<int4*>(&s_stg[rr][4 * v4]) = x;
-      }
-      __syncwarp();
-    }
     int done = base - 1;
     for (;;) {
       int first = INT32_MAX;
@@ -408,9 +394,11 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
         if (u == uu) cl = __shfl_sync(kFull, cl4[u], owner);
       // classes 0 / 1 are bit-identical to +0.0 / a*; only "other" alphas are fetched
       const double a = cl == 0 ? 0.0 : (cl == 1 ? astar : A.req[first].alpha);
+      // the staged row is read where it is needed (one L2 line per evaluated request);
+      // staging every visited chunk's rows in shared memory cost more than it saved once
+      // groups interleave (probe: tools/route_probe.py)
       auto staged_of = [&](int j) -> int32_t {
-        return cache_staged ? s_stg[first - base][j]
-                            : A.staged[static_cast<int64_t>(first) * A.max_cand + j];
+        return A.staged[static_cast<int64_t>(first) * A.max_cand + j];
       };
       // full sched::route over the group's candidates (router.cpp:24-43): the
       // reference's strict lexicographic running max on (headroom, staged, -replica_id) in
