@@ -296,6 +296,8 @@ typedef struct {
   const void* l2_list;
   const uint64_t* l3_list;
   const int64_t* list_counts;
+  const int32_t* workflow;      /* lineage of its requests */
+  const int32_t* role;
 } pyg_peer;
 
 /* CUDA IPC: handle (64 bytes) + offset of the allocation holding d_ptr; import maps it into this
@@ -308,10 +310,21 @@ int pyg_ipc_import(pyg_ctx* ctx, const void* handle, int64_t offset, void** d_pt
    count (the prompt tokens placed on a replica never exceed its kv_capacity).  Lineage
    (workflow, role) of the received requests is gathered from the burst-wide arrays. */
 int pyg_shard_recv_plan_dev(pyg_ctx* ctx, int32_t R_total, const pyg_decision* d_dec,
-                            const int64_t* d_lens, const int32_t* d_wf, const int32_t* d_role,
+                            const pyg_peer* d_peers, int32_t world, const int64_t* d_req_off,
                             int64_t cap, int32_t* d_recv_gidx, int64_t* d_recv_count,
                             int64_t* d_recv_toff, int64_t* d_recv_hoff, int32_t* d_recv_wf,
                             int32_t* d_recv_role);
+/* Route inputs of this shard's requests as compact rows for the all-gather: tokens()
+   (router.hpp:19-21) and alpha (4 words), candidate group (1 word), staged row as 16-bit
+   (staged16 != 0; every prompt < 65536 tokens) or 32-bit values.  unpack rebuilds the
+   reservation as {tokens(), 0, alpha, 0}, which routes identically (capacity_holds and
+   oom_bound read only tokens() and alpha, router.cpp:7-17). */
+int pyg_shard_pack_dev(pyg_ctx* ctx, const pyg_reservation* d_req, const int32_t* d_group,
+                       const int32_t* d_staged, int32_t n_req, int32_t max_cand, int32_t staged16,
+                       int32_t* d_rows);
+int pyg_shard_unpack_dev(pyg_ctx* ctx, const int32_t* d_rows, int32_t n_req, int32_t max_cand,
+                         int32_t staged16, pyg_reservation* d_req, int32_t* d_group,
+                         int32_t* d_staged);
 /* Pull the received requests' tokens and hashes from their origin shards (peer loads). */
 int pyg_shard_pull_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world,
                        const int64_t* d_req_off, const int32_t* d_recv_gidx,

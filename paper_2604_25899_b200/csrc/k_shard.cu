@@ -73,21 +73,76 @@ __global__ void k_iota(int32_t* x, int64_t n) {
   if (i < n) x[i] = static_cast<int32_t>(i);
 }
 
-// k-th received request (0 beyond the count): global index, lineage, token / hash counts
-__global__ void k_recv_lens(const int32_t* sel, const int64_t* count, const int64_t* lens,
-                            const int32_t* wf_all, const int32_t* role_all, int64_t cap, int B,
-                            int32_t* gidx, int32_t* wf, int32_t* role, int64_t* tl, int64_t* hl) {
+// k-th received request (0 beyond the count): global index, lineage and token / hash counts,
+// read from the origin shard's HBM (peer loads)
+__global__ void k_recv_lens(const int32_t* sel, const int64_t* count, const pyg_peer* peers,
+                            int world, const int64_t* req_off, int64_t cap, int B, int32_t* gidx,
+                            int32_t* wf, int32_t* role, int64_t* tl, int64_t* hl) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k > cap) return;
   const bool in = k < *count;
   const int32_t g = in ? sel[k] : 0;
-  const int64_t L = in ? lens[g] : 0;
+  int64_t L = 0;
+  int32_t w = 0, ro = 0;
+  if (in) {
+    const int s = src_of(req_off, world, g);
+    const pyg_peer& p = peers[s];
+    const int64_t li = g - req_off[s];
+    L = p.tok_off[li + 1] - p.tok_off[li];
+    w = p.workflow[li];
+    ro = p.role[li];
+  }
   tl[k] = L;
   hl[k] = (L + B - 1) / B;
   if (k < cap) {
     gidx[k] = g;
-    wf[k] = in ? wf_all[g] : 0;
-    role[k] = in ? role_all[g] : 0;
+    wf[k] = w;
+    role[k] = ro;
+  }
+}
+
+__global__ void k_pack(const pyg_reservation* req, const int32_t* group, const int32_t* staged,
+                       int R, int mc, int s16, int32_t* rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int wd = 5 + (s16 ? (mc + 1) / 2 : mc);
+  int32_t* o = rows + static_cast<int64_t>(r) * wd;
+  const pyg_reservation q = req[r];
+  const int64_t t = res_tokens(q.prompt_len, q.upper, q.tokens_generated);
+  const int64_t ab = __double_as_longlong(q.alpha);
+  o[0] = static_cast<int32_t>(t);
+  o[1] = static_cast<int32_t>(t >> 32);
+  o[2] = static_cast<int32_t>(ab);
+  o[3] = static_cast<int32_t>(ab >> 32);
+  o[4] = group[r];
+  const int32_t* st = staged + static_cast<int64_t>(r) * mc;
+  if (s16) {
+    for (int j = 0; j < mc; j += 2) {
+      const uint32_t lo = static_cast<uint32_t>(st[j]) & 0xffffu;
+      const uint32_t hi = j + 1 < mc ? (static_cast<uint32_t>(st[j + 1]) & 0xffffu) : 0u;
+      o[5 + j / 2] = static_cast<int32_t>(lo | (hi << 16));
+    }
+  } else {
+    for (int j = 0; j < mc; ++j) o[5 + j] = st[j];
+  }
+}
+
+__global__ void k_unpack(const int32_t* rows, int R, int mc, int s16, pyg_reservation* req,
+                         int32_t* group, int32_t* staged) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int wd = 5 + (s16 ? (mc + 1) / 2 : mc);
+  const int32_t* o = rows + static_cast<int64_t>(r) * wd;
+  const int64_t t = (static_cast<int64_t>(o[1]) << 32) | static_cast<uint32_t>(o[0]);
+  const int64_t ab = (static_cast<int64_t>(o[3]) << 32) | static_cast<uint32_t>(o[2]);
+  req[r] = pyg_reservation{t, 0, __longlong_as_double(ab), 0};
+  group[r] = o[4];
+  int32_t* st = staged + static_cast<int64_t>(r) * mc;
+  if (s16) {
+    for (int j = 0; j < mc; ++j)
+      st[j] = static_cast<int32_t>((static_cast<uint32_t>(o[5 + j / 2]) >> (16 * (j & 1))) & 0xffffu);
+  } else {
+    for (int j = 0; j < mc; ++j) st[j] = o[5 + j];
   }
 }
 
@@ -267,7 +322,7 @@ int pyg_ipc_import(pyg_ctx* c, const void* handle, int64_t offset, void** d_ptr_
 }
 
 int pyg_shard_recv_plan_dev(pyg_ctx* c, int32_t R_total, const pyg_decision* d_dec,
-                            const int64_t* d_lens, const int32_t* d_wf, const int32_t* d_role,
+                            const pyg_peer* d_peers, int32_t world, const int64_t* d_req_off,
                             int64_t cap, int32_t* d_recv_gidx, int64_t* d_recv_count,
                             int64_t* d_recv_toff, int64_t* d_recv_hoff, int32_t* d_recv_wf,
                             int32_t* d_recv_role) {
@@ -308,12 +363,31 @@ int pyg_shard_recv_plan_dev(pyg_ctx* c, int32_t R_total, const pyg_decision* d_d
   k_clamp<<<1, 1, 0, c->stream>>>(d_recv_count, cap, c->hd.error);
   PYG_LAUNCHED(c);
   k_recv_lens<<<static_cast<unsigned>((cap + 1 + 255) / 256), 256, 0, c->stream>>>(
-      sel, d_recv_count, d_lens, d_wf, d_role, cap, c->B, d_recv_gidx, d_recv_wf, d_recv_role,
-      tl, hl);
+      sel, d_recv_count, d_peers, world, d_req_off, cap, c->B, d_recv_gidx, d_recv_wf,
+      d_recv_role, tl, hl);
   PYG_LAUNCHED(c);
   PYG_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, t2, tl, d_recv_toff, cap + 1, c->stream));
   PYG_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, t2, hl, d_recv_hoff, cap + 1, c->stream));
   count_launch(c, 3);
+  return PYG_OK;
+}
+
+int pyg_shard_pack_dev(pyg_ctx* c, const pyg_reservation* d_req, const int32_t* d_group,
+                       const int32_t* d_staged, int32_t R, int32_t mc, int32_t s16,
+                       int32_t* d_rows) {
+  if (!c || R < 0 || mc < 0) return PYG_EINVAL;
+  if (!R) return PYG_OK;
+  k_pack<<<(R + 255) / 256, 256, 0, c->stream>>>(d_req, d_group, d_staged, R, mc, s16, d_rows);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_shard_unpack_dev(pyg_ctx* c, const int32_t* d_rows, int32_t R, int32_t mc, int32_t s16,
+                         pyg_reservation* d_req, int32_t* d_group, int32_t* d_staged) {
+  if (!c || R < 0 || mc < 0) return PYG_EINVAL;
+  if (!R) return PYG_OK;
+  k_unpack<<<(R + 255) / 256, 256, 0, c->stream>>>(d_rows, R, mc, s16, d_req, d_group, d_staged);
+  PYG_LAUNCHED(c);
   return PYG_OK;
 }
 

@@ -8,8 +8,8 @@ the burst (global issue order = rank order, then index).  One step:
   1. K1  hash the local requests                        (local)
   2. K2  staged row of every local request against ALL its candidates, through the
          replicated L2 directory (one walk per request)  (local)
-  3. NCCL all-gather of the per-request route inputs (reservation, group, length,
-         lineage, staged row) -> every rank holds the whole burst's K3 inputs
+  3. NCCL all-gather of compact per-request route rows (tokens(), alpha, group, 16-bit
+         staged row: 52 B at 16 candidates) -> every rank holds the whole burst's K3 inputs
   4. K3  sequential-commit route of the whole burst over the global node table,
          identically on every rank (engine.cpp:650-692 order; decisions bit-equal)
   5. the owner of each target replica PULLS the placed requests' tokens and boundary
@@ -102,28 +102,6 @@ def allgather_var(t: torch.Tensor, counts) -> torch.Tensor:
     return torch.cat([g[k * cap:k * cap + counts[k]] for k in range(ws)])
 
 
-def pack_payload(res_i64: torch.Tensor, group, wf, role, lens, staged) -> torch.Tensor:
-    """Per-request route inputs as one int32 row: reservation (8 words), group, wf, role,
-    pad, length (2 words), staged row."""
-    R = res_i64.shape[0]
-    fixed = torch.empty((R, _PAYLOAD_FIXED), dtype=torch.int32, device=res_i64.device)
-    fixed[:, 0:8] = res_i64.contiguous().view(torch.int32).reshape(R, 8)
-    fixed[:, 8] = group
-    fixed[:, 9] = wf
-    fixed[:, 10] = role
-    fixed[:, 11] = 0
-    fixed[:, 12:14] = lens.to(torch.int64).reshape(R, 1).view(torch.int32).reshape(R, 2)
-    return torch.cat([fixed, staged.to(torch.int32)], dim=1)
-
-
-def unpack_payload(p: torch.Tensor):
-    R = p.shape[0]
-    res = p[:, 0:8].contiguous().view(torch.int64).reshape(R, 4)
-    lens = p[:, 12:14].contiguous().view(torch.int64).reshape(R)
-    return (res, p[:, 8].contiguous(), p[:, 9].contiguous(), p[:, 10].contiguous(), lens,
-            p[:, _PAYLOAD_FIXED:].contiguous())
-
-
 def csr_offsets(lens: torch.Tensor) -> torch.Tensor:
     off = torch.zeros(lens.numel() + 1, dtype=torch.int64, device=lens.device)
     torch.cumsum(lens.to(torch.int64), 0, out=off[1:])
@@ -131,7 +109,7 @@ def csr_offsets(lens: torch.Tensor) -> torch.Tensor:
 
 
 WINDOW_FIELDS = ("tokens", "tok_off", "hashes", "hash_off", "recv_gidx", "recv_count", "admitted",
-                 "match3", "l2_list", "l3_list", "list_counts")  # == pyg_peer (include/pyg.h)
+                 "match3", "l2_list", "l3_list", "list_counts", "workflow", "role")  # == pyg_peer
 
 
 def exchange_windows(local_ptrs, export, import_):
@@ -204,7 +182,8 @@ class ShardedStep:
         self.rep_off_d = torch.as_tensor(plan.rep_off, dtype=i64, device=device)
         self.req_off_d = torch.as_tensor(plan.req_off, dtype=i64, device=device)
         local = [batch.tokens, batch.tok_off, batch.hashes, batch.hash_off, self.recv_gidx,
-                 self.recv_count, self.adm, self.m3, self.l2_list, self.l3_list, self.counts]
+                 self.recv_count, self.adm, self.m3, self.l2_list, self.l3_list, self.counts,
+                 batch.wf, batch.role]
         lib = _lib._lib
 
         def export(t):
@@ -219,7 +198,19 @@ class ShardedStep:
             return p.value
 
         wins = exchange_windows([t.data_ptr() for t in local], export, import_)
-        self.peers = torch.tensor(wins, dtype=torch.int64, device=device)  # [world, 11]
+        self.peers = torch.tensor(wins, dtype=torch.int64, device=device)  # [world, 13]
+        # compact route rows: 16-bit staged values when every prompt of the burst is < 64k
+        lmax = torch.zeros(1, dtype=torch.int64, device=device)
+        if R:
+            lmax[0] = self.lens.max()
+        if dist.is_initialized() and dist.get_world_size() > 1:
+            dist.all_reduce(lmax, op=dist.ReduceOp.MAX)
+        self.s16 = int(int(lmax.item()) < 65536)
+        self.row_words = 5 + ((mc + 1) // 2 if self.s16 else mc)
+        self.rows = z(max(R, 1), self.row_words, dt=i32)
+        self.g_res = z(max(Rt, 1), 4)
+        self.g_group = z(max(Rt, 1), dt=i32)
+        self.g_staged = z(max(Rt, 1), mc, dt=i32)
 
     # ---------------------------------------------------------------- directory
     def build_directory(self):
@@ -261,11 +252,16 @@ class ShardedStep:
                                         nodes.n_groups, _ptr(nodes.cand_off), _ptr(nodes.cand),
                                         nodes.max_cand, _ptr(self.staged)))
         mark("hash+staged")
-        # 3: all-gather route inputs (also the barrier that frees last step's shared buffers)
-        pay = pack_payload(b.res[:plan.R_local], b.group[:plan.R_local], b.wf[:plan.R_local],
-                           b.role[:plan.R_local], self.lens, self.staged[:plan.R_local])
-        g_res, g_group, g_wf, g_role, g_lens, g_staged = unpack_payload(
-            allgather_var(pay, self.req_counts) if dist.is_initialized() else pay)
+        # 3: all-gather compact route rows (also the barrier that frees last step's shared
+        # buffers); every rank unpacks the whole burst's reservations, groups, staged rows
+        mc = max(nodes.max_cand, 1)
+        check(lib.pyg_shard_pack_dev(ctx.h, _ptr(b.res), _ptr(b.group), _ptr(self.staged),
+                                     plan.R_local, mc, self.s16, _ptr(self.rows)))
+        g_rows = (allgather_var(self.rows[:plan.R_local], self.req_counts)
+                  if dist.is_initialized() else self.rows[:plan.R_local])
+        check(lib.pyg_shard_unpack_dev(ctx.h, _ptr(g_rows), plan.R_total, mc, self.s16,
+                                       _ptr(self.g_res), _ptr(self.g_group), _ptr(self.g_staged)))
+        g_res, g_group, g_staged = self.g_res, self.g_group, self.g_staged
         mark("allgather")
         # 4: route the whole burst (identical on every rank)
         ns = nodes.struct()
@@ -276,8 +272,8 @@ class ShardedStep:
                                       _ptr(self.placed)))
         mark("route")
         # 5: requests placed on my replicas: plan, pull their tokens/hashes from the origins
-        check(lib.pyg_shard_recv_plan_dev(ctx.h, plan.R_total, _ptr(self.decisions), _ptr(g_lens),
-                                          _ptr(g_wf), _ptr(g_role), self.cap_req,
+        check(lib.pyg_shard_recv_plan_dev(ctx.h, plan.R_total, _ptr(self.decisions), _ptr(self.peers),
+                                          W, _ptr(self.req_off_d), self.cap_req,
                                           _ptr(self.recv_gidx), _ptr(self.recv_count),
                                           _ptr(self.recv_toff), _ptr(self.recv_hoff),
                                           _ptr(self.recv_wf), _ptr(self.recv_role)))

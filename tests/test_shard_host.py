@@ -31,7 +31,7 @@ def _worker(rank, world, port, q):
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         from paper_2604_25899_b200.shard import (ShardPlan, allgather_cat, allgather_var,
-                                                 exchange_windows, pack_payload, unpack_payload)
+                                                 exchange_windows)
         B = 16
         rng = np.random.default_rng(0)  # same global data on every rank
         reps = [3, 5, 2][:world]
@@ -47,17 +47,11 @@ def _worker(rank, world, port, q):
         want = [-1] + [int(np.searchsorted(plan.rep_off[1:], t, side="right"))
                        for t in range(n_global)]
         assert plan.owner(tg).tolist() == want
-        # payload round trip through the variable all-gather (ranks hold different R)
-        res = torch.from_numpy(rng.integers(0, 1 << 40, (R, 4)))
-        grp = torch.from_numpy(rng.integers(0, 5, R).astype(np.int32))
-        stg = torch.from_numpy(rng.integers(0, 9999, (R, 3)).astype(np.int32))
-        L = torch.from_numpy(lens.astype(np.int64))
-        pay = pack_payload(res[lo:hi], grp[lo:hi], grp[lo:hi] + 1, grp[lo:hi] + 2, L[lo:hi],
-                           stg[lo:hi])
-        g = unpack_payload(allgather_var(pay, reqs))
-        assert torch.equal(g[0], res) and torch.equal(g[1], grp) and torch.equal(g[4], L)
-        assert torch.equal(g[2], grp + 1) and torch.equal(g[3], grp + 2)
-        assert torch.equal(g[5], stg)
+        # route rows through the variable all-gather (ranks hold different R; global order)
+        rows = torch.from_numpy(rng.integers(-(1 << 31), 1 << 31, (R, 13)).astype(np.int32))
+        g = allgather_var(rows[lo:hi].contiguous(), reqs)
+        assert torch.equal(g, rows)
+        assert lens.shape[0] == R
         mine = torch.arange(rank + 1, dtype=torch.int64) + 100 * rank
         allv = allgather_var(mine, [k + 1 for k in range(world)])
         assert allv.tolist() == [100 * k + i for k in range(world) for i in range(k + 1)]
