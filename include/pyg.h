@@ -92,6 +92,9 @@ int pyg_set_stream(pyg_ctx* ctx, void* cuda_stream);
 int pyg_synchronize(pyg_ctx* ctx);
 /* number of kernels this ctx has launched (for the bench's gpu_launches claim) */
 int64_t pyg_kernel_launches(pyg_ctx* ctx);
+/* (Re)sets a replica's tier capacities -- CacheHierarchy(l1_capacity, l2_capacity)
+   (hierarchy.hpp:100) for a replica slot the engine provisions later (engine.cpp:197, 1482). */
+int pyg_set_capacity(pyg_ctx* ctx, int32_t replica, int64_t l1_capacity, int64_t l2_capacity);
 
 /* ------------------------------------------------------------- hashing */
 /* chain_boundary_hashes (hierarchy.cpp:21-30).  out holds ceil(n/B) hashes. */

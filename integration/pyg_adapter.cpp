@@ -1,0 +1,398 @@
+// integration/pyg_adapter.cpp -- the reference-side binding a maintainer adds.
+//
+// Implements the reference's cache (hierarchy.hpp, manager.hpp) and router
+// (router.hpp) interfaces over the C-ABI of libpyg_b200.so, so the reference's
+// own simulator engine (src/sim/engine.cpp, unmodified) runs its hot path on a
+// B200: lookups, inserts, pins, eviction, completion sweeps, staging lookups and
+// every routing decision are device calls.  Compiled with the overlay headers in
+// integration/overlay first on the include path (integration/Makefile).
+//
+// One pyg_ctx holds every replica of the simulation (slots handed out in the
+// order the engine constructs CacheHierarchy objects) plus the shared L3.
+// Workflow / role strings are interned to ints; role ids must stay < 64.
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "pyg.h"
+#include "pythia/cache/hierarchy.hpp"
+#include "pythia/cache/manager.hpp"
+#include "pythia/sched/router.hpp"
+
+namespace {
+
+void check(int rc) {
+  if (rc != PYG_OK) throw std::runtime_error(std::string("libpyg_b200: ") + pyg_last_error());
+}
+
+struct Backend {
+  pyg_ctx* ctx = nullptr;
+  int32_t next_slot = 0;
+  int32_t max_slots = 0;
+  std::unordered_map<std::string, int32_t> wf_ids, role_ids;
+  std::vector<std::string> wf_names, role_names;
+  std::vector<pyg_block> dump_buf;
+
+  static Backend& get() {
+    static Backend b;
+    if (!b.ctx) b.create();
+    return b;
+  }
+
+  void create() {
+    const char* e = std::getenv("PYG_ENGINE_MAX_REPLICAS");
+    max_slots = e ? std::atoi(e) : 64;
+    const char* d = std::getenv("PYG_ENGINE_DEVICE");
+    std::vector<int64_t> zero(max_slots, 0);
+    pyg_config cfg{static_cast<int32_t>(pythia::cache::kBlockTokens), max_slots, d ? std::atoi(d) : 0,
+                   0, zero.data(), zero.data(), 4096};
+    check(pyg_create(&cfg, &ctx));
+  }
+
+  int32_t wf(const std::string& s) {
+    auto it = wf_ids.find(s);
+    if (it != wf_ids.end()) return it->second;
+    const int32_t id = static_cast<int32_t>(wf_names.size());
+    wf_ids.emplace(s, id);
+    wf_names.push_back(s);
+    return id;
+  }
+  int32_t role(const std::string& s) {
+    auto it = role_ids.find(s);
+    if (it != role_ids.end()) return it->second;
+    const int32_t id = static_cast<int32_t>(role_names.size());
+    if (id >= 64) throw std::runtime_error("libpyg_b200 adapter: more than 64 distinct roles");
+    role_ids.emplace(s, id);
+    role_names.push_back(s);
+    return id;
+  }
+  uint64_t mask(const std::set<std::string>& roles) {
+    uint64_t m = 0;
+    for (const auto& r : roles) m |= 1ULL << role(r);
+    return m;
+  }
+  pythia::cache::CacheBlock block(const pyg_block& b) const {
+    pythia::cache::CacheBlock x;
+    x.block_id = b.block_id;
+    x.chain_hash = b.chain_hash;
+    x.span_start = b.span_start;
+    x.span_end = b.span_end;
+    x.lineage = {wf_names.at(b.workflow), role_names.at(b.role)};
+    x.last_access = b.last_access;
+    x.pin_count = b.pin_count;
+    return x;
+  }
+};
+
+int32_t api_slot(int32_t slot) { return slot < 0 ? 0 : slot; }
+
+}  // namespace
+
+namespace pythia::cache {
+
+const char* tier_name(Tier t) {
+  return t == Tier::L1 ? "L1" : t == Tier::L2 ? "L2" : "L3";
+}
+
+std::vector<uint64_t> chain_boundary_hashes(const workflow::TokenSeq& tokens) {
+  Backend& b = Backend::get();
+  std::vector<uint64_t> out((tokens.size() + kBlockTokens - 1) / kBlockTokens);
+  int64_t n = 0;
+  check(pyg_chain_hashes(b.ctx, tokens.data(), static_cast<int64_t>(tokens.size()), out.data(), &n));
+  out.resize(n);
+  return out;
+}
+
+// ------------------------------------------------------------------ TierStore
+TierStore::TierStore(int64_t) : slot_(-1), tier_(2) {}
+
+int64_t TierStore::capacity() const {
+  int64_t occ, cap, n;
+  check(pyg_tier_stats(Backend::get().ctx, api_slot(slot_), tier_, &occ, &cap, &n));
+  return cap;
+}
+
+int64_t TierStore::occupancy() const {
+  int64_t occ, cap, n;
+  check(pyg_tier_stats(Backend::get().ctx, api_slot(slot_), tier_, &occ, &cap, &n));
+  return occ;
+}
+
+const std::map<uint64_t, CacheBlock>& TierStore::blocks() const {
+  Backend& b = Backend::get();
+  int64_t n = 0;
+  if (b.dump_buf.empty()) b.dump_buf.resize(1 << 14);
+  for (;;) {
+    check(pyg_tier_dump(b.ctx, api_slot(slot_), tier_, b.dump_buf.data(),
+                        static_cast<int64_t>(b.dump_buf.size()), &n));
+    if (n <= static_cast<int64_t>(b.dump_buf.size())) break;
+    b.dump_buf.resize(2 * n);
+  }
+  view_.clear();
+  for (int64_t i = 0; i < n; ++i)
+    if (b.dump_buf[i].alive) view_.emplace_hint(view_.end(), b.dump_buf[i].block_id, b.block(b.dump_buf[i]));
+  return view_;
+}
+
+const CacheBlock* TierStore::find_chain(uint64_t chain_hash) const {
+  Backend& b = Backend::get();
+  pyg_block x{};
+  int32_t found = 0;
+  check(pyg_tier_find(b.ctx, api_slot(slot_), tier_, chain_hash, &x, &found));
+  if (!found) return nullptr;
+  found_ = b.block(x);
+  return &found_;
+}
+
+CacheBlock* TierStore::find_chain_mut(uint64_t chain_hash) {
+  return const_cast<CacheBlock*>(static_cast<const TierStore*>(this)->find_chain(chain_hash));
+}
+
+uint64_t TierStore::put(uint64_t chain_hash, int64_t span_start, int64_t span_end,
+                        const Lineage& lineage, double now, int pin_delta, uint64_t*) {
+  Backend& b = Backend::get();
+  uint64_t id = 0;
+  check(pyg_tier_put(b.ctx, api_slot(slot_), tier_, chain_hash, span_start, span_end,
+                     b.wf(lineage.workflow_id), b.role(lineage.role_id), now, pin_delta, &id));
+  return id;
+}
+
+void TierStore::erase(uint64_t block_id) {
+  check(pyg_tier_erase(Backend::get().ctx, api_slot(slot_), tier_, block_id));
+}
+
+int64_t TierStore::matched_prefix(const workflow::TokenSeq& tokens,
+                                  const std::vector<uint64_t>&) const {
+  int64_t m = 0;
+  check(pyg_matched_prefix(Backend::get().ctx, api_slot(slot_), tier_, tokens.data(),
+                           static_cast<int64_t>(tokens.size()), &m));
+  return m;
+}
+
+// ------------------------------------------------------------- CacheHierarchy
+CacheHierarchy::CacheHierarchy(int64_t l1_capacity, int64_t l2_capacity)
+    : slot_(Backend::get().next_slot++), l1_(slot_, 0), l2_(slot_, 1) {
+  Backend& b = Backend::get();
+  if (slot_ >= b.max_slots)
+    throw std::runtime_error("libpyg_b200 adapter: raise PYG_ENGINE_MAX_REPLICAS");
+  check(pyg_set_capacity(b.ctx, slot_, l1_capacity, l2_capacity));
+}
+
+CacheHierarchy::Match CacheHierarchy::lookup(const workflow::TokenSeq& prompt,
+                                             const SharedL3* l3) const {
+  int64_t m[3];
+  check(pyg_lookup(Backend::get().ctx, slot_, prompt.data(), static_cast<int64_t>(prompt.size()),
+                   l3 != nullptr, m));
+  return {m[0], m[1], m[2]};
+}
+
+void CacheHierarchy::insert_chain(Tier t, const workflow::TokenSeq& tokens, int64_t upto,
+                                  const Lineage& lineage, double now, int pin_delta) {
+  Backend& b = Backend::get();
+  check(pyg_insert_chain(b.ctx, slot_, static_cast<int32_t>(t), tokens.data(),
+                         static_cast<int64_t>(tokens.size()), upto, b.wf(lineage.workflow_id),
+                         b.role(lineage.role_id), now, pin_delta));
+}
+
+void CacheHierarchy::unpin_chain(const workflow::TokenSeq& tokens, int64_t upto) {
+  check(pyg_unpin_chain(Backend::get().ctx, slot_, tokens.data(),
+                        static_cast<int64_t>(tokens.size()), upto));
+}
+
+void CacheHierarchy::add_decode_tokens(int64_t n) {
+  check(pyg_add_decode_tokens(Backend::get().ctx, slot_, n));
+}
+
+int64_t CacheHierarchy::l1_occupancy() const {
+  int64_t o = 0;
+  check(pyg_l1_occupancy(Backend::get().ctx, slot_, &o));
+  return o;
+}
+
+int64_t CacheHierarchy::decode_tokens() const { return l1_occupancy() - l1_.occupancy(); }
+
+// ------------------------------------------------------------------- manager
+std::set<std::string> future_nodes(const workflow::PathCursor& position) {
+  return workflow::future_roles(position);
+}
+
+void FutureRegistry::update(const std::string& workflow_id, std::set<std::string> roles) {
+  Backend& b = Backend::get();
+  check(pyg_registry_update(b.ctx, b.wf(workflow_id), b.mask(roles)));
+  futures_[workflow_id] = std::move(roles);
+}
+
+void FutureRegistry::drop(const std::string& workflow_id) {
+  Backend& b = Backend::get();
+  check(pyg_registry_drop(b.ctx, b.wf(workflow_id)));
+  futures_.erase(workflow_id);
+}
+
+bool FutureRegistry::lineage_live(const Lineage& lineage) const {
+  auto it = futures_.find(lineage.workflow_id);
+  return it != futures_.end() && it->second.count(lineage.role_id) > 0;
+}
+
+// manager.cpp:25-42 over a device dump of the replica's L1 and L2
+std::vector<CompletionAction> on_request_complete(const workflow::RequestEnvelope& req,
+                                                  const CacheHierarchy& cache) {
+  std::vector<CompletionAction> out;
+  if (req.unprofiled() || !req.position) return out;
+  const std::set<std::string> future = future_nodes(*req.position);
+  for (Tier t : {Tier::L1, Tier::L2}) {
+    for (const auto& [id, blk] : cache.tier(t).blocks()) {
+      if (blk.pinned() || blk.lineage.workflow_id != req.app_metadata.workflow_id) continue;
+      out.push_back({future.count(blk.lineage.role_id) ? CompletionAction::Kind::RetainAndWriteL3
+                                                       : CompletionAction::Kind::Free,
+                     t, id});
+    }
+  }
+  return out;
+}
+
+// manager.cpp:44-58: one dump per tier, then device erases / L3 puts in action order
+void apply_completion(const std::vector<CompletionAction>& actions, CacheHierarchy& cache,
+                      SharedL3& l3, double now) {
+  std::map<uint64_t, CacheBlock> view[2];
+  bool have[2] = {false, false};
+  for (const auto& a : actions) {
+    const int k = a.tier == Tier::L1 ? 0 : 1;
+    if (!have[k]) {
+      view[k] = cache.tier(a.tier).blocks();
+      have[k] = true;
+    }
+    auto it = view[k].find(a.block_id);
+    if (it == view[k].end()) continue;
+    if (a.kind == CompletionAction::Kind::Free) {
+      cache.tier(a.tier).erase(a.block_id);
+      view[k].erase(it);
+    } else {
+      const CacheBlock& blk = it->second;
+      l3.store().put(blk.chain_hash, blk.span_start, blk.span_end, blk.lineage, now, 0,
+                     l3.id_counter());
+    }
+  }
+}
+
+// manager.cpp:60-100 with device lookups
+std::vector<StageAction> on_prefetch_requested(const workflow::RequestEnvelope& req,
+                                               const CacheHierarchy& target_cache,
+                                               const SharedL3& l3,
+                                               const workflow::PromptHistory& history,
+                                               bool gpu_idle) {
+  std::vector<StageAction> out;
+  if (req.unprofiled()) return out;
+  for (const auto& [role, tmpl] : req.sys_annotations->prompt_composition) {
+    StageAction a;
+    a.successor_role = role;
+    a.lineage = {req.app_metadata.workflow_id, role};
+    auto prefix = workflow::assemble_resolvable_prefix(tmpl, history);
+    if (prefix.tokens.empty()) {
+      a.reason = "unresolved";
+      out.push_back(std::move(a));
+      continue;
+    }
+    a.tokens = std::move(prefix.tokens);
+    const int64_t len = static_cast<int64_t>(a.tokens.size());
+    const auto m = target_cache.lookup(a.tokens, &l3);
+    const int64_t staged = std::max(m.l1, m.l2);
+    if (staged >= len) {
+      a.reason = "already-staged";
+    } else if (m.l3 > staged) {
+      a.kind = StageAction::Kind::PromoteToHost;
+      a.from = staged;
+      a.to = m.l3;
+    } else if (gpu_idle) {
+      a.kind = StageAction::Kind::BackgroundPrefill;
+      a.from = staged;
+      a.to = len;
+    } else {
+      a.reason = "gpu-busy";
+    }
+    out.push_back(std::move(a));
+  }
+  return out;
+}
+
+EvictionResult evict_for_space(CacheHierarchy& cache, Tier tier, int64_t needed,
+                               const FutureRegistry&, bool speculative) {
+  Backend& b = Backend::get();
+  static std::vector<uint64_t> ids(1 << 20);
+  int64_t n = 0, ft = 0;
+  int32_t ok = 0;
+  check(pyg_evict_for_space(b.ctx, cache.tier(Tier::L1).slot(), static_cast<int32_t>(tier), needed,
+                            speculative, ids.data(), static_cast<int64_t>(ids.size()), &n, &ft,
+                            &ok));
+  if (n > static_cast<int64_t>(ids.size()))
+    throw std::runtime_error("libpyg_b200 adapter: eviction list longer than 2^20 blocks");
+  EvictionResult r;
+  r.freed.assign(ids.begin(), ids.begin() + n);
+  r.freed_tokens = ft;
+  r.satisfied = ok != 0;
+  return r;
+}
+
+}  // namespace pythia::cache
+
+// -------------------------------------------------------------------- router
+namespace pythia::sched {
+
+bool capacity_holds(const NodeView& node, const Reservation& req) {
+  int64_t sum = req.tokens();
+  for (const auto& a : node.assigned) sum += a.tokens();
+  return sum <= node.kv_capacity;
+}
+
+double oom_bound(const NodeView& node, const Reservation& req) {
+  double b = req.alpha;
+  for (const auto& a : node.assigned) b += a.alpha;
+  return b;
+}
+
+RoutingDecision route(const std::vector<NodeView>& nodes, const Reservation& req, double eps) {
+  Backend& b = Backend::get();
+  const int32_t n = static_cast<int32_t>(nodes.size());
+  std::vector<int32_t> rid(n);
+  std::vector<int64_t> kv(n), off(n + 1, 0), staged(n);
+  std::vector<pyg_reservation> asg;
+  for (int32_t i = 0; i < n; ++i) {
+    rid[i] = nodes[i].replica_id;
+    kv[i] = nodes[i].kv_capacity;
+    staged[i] = nodes[i].staged_l2_prefix;
+    for (const auto& a : nodes[i].assigned)
+      asg.push_back({a.prompt_len, a.upper, a.alpha, a.tokens_generated});
+    off[i + 1] = static_cast<int64_t>(asg.size());
+  }
+  const pyg_reservation q{req.prompt_len, req.upper, req.alpha, req.tokens_generated};
+  if (asg.empty()) asg.push_back({0, 0, 0.0, 0});  // never read: off[n] == 0
+  pyg_decision d{};
+  check(pyg_route(b.ctx, n, rid.data(), kv.data(), off.data(), asg.data(), staged.data(), &q, eps,
+                  &d));
+  RoutingDecision out;
+  if (d.target >= 0) out.target = d.target;
+  out.headroom = d.headroom;
+  out.oom_bound = d.oom_bound;
+  out.cache_tiebreak_used = d.tiebreak != 0;
+  return out;
+}
+
+std::optional<int> route_least_outstanding(const std::vector<NodeView>& nodes) {
+  Backend& b = Backend::get();
+  const int32_t n = static_cast<int32_t>(nodes.size());
+  if (n == 0) return std::nullopt;
+  std::vector<int32_t> rid(n);
+  std::vector<int64_t> off(n + 1, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    rid[i] = nodes[i].replica_id;
+    off[i + 1] = off[i] + static_cast<int64_t>(nodes[i].assigned.size());
+  }
+  int32_t t = -1;
+  check(pyg_route_least_outstanding(b.ctx, n, rid.data(), off.data(), &t));
+  if (t < 0) return std::nullopt;
+  return t;
+}
+
+}  // namespace pythia::sched

@@ -280,4 +280,18 @@ int pyg_synchronize(pyg_ctx* c) {
 
 int64_t pyg_kernel_launches(pyg_ctx* c) { return c ? c->launches : 0; }
 
+int pyg_set_capacity(pyg_ctx* c, int32_t replica, int64_t l1_capacity, int64_t l2_capacity) {
+  if (!c || replica < 0 || replica >= c->n_rep || l1_capacity < 0 || l2_capacity < 0)
+    return PYG_EINVAL;
+  const int64_t caps[2] = {l1_capacity, l2_capacity};
+  for (int k = 0; k < 2; ++k) {
+    const int ti = 2 * replica + k;
+    c->tiers[ti].d.capacity = caps[k];
+    PYG_CUDA(cudaMemcpyAsync(&c->d_tiers[ti].capacity, &caps[k], sizeof(int64_t),
+                             cudaMemcpyHostToDevice, c->stream));
+  }
+  PYG_CUDA(cudaStreamSynchronize(c->stream));
+  return PYG_OK;
+}
+
 }  // extern "C"
