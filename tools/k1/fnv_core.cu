@@ -84,6 +84,38 @@ __device__ __forceinline__ uint64_t f_lea2(uint64_t h, uint64_t v) {
   return ((uint64_t)hi << 32) | lo;
 }
 
+// h' = x*435 + {hi*435 + (x << 8), 0}: one IMAD.WIDE with the high half as its 64-bit addend
+__device__ __forceinline__ uint64_t f_wacc(uint64_t h, uint64_t v) {
+  uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
+  const uint32_t vl = (uint32_t)v, vh = (uint32_t)(v >> 32);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t w = i < 4 ? vl : vh;
+    const uint32_t x = lo ^ ((w >> (8 * (i & 3))) & 0xffu);
+    const uint32_t u = hi * 435u + (x << 8);
+    uint64_t r;
+    asm("mad.wide.u32 %0, %1, 435, %2;" : "=l"(r) : "r"(x), "l"((uint64_t)u << 32));
+    lo = (uint32_t)r;
+    hi = (uint32_t)(r >> 32);
+  }
+  return ((uint64_t)hi << 32) | lo;
+}
+// same, the low half computed separately (short lo chain) and the pair only for hi
+__device__ __forceinline__ uint64_t f_wacc2(uint64_t h, uint64_t v) {
+  uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
+  const uint32_t vl = (uint32_t)v, vh = (uint32_t)(v >> 32);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t w = i < 4 ? vl : vh;
+    const uint32_t x = lo ^ ((w >> (8 * (i & 3))) & 0xffu);
+    uint32_t c;
+    asm("mul.hi.u32 %0, %1, 435;" : "=r"(c) : "r"(x));
+    hi = hi * 435u + (x << 8) + c;
+    lo = x * 435u;
+  }
+  return ((uint64_t)hi << 32) | lo;
+}
+
 template <int V>
 __global__ void __launch_bounds__(256) bench(uint64_t* out, int ntok, uint64_t seed) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -97,6 +129,8 @@ __global__ void __launch_bounds__(256) bench(uint64_t* out, int ntok, uint64_t s
     if (V == 3) h = f_prmt(h, v);
     if (V == 4) h = f_lea(h, v);
     if (V == 5) h = f_lea2(h, v);
+    if (V == 6) h = f_wacc(h, v);
+    if (V == 7) h = f_wacc2(h, v);
   }
   out[t] = h;
 }
@@ -105,12 +139,12 @@ int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   uint64_t* d; cudaMalloc(&d, 8ull << 22);
   const int ntok = 4096;
-  const char* names[] = {"fnv_token (product)", "plain u64 *= P", "split IMAD.HI + PRMT", "PRMT byte extract", "mad hi + LEA", "mad hi + shf + add"};
-  for (int blocks_per_sm : {0, 8}) {
+  const char* names[] = {"fnv_token (product)", "plain u64 *= P", "split IMAD.HI + PRMT", "PRMT byte extract", "mad hi + LEA", "mad hi + shf + add", "wide with hi addend", "mul.hi + lo split"};
+  for (int blocks_per_sm : {0, 2, 8}) {
     const int grid = blocks_per_sm ? nsm * blocks_per_sm : nsm;  // 0: one warp per SM (latency)
     const int threads = blocks_per_sm ? 256 : 32;
-    uint64_t ref[6] = {0, 0, 0, 0, 0, 0};
-    for (int V = 0; V < 6; ++V) {
+    uint64_t ref[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int V = 0; V < 8; ++V) {
       cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
       auto launch = [&]() {
         if (V == 0) bench<0><<<grid, threads>>>(d, ntok, 7);
@@ -119,6 +153,8 @@ int main() {
         if (V == 3) bench<3><<<grid, threads>>>(d, ntok, 7);
         if (V == 4) bench<4><<<grid, threads>>>(d, ntok, 7);
         if (V == 5) bench<5><<<grid, threads>>>(d, ntok, 7);
+        if (V == 6) bench<6><<<grid, threads>>>(d, ntok, 7);
+        if (V == 7) bench<7><<<grid, threads>>>(d, ntok, 7);
       };
       launch();
       cudaEventRecord(a); launch(); cudaEventRecord(b); cudaEventSynchronize(b);

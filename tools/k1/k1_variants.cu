@@ -197,6 +197,125 @@ k(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int 
 }
 }  // namespace v2
 
+
+// ---------------- V3: v0 + per-lane direct loads (no staging) for tasks longer than kLong tokens
+namespace v3 {
+using v0::kChunk; using v0::kRowBytes; using v0::kStageBytes;
+__device__ __forceinline__ void hash_direct(const uint64_t* __restrict__ p, int64_t n, int B,
+                                            uint64_t* __restrict__ out) {
+  uint64_t h = kFnvOffset;
+  int64_t k = 0;
+  int cnt = 0;
+  int64_t i = 0;
+  if (n > 0 && (reinterpret_cast<uintptr_t>(p) & 8)) {
+    h = fnv_token(h, __ldg(p));
+    i = 1;
+    if (++cnt == B) { out[k++] = h; cnt = 0; }
+  }
+  const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p + i);
+  const int64_t npair = (n - i) / 2;
+  constexpr int U = 8;  // pairs per group (16 tokens)
+  ulonglong2 cur[U], nxt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) cur[u] = u < npair ? __ldg(q + u) : make_ulonglong2(0, 0);
+  for (int64_t g = 0; g < npair; g += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) nxt[u] = g + U + u < npair ? __ldg(q + g + U + u) : make_ulonglong2(0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (g + u < npair) {
+        h = fnv_token(h, cur[u].x);
+        if (++cnt == B) { out[k++] = h; cnt = 0; }
+        h = fnv_token(h, cur[u].y);
+        if (++cnt == B) { out[k++] = h; cnt = 0; }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+  }
+  for (int64_t j = i + 2 * npair; j < n; ++j) {
+    h = fnv_token(h, __ldg(p + j));
+    if (++cnt == B) { out[k++] = h; cnt = 0; }
+  }
+  if (cnt > 0) out[k++] = h;
+}
+
+template <int kWarps, int kMinB, int kLong>
+__global__ void __launch_bounds__(kWarps * 32, kMinB)
+k(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int R,
+  const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
+  uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbuf = smem + warp * 2 * kStageBytes;
+  const int ntasks = (R + 31) / 32;
+  for (;;) {
+    int task = 0;
+    if (lane == 0) task = atomicAdd(next_task, 1);
+    task = __shfl_sync(kFull, task, 0);
+    if (task >= ntasks) break;
+    const int idx = task * 32 + lane;
+    const bool valid = idx < R;
+    const int r = valid ? order[idx] : 0;
+    const int64_t s = valid ? tok_off[r] : 0;
+    const int64_t n = valid ? tok_off[r + 1] - s : 0;
+    const int nch = static_cast<int>((n + kChunk - 1) / kChunk);
+    const int maxch = __reduce_max_sync(kFull, nch);
+    if (maxch == 0) continue;
+    uint64_t* out = hashes + (valid ? hash_off[r] : 0);
+    if (maxch * kChunk >= kLong) {
+      if (valid) hash_direct(tokens + s, n, B, out);
+      __syncwarp();
+      continue;
+    }
+    const int cpb = B / kChunk;
+    int cc = cpb;
+    const int sub = lane >> 4, q = lane & 15;
+    auto issue = [&](int c) {
+      unsigned char* st = wbuf + (c & 1) * kStageBytes;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const int jj = j + sub;
+        const int64_t sj = __shfl_sync(kFull, s, jj);
+        const int64_t nj = __shfl_sync(kFull, n, jj);
+        const int64_t pos = static_cast<int64_t>(c) * kChunk + q;
+        if (pos < nj) cp_async8(st + jj * kRowBytes + q * 8, tokens + sj + pos, 8);
+      }
+      cp_commit();
+    };
+    uint64_t h = kFnvOffset;
+    int64_t kk = 0;
+    issue(0);
+    for (int c = 0; c < maxch; ++c) {
+      if (c + 1 < maxch) issue(c + 1); else cp_commit();
+      cp_wait1();
+      __syncwarp();
+      if (c < nch) {
+        const unsigned char* row = wbuf + (c & 1) * kStageBytes + lane * kRowBytes;
+        const int64_t rem = n - static_cast<int64_t>(c) * kChunk;
+        if (rem >= kChunk) {
+#pragma unroll
+          for (int x = 0; x < kChunk / 2; ++x) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(row + 16 * x);
+            h = fnv_token(h, v.x);
+            h = fnv_token(h, v.y);
+          }
+          if (--cc == 0 || rem == kChunk) { out[kk++] = h; cc = cpb; }
+        } else {
+          const int p1 = static_cast<int>(rem);
+          for (int p = 0; p < p1; ++p) {
+            h = fnv_token(h, *reinterpret_cast<const uint64_t*>(row + 8 * p));
+            const int64_t j = static_cast<int64_t>(c) * kChunk + p;
+            if ((j + 1) % B == 0 || j + 1 == n) out[kk++] = h;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+}  // namespace v3
+
 __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
@@ -265,15 +384,11 @@ int main(int argc, char** argv) {
     if (got != ref) printf("  !! %s MISMATCH\n", name);
     CK(cudaMemset(d_h1, 0, H * 8));
   };
-  run("v0 4w x4", v0::k<4, 4>, 4, 4, 4 * 2 * v0::kStageBytes, 32, d_h1); check("v0 4w");
-  run("v0 8w x3", v0::k<8, 3>, 8, 3, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v0 8x3");
   run("v0 8w x1", v0::k<8, 1>, 8, 1, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v0 8x1");
-  run("v0 8w x1 3 stages", v0::k<8, 1, 3>, 8, 1, 8 * 3 * v0::kStageBytes, 32, d_h1); check("v0 8x1s3");
-  run("v0 8w x1 4 stages", v0::k<8, 1, 4>, 8, 1, 8 * 4 * v0::kStageBytes, 32, d_h1); check("v0 8x1s4");
-  run("v0 12w x1 3 stages", v0::k<12, 1, 3>, 12, 1, 12 * 3 * v0::kStageBytes, 32, d_h1); check("v0 12x1s3");
-  run("v0 4w x2 4 stages", v0::k<4, 2, 4>, 4, 2, 4 * 4 * v0::kStageBytes, 32, d_h1); check("v0 4x2s4");
-  run("v0 4w x1 6 stages", v0::k<4, 1, 6>, 4, 1, 4 * 6 * v0::kStageBytes, 32, d_h1); check("v0 4x1s6");
-  run("v0 4w x2", v0::k<4, 2>, 4, 2, 4 * 2 * v0::kStageBytes, 32, d_h1); check("v0 4x2");
-  run("v0 4w x1", v0::k<4, 1>, 4, 1, 4 * 2 * v0::kStageBytes, 32, d_h1); check("v0 4x1");
+  run("v3 8w x1 long>=4096", v3::k<8, 1, 4096>, 8, 1, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v3 4096");
+  run("v3 8w x1 long>=2048", v3::k<8, 1, 2048>, 8, 1, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v3 2048");
+  run("v3 8w x1 long>=512", v3::k<8, 1, 512>, 8, 1, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v3 512");
+  run("v3 8w x1 all direct", v3::k<8, 1, 16>, 8, 1, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v3 all");
+  run("v3 8w x2 all direct", v3::k<8, 2, 16>, 8, 2, 8 * 2 * v0::kStageBytes, 32, d_h1); check("v3 all x2");
   return 0;
 }
