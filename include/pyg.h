@@ -378,6 +378,22 @@ int pyg_registry_from_cursors_dev(pyg_ctx* ctx, int32_t n, int32_t max_wf, const
                                   const int32_t* d_cursor, const uint64_t* d_future,
                                   const int32_t* d_current_role);
 
+/* ------------------------------------------------- device prompt assembly (§8f-4) */
+/* One segment of assemble_prompt (prompt.cpp:128-164) resolved by the host to a range of a
+   device token pool: a Ref into a resident exchange (request / response tokens in HBM), a
+   literal's tokenization, or freshly uploaded tokens. */
+typedef struct {
+  int64_t src;  /* pool offset */
+  int64_t len;  /* tokens */
+} pyg_segment;
+
+/* Concatenates each request's segments: d_tok_off[n_req+1] (exclusive scan of the request
+   lengths) and the token CSR d_tokens, ready for pyg_hash_batch_dev.  Segments of request r
+   are d_segs[d_seg_off[r] .. d_seg_off[r+1]). */
+int pyg_assemble_dev(pyg_ctx* ctx, int32_t n_req, const int64_t* d_seg_off,
+                     const pyg_segment* d_segs, const uint64_t* d_pool, int64_t* d_tok_off,
+                     uint64_t* d_tokens);
+
 /* ------------------------------------------------- host-buffer batch entry */
 /* The drop-in batch call for a C++ engine: host arrays in, host arrays out.  Copies the batch
    to the device (pinned host memory is fastest), runs K1..K5 exactly as the _dev sequence

@@ -1,0 +1,106 @@
+"""Device prompt assembly (csrc/k_prompt.cu).
+
+assemble_prompt (prompt.cpp:128-164) builds each prompt from a template: literal words
+and references into earlier exchanges.  A B200 serving loop keeps those exchanges in HBM
+(responses are decoded there, earlier prompts were assembled there), so per step the host
+ships only segment descriptors (pool offset, length) plus genuinely new tokens (task
+text, per-request salts, unique suffixes); pyg_assemble_dev gathers the prompts on device.
+
+PromptPool lays out one device token pool for a trace: every distinct resident sequence
+(a word table, an earlier exchange) once, then a fresh region rewritten every step.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+from .workload import _signed, fnv1a_u64_vec
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class PromptPool:
+    def __init__(self, trace, device="cuda", pinned=True):
+        seg = trace.segments
+        if seg is None:
+            raise ValueError("trace has no prompt segments")
+        kinds, keys = seg["kind"], seg["key"]
+        start, length, fresh = seg["start"], seg["len"], seg["fresh"]
+        S = len(kinds)
+        R = trace.R
+        # resident ranges: one per distinct (kind, key), long enough for every use
+        need = {}
+        for k in range(S):
+            if not fresh[k]:
+                kk = (kinds[k], keys[k])
+                need[kk] = max(need.get(kk, 0), int(start[k] + length[k]))
+        base = {}
+        off = 0
+        for kk, n in need.items():
+            base[kk] = off
+            off += n
+        self.resident_tokens = off
+        fresh_len = int(length[fresh].sum()) if S else 0
+        self.fresh_tokens = fresh_len
+        self.pool = torch.empty(max(off + fresh_len, 1), dtype=torch.int64, device=device)
+        for (kind, key), n in need.items():
+            b = base[(kind, key)]
+            if kind == "w":
+                tab = seg["word_tables"][key]
+                self.pool[b:b + n] = torch.from_numpy(tab[:n]).to(device)
+            else:
+                idx = torch.arange(n, dtype=torch.int64, device=device)
+                self.pool[b:b + n] = fnv1a_u64_vec(idx, torch.full_like(idx, _signed(key)))
+        # segment descriptors (pool offset, length) in request order; fresh ones point into
+        # the fresh region, filled from host memory every step
+        src = np.zeros(S, np.int64)
+        f_pos = off
+        fresh_host = []
+        for k in range(S):
+            if fresh[k]:
+                src[k] = f_pos
+                f_pos += int(length[k])
+                idx = torch.arange(int(start[k]), int(start[k] + length[k]), dtype=torch.int64)
+                fresh_host.append(fnv1a_u64_vec(idx, torch.full_like(idx, _signed(keys[k]))))
+            else:
+                src[k] = base[(kinds[k], keys[k])] + int(start[k])
+        segs = np.stack([src, length.astype(np.int64)], axis=1) if S else np.zeros((0, 2), np.int64)
+        seg_off = np.zeros(R + 1, np.int64)
+        np.cumsum(np.bincount(seg["req"], minlength=R), out=seg_off[1:])
+        fh = torch.cat(fresh_host) if fresh_host else torch.zeros(0, dtype=torch.int64)
+
+        def host(a):
+            t = torch.as_tensor(a)
+            return t.pin_memory() if pinned else t
+
+        # per-step host inputs (pinned) and their device twins
+        self.h_seg_off, self.h_segs, self.h_fresh = host(seg_off), host(segs), host(fh)
+        self.d_seg_off = torch.empty_like(self.h_seg_off, device=device)
+        self.d_segs = torch.empty_like(self.h_segs, device=device)
+        self.R = R
+        self.n_tokens = int(trace.tok_off[-1])
+        self.device = device
+
+    @property
+    def h2d_bytes(self):
+        return int(self.h_seg_off.numel() * 8 + self.h_segs.numel() * 8 + self.h_fresh.numel() * 8)
+
+    def upload(self):
+        """The step's host->device traffic: segment descriptors and the fresh tokens (written
+        straight into the pool's fresh region)."""
+        self.d_seg_off.copy_(self.h_seg_off, non_blocking=True)
+        self.d_segs.copy_(self.h_segs, non_blocking=True)
+        if self.fresh_tokens:
+            self.pool[self.resident_tokens:self.resident_tokens + self.fresh_tokens].copy_(
+                self.h_fresh, non_blocking=True)
+
+    def assemble(self, ctx, tok_off: torch.Tensor, tokens: torch.Tensor):
+        """pyg_assemble_dev into (tok_off [R+1], tokens [>= n_tokens])."""
+        check(_lib._lib.pyg_assemble_dev(ctx.h, self.R, _p(self.d_seg_off), _p(self.d_segs),
+                                         _p(self.pool), _p(tok_off), _p(tokens)))

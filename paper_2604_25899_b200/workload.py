@@ -88,6 +88,7 @@ class Trace:
     roles: list = field(default_factory=list)
     n_models: int = 1
     name: str = ""
+    segments: dict = None         # prompt segments (see _Builder.segments), for prompts.py
 
     @property
     def R(self):
@@ -127,12 +128,18 @@ def _lognormal(rng, mean, cv, size):
     return np.clip(np.rint(rng.lognormal(mu, math.sqrt(s2), size)), 1, GLOBAL_MAX_OUTPUT).astype(np.int64)
 
 
+def _with_segments(b, tr):
+    tr.segments = b.segments()
+    return tr
+
+
 class _Builder:
     """Accumulates segment descriptors; materializes all tokens in one vectorized pass."""
 
     def __init__(self):
         self.word_tables = {}
         self.seg_req, self.seg_kind, self.seg_key, self.seg_start, self.seg_len = [], [], [], [], []
+        self.seg_fresh = []
 
     def words(self, prefix, n):
         key = (prefix, n)
@@ -141,7 +148,10 @@ class _Builder:
                                              np.int64)
         return key
 
-    def add(self, r, kind, key, start, length):
+    def add(self, r, kind, key, start, length, fresh=False):
+        """One prompt segment.  fresh: new content of this request (task text, salt, unique
+        suffix) that a serving system must upload; otherwise it is history already resident
+        on the device (sys-prompt words, an earlier exchange's tokens)."""
         if length <= 0:
             return
         self.seg_req.append(r)
@@ -149,6 +159,13 @@ class _Builder:
         self.seg_key.append(key)
         self.seg_start.append(start)
         self.seg_len.append(length)
+        self.seg_fresh.append(bool(fresh))
+
+    def segments(self):
+        return {"req": np.asarray(self.seg_req, np.int64), "kind": list(self.seg_kind),
+                "key": list(self.seg_key), "start": np.asarray(self.seg_start, np.int64),
+                "len": np.asarray(self.seg_len, np.int64),
+                "fresh": np.asarray(self.seg_fresh, bool), "word_tables": self.word_tables}
 
     def build(self, R, device):
         seg_req = np.asarray(self.seg_req, np.int64)
@@ -225,8 +242,8 @@ def deep_research(n_workflows=10_000, seed=1, device=None, unprofiled_frac=0.1,
                 if prev_first is not None:
                     b.add(r, "i", response_key(prev_first), 0, min(role.carry_tokens, prev_out))
                 if si == 0:
-                    b.add(r, "i", task_key(wid), 0, task_tokens)
-                b.add(r, "i", salt_key(rid), 0, salt_tokens)
+                    b.add(r, "i", task_key(wid), 0, task_tokens, fresh=True)
+                b.add(r, "i", salt_key(rid), 0, salt_tokens, fresh=True)
                 plen = role.sys_tokens + (min(role.carry_tokens, prev_out) if prev_first else 0) + \
                     (task_tokens if si == 0 else 0) + salt_tokens
                 if rng.random() < unprofiled_frac:
@@ -239,9 +256,9 @@ def deep_research(n_workflows=10_000, seed=1, device=None, unprofiled_frac=0.1,
                 r += 1
             prev_first, prev_out = first_rid, int(outs[0])
     toks, tok_off = b.build(r, device)
-    return Trace(toks, tok_off, np.array(res, RES_DTYPE), np.array(group, np.int32),
+    return _with_segments(b, Trace(toks, tok_off, np.array(res, RES_DTYPE), np.array(group, np.int32),
                  np.array(wfs, np.int32), np.array(rls, np.int32), roles,
-                 2 * max(model_stride, 1), "deep_research")
+                 2 * max(model_stride, 1), "deep_research"))
 
 
 def coding_assistant(n_workflows=1_000, seed=1, device=None, unprofiled_frac=0.0) -> Trace:
@@ -295,8 +312,8 @@ def coding_assistant(n_workflows=1_000, seed=1, device=None, unprofiled_frac=0.0
                 r += 1
             prev_first, prev_out = first_rid, int(outs[0])
     toks, tok_off = b.build(r, device)
-    return Trace(toks, tok_off, np.array(res, RES_DTYPE), np.array(group, np.int32),
-                 np.array(wfs, np.int32), np.array(rls, np.int32), roles, 1, "coding_assistant")
+    return _with_segments(b, Trace(toks, tok_off, np.array(res, RES_DTYPE), np.array(group, np.int32),
+                 np.array(wfs, np.int32), np.array(rls, np.int32), roles, 1, "coding_assistant"))
 
 
 def long_context(n_requests=100_000, seed=1, device=None, n_roles=8, steps=4,
@@ -314,14 +331,14 @@ def long_context(n_requests=100_000, seed=1, device=None, n_roles=8, steps=4,
         ro = int(rng.integers(0, n_roles))
         b.add(r, "w", b.words(f"sys_role{ro}", sys_tokens), 0, sys_tokens)
         b.add(r, "i", response_key(f"w{w}_ctx"), 0, ctx_tokens)
-        b.add(r, "i", salt_key(f"w{w}_s{r % steps}_0"), 0, unique_tokens)
+        b.add(r, "i", salt_key(f"w{w}_s{r % steps}_0"), 0, unique_tokens, fresh=True)
         res.append((sys_tokens + ctx_tokens + unique_tokens, up, ALPHA, 0))
         group.append(0)
         wfs.append(w)
         rls.append(ro)
     toks, tok_off = b.build(n_requests, device)
-    return Trace(toks, tok_off, np.array(res, RES_DTYPE), np.array(group, np.int32),
-                 np.array(wfs, np.int32), np.array(rls, np.int32), roles, 1, "long_context")
+    return _with_segments(b, Trace(toks, tok_off, np.array(res, RES_DTYPE), np.array(group, np.int32),
+                 np.array(wfs, np.int32), np.array(rls, np.int32), roles, 1, "long_context"))
 
 
 def bursty(n_requests=1_000_000, seed=1, device=None, n_models=4, mean_len=2048, cv=1.0,
@@ -343,15 +360,15 @@ def bursty(n_requests=1_000_000, seed=1, device=None, n_models=4, mean_len=2048,
     unprof = rng.random(n_requests) < 0.1
     for r in range(n_requests):
         b.add(r, "i", pkeys[pre[r]], 0, int(plen[r]))
-        b.add(r, "i", salt_key(f"b{r_base + r}"), 0, int(L[r] - plen[r]))
+        b.add(r, "i", salt_key(f"b{r_base + r}"), 0, int(L[r] - plen[r]), fresh=True)
     res = np.zeros(n_requests, RES_DTYPE)
     res["prompt_len"] = L
     res["upper"] = np.where(unprof, GLOBAL_MAX_OUTPUT, up)
     res["alpha"] = np.where(unprof, 0.0, ALPHA)
     toks, tok_off = b.build(n_requests, device)
-    return Trace(toks, tok_off, res, model,
+    return _with_segments(b, Trace(toks, tok_off, res, model,
                  ((r_base + np.arange(n_requests)) // 8).astype(np.int32),
-                 (pre % 16).astype(np.int32), [], n_models, "bursty")
+                 (pre % 16).astype(np.int32), [], n_models, "bursty"))
 
 
 @dataclass
