@@ -640,157 +640,6 @@ def run_sharded(args, ws, rank, local, dev):
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {
                 "workload": describe(args, tr, ws),
-                "route_mode": "seq_commit" if mode == PB.SEQ_COMMIT else "snapshot",
-                "requests_per_step_per_gpu": tr.R, "tokens_per_step_per_gpu": tr.n_tokens,
-                "placed_per_step": n_placed, "admitted_per_step": n_admitted,
-                "l2_flush": "none needed: step inputs (tokens %.2f GB) exceed the 126 MB L2"
-                            % (tr.n_tokens * 8 / 1e9),
-                "parallelism": f"replica shards x{ws} (weak)"},
-            "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1)", "achieved": hash_gbs,
-                         "peak": peak, "unit": "GB/s", "frac": hash_gbs / peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": ab["hash"],
-                         "avg_launch_ms": phase_ms["hash"]},
-            "step_roofline": {"achieved": step_gbs, "frac": step_gbs / peak,
-                              "algorithmic_bytes_per_step": ab["total"], "probes": ab["probes"]},
-            "phase_ms": phase_ms,
-            "clocks": clk,
-            "gpu_launches": int(launches),
-            "e2e": e2e,
-            "e2e_tokens": e2e_tokens,
-            "cpu_baseline": cpu,
-        }
-        print(json.dumps(line))
-    if ws > 1:
-        dist.barrier()
-        dist.destroy_process_group()
-
-
-def run_sharded(args, ws, rank, local, dev):
-    """N > 1: the sharded step (paper_2604_25899_b200/shard.py) -- replicas partitioned over
-    the GPUs, route inputs all-gathered, placed requests dispatched to their owner GPU."""
-    import torch
-    import torch.distributed as dist
-    from paper_2604_25899_b200 import Context
-    from paper_2604_25899_b200 import batch as PB
-    from paper_2604_25899_b200.shard import ShardPlan, ShardedStep
-
-    tr, cl = build_workload(args, rank, ws, dev)
-    n_loc = args.replicas
-    base = rank * n_loc
-    counts = torch.tensor([tr.R], dtype=torch.int64, device=dev)
-    allc = [torch.zeros_like(counts) for _ in range(ws)]
-    dist.all_gather(allc, counts)
-    plan = ShardPlan([n_loc] * ws, [int(x.item()) for x in allc], rank, args.block)
-    ctx = Context(n_loc, cl.kv_capacity[base:base + n_loc], cl.l2_capacity[base:base + n_loc],
-                  args.block, device=local)
-    PB.bind_current_stream(ctx)
-    rng = np.random.default_rng(rank)
-    warm_l2(ctx, tr, cl, rng, rep_base=base, n_local=n_loc,
-            n_workflows=n_workflows_total(args, ws, tr))
-    db = PB.DeviceBatch(tr.R, tr.tokens, torch.from_numpy(tr.tok_off).to(dev), None, None,
-                        torch.from_numpy(tr.res.view(np.int64).reshape(tr.R, 4).copy()).to(dev),
-                        torch.from_numpy(tr.group).to(dev), torch.from_numpy(tr.wf).to(dev),
-                        torch.from_numpy(tr.role).to(dev), 0, tr.n_tokens)
-    nb = (np.diff(tr.tok_off) + args.block - 1) // args.block
-    hoff = np.zeros(tr.R + 1, np.int64)
-    np.cumsum(nb, out=hoff[1:])
-    db.hash_off = torch.from_numpy(hoff).to(dev)
-    db.hashes = torch.empty(int(hoff[-1]), dtype=torch.int64, device=dev)
-    dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand,
-                         device=dev)
-    tt = torch.tensor([tr.n_tokens], dtype=torch.int64, device=dev)
-    dist.all_reduce(tt)
-    st = ShardedStep(ctx, plan, db, dn, dev, cl.kv_capacity[base:base + n_loc], int(tt.item()))
-    st.build_directory()
-    now = [1.0]
-    for _ in range(args.warmup):
-        st.step(now[0])
-        now[0] += 1.0
-    torch.cuda.synchronize()
-    ctx.check_device_error()
-    dist.barrier()
-    torch.cuda.synchronize()
-    clocks = Clocks(local)
-    clocks.start()
-    time.sleep(0.3)
-    launches0 = ctx.kernel_launches()
-    evh = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    t0e = torch.cuda.Event(enable_timing=True)
-    t1e = torch.cuda.Event(enable_timing=True)
-    t0e.record()
-    n_here = 0
-    for s_ in range(args.steps):
-        out = st.step(now[0], ev_hash=evh[s_])
-        now[0] += 1.0
-    t1e.record()
-    torch.cuda.synchronize()
-    launches = ctx.kernel_launches() - launches0
-    clk = clocks.stop()
-    ctx.check_device_error()
-    ms = t0e.elapsed_time(t1e)
-    hash_ms = sum(a.elapsed_time(b) for a, b in evh) / args.steps
-    t = torch.tensor([ms, hash_ms], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, hash_ms_max = float(t[0].item()), float(t[1].item())
-    ms_step = ms / args.steps
-    value = plan.R_total * args.steps / (ms / 1000.0)
-    peak, peak_src = peaks()
-    L = np.diff(tr.tok_off)
-    hash_bytes = 8 * int(L.sum()) + 8 * int(nb.sum()) + 16 * (tr.R + 1)
-    hash_gbs = hash_bytes / (hash_ms / 1000.0) / 1e9
-
-    # e2e: pinned host inputs copied in and results copied out every step
-    e2e = None
-    if not args.no_e2e and not args.profile:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        h_tok = tr.tokens.cpu().pin_memory()
-        h_off, h_res = pin(tr.tok_off), pin(tr.res.view(np.int64).reshape(tr.R, 4))
-        h_grp, h_wf, h_role = pin(tr.group), pin(tr.wf), pin(tr.role)
-        h_dec = torch.empty((plan.R_local, 3), dtype=torch.int64).pin_memory()
-        h_adm = torch.empty(plan.R_local, dtype=torch.int32).pin_memory()
-        h_m3 = torch.empty((plan.R_local, 3), dtype=torch.int64).pin_memory()
-        h2d = sum(x.numel() * x.element_size() for x in (h_tok, h_off, h_res, h_grp, h_wf, h_role))
-        d2h = sum(x.numel() * x.element_size() for x in (h_dec, h_adm, h_m3))
-
-        def e2e_step():
-            db.tokens.copy_(h_tok, non_blocking=True)
-            db.tok_off.copy_(h_off, non_blocking=True)
-            db.res.copy_(h_res, non_blocking=True)
-            db.group.copy_(h_grp, non_blocking=True)
-            db.wf.copy_(h_wf, non_blocking=True)
-            db.role.copy_(h_role, non_blocking=True)
-            o = st.step(now[0])
-            now[0] += 1.0
-            a = plan.req_base
-            h_dec.copy_(o["decisions"][a:a + plan.R_local], non_blocking=True)
-            h_adm.copy_(o["admitted"], non_blocking=True)
-            h_m3.copy_(o["match3"], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-
-        e2e_step()
-        dist.barrier()
-        e_steps = max(2, min(args.steps, 5))
-        t0 = time.perf_counter()
-        for _ in range(e_steps):
-            e2e_step()
-        e_ms = (time.perf_counter() - t0) * 1000.0
-        t = torch.tensor([e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
-        e2e = {"value": plan.R_total * e_steps / (e_ms / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d * ws), "d2h_bytes_per_step": int(d2h * ws),
-               "ms_per_step": e_ms / e_steps,
-               "via": "ShardedStep with pinned host inputs copied in / results copied out "
-                      "(bytes summed over ranks)"}
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {
-                "workload": describe(args, tr, ws),
                 "route_mode": "seq_commit (whole burst, identical on every GPU)",
                 "requests_per_step": plan.R_total, "requests_per_step_per_gpu": tr.R,
                 "tokens_per_step_per_gpu": tr.n_tokens,
