@@ -394,6 +394,28 @@ int pyg_assemble_dev(pyg_ctx* ctx, int32_t n_req, const int64_t* d_seg_off,
                      const pyg_segment* d_segs, const uint64_t* d_pool, int64_t* d_tok_off,
                      uint64_t* d_tokens);
 
+/* ----------------------------------------- worker batch formation / preemption (§8f-3) */
+/* sched::QueueItem (worker.hpp:11-16) with the request id replaced by its rank in the
+   ids' string order (ties in form_batch / select_preemption_victim break on request_id). */
+typedef struct {
+  double base_priority;
+  double enqueue_time;
+  int64_t reservation;
+  int64_t id_rank;
+} pyg_queue_item;
+
+/* form_batch (worker.cpp:16-37) for n_sets queues at once (one per replica): items of set s
+   are d_items[d_off[s] .. d_off[s+1]) (at most 4096); d_order[d_off[s] + k] = index (within
+   the set) of the k-th admitted item, d_n_admitted[s] = admitted count. */
+int pyg_form_batch_dev(pyg_ctx* ctx, int32_t n_sets, const int64_t* d_off,
+                       const pyg_queue_item* d_items, const int64_t* d_active_reservation,
+                       const int64_t* d_capacity, double now, double aging_rate, int32_t* d_order,
+                       int32_t* d_n_admitted);
+/* select_preemption_victim (worker.cpp:39-58) per set; -1 for an empty set. */
+int pyg_preemption_victim_dev(pyg_ctx* ctx, int32_t n_sets, const int64_t* d_off,
+                              const pyg_queue_item* d_items, double now, double aging_rate,
+                              int32_t* d_victim);
+
 /* ------------------------------------------------- host-buffer batch entry */
 /* The drop-in batch call for a C++ engine: host arrays in, host arrays out.  Copies the batch
    to the device (pinned host memory is fastest), runs K1..K5 exactly as the _dev sequence

@@ -10,6 +10,9 @@
 // One pyg_ctx holds every replica of the simulation (slots handed out in the
 // order the engine constructs CacheHierarchy objects) plus the shared L3.
 // Workflow / role strings are interned to ints; role ids must stay < 64.
+#include <cuda_runtime.h>
+
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -21,6 +24,7 @@
 #include "pythia/cache/hierarchy.hpp"
 #include "pythia/cache/manager.hpp"
 #include "pythia/sched/router.hpp"
+#include "pythia/sched/worker.hpp"
 
 namespace {
 
@@ -377,6 +381,81 @@ RoutingDecision route(const std::vector<NodeView>& nodes, const Reservation& req
   out.oom_bound = d.oom_bound;
   out.cache_tiebreak_used = d.tiebreak != 0;
   return out;
+}
+
+double effective_priority(double base_priority, double enqueue_time, double now,
+                          double aging_rate) {
+  return base_priority + aging_rate * (now - enqueue_time);
+}
+
+namespace {
+// QueueItems as device records; request ids become their rank in string order
+std::vector<pyg_queue_item> queue_items(const std::vector<QueueItem>& q) {
+  std::vector<size_t> by_id(q.size());
+  for (size_t i = 0; i < q.size(); ++i) by_id[i] = i;
+  std::sort(by_id.begin(), by_id.end(),
+            [&](size_t a, size_t b) { return q[a].request_id < q[b].request_id; });
+  std::vector<pyg_queue_item> out(q.size());
+  for (size_t r = 0; r < by_id.size(); ++r) {
+    const QueueItem& x = q[by_id[r]];
+    out[by_id[r]] = {x.base_priority, x.enqueue_time, x.reservation, static_cast<int64_t>(r)};
+  }
+  return out;
+}
+
+struct DeviceQueue {  // one queue's arrays on the device for the K7 calls
+  void* mem = nullptr;
+  ~DeviceQueue() { cudaFree(mem); }
+};
+}  // namespace
+
+std::vector<size_t> form_batch(const std::vector<QueueItem>& pool, int64_t active_reservation,
+                               int64_t capacity, double now, double aging_rate) {
+  if (pool.empty()) return {};
+  Backend& b = Backend::get();
+  const auto items = queue_items(pool);
+  const int64_t n = static_cast<int64_t>(items.size());
+  const int64_t hdr[4] = {0, n, active_reservation, capacity};
+  DeviceQueue dq;
+  const size_t bytes = 32 + n * sizeof(pyg_queue_item) + n * 4 + 8;
+  if (cudaMalloc(&dq.mem, bytes) != cudaSuccess) throw std::runtime_error("cudaMalloc");
+  char* p = static_cast<char*>(dq.mem);
+  cudaMemcpy(p, hdr, 32, cudaMemcpyHostToDevice);
+  cudaMemcpy(p + 32, items.data(), n * sizeof(pyg_queue_item), cudaMemcpyHostToDevice);
+  auto* d_order = reinterpret_cast<int32_t*>(p + 32 + n * sizeof(pyg_queue_item));
+  auto* d_n = d_order + n;
+  const auto* d_hdr = reinterpret_cast<const int64_t*>(p);
+  check(pyg_set_stream(b.ctx, nullptr));
+  check(pyg_form_batch_dev(b.ctx, 1, d_hdr, reinterpret_cast<const pyg_queue_item*>(p + 32),
+                           d_hdr + 2, d_hdr + 3, now, aging_rate, d_order, d_n));
+  int32_t na = 0;
+  std::vector<int32_t> ord(n);
+  cudaMemcpy(&na, d_n, 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(ord.data(), d_order, n * 4, cudaMemcpyDeviceToHost);
+  check(pyg_check_device_error(b.ctx));
+  return std::vector<size_t>(ord.begin(), ord.begin() + na);
+}
+
+size_t select_preemption_victim(const std::vector<QueueItem>& active, double now,
+                                double aging_rate) {
+  Backend& b = Backend::get();
+  const auto items = queue_items(active);
+  const int64_t n = static_cast<int64_t>(items.size());
+  const int64_t hdr[2] = {0, n};
+  DeviceQueue dq;
+  if (cudaMalloc(&dq.mem, 16 + n * sizeof(pyg_queue_item) + 8) != cudaSuccess)
+    throw std::runtime_error("cudaMalloc");
+  char* p = static_cast<char*>(dq.mem);
+  cudaMemcpy(p, hdr, 16, cudaMemcpyHostToDevice);
+  cudaMemcpy(p + 16, items.data(), n * sizeof(pyg_queue_item), cudaMemcpyHostToDevice);
+  auto* d_v = reinterpret_cast<int32_t*>(p + 16 + n * sizeof(pyg_queue_item));
+  check(pyg_set_stream(b.ctx, nullptr));
+  check(pyg_preemption_victim_dev(b.ctx, 1, reinterpret_cast<const int64_t*>(p),
+                                  reinterpret_cast<const pyg_queue_item*>(p + 16), now, aging_rate,
+                                  d_v));
+  int32_t v = 0;
+  cudaMemcpy(&v, d_v, 4, cudaMemcpyDeviceToHost);
+  return static_cast<size_t>(v);
 }
 
 std::optional<int> route_least_outstanding(const std::vector<NodeView>& nodes) {

@@ -14,6 +14,7 @@
 // masks into sets of those role names.
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -24,6 +25,7 @@
 #include "pythia/cache/hierarchy.hpp"
 #include "pythia/cache/manager.hpp"
 #include "pythia/sched/router.hpp"
+#include "pythia/sched/worker.hpp"
 #include "pythia/workflow/path_analysis.hpp"
 #include "pythia/workflow/path_expr.hpp"
 
@@ -529,4 +531,32 @@ int32_t pref_path_distance(void* e, const int32_t* hist, int32_t n_hist, int32_t
 }
 
 }  // extern "C"
+// ---- worker batch formation / preemption (sched/worker.cpp) over plain arrays; request ids
+// are "q%08lld" of the given rank, so string order == rank order.
+int64_t pref_form_batch(int32_t n, const double* base, const double* enq, const int64_t* res,
+                        const int64_t* id_rank, int64_t active_reservation, int64_t capacity,
+                        double now, double aging, int32_t* out) {
+  std::vector<sched::QueueItem> pool(n);
+  char buf[32];
+  for (int32_t i = 0; i < n; ++i) {
+    std::snprintf(buf, sizeof(buf), "q%08lld", static_cast<long long>(id_rank[i]));
+    pool[i] = {buf, base[i], enq[i], res[i]};
+  }
+  auto adm = sched::form_batch(pool, active_reservation, capacity, now, aging);
+  for (size_t k = 0; k < adm.size(); ++k) out[k] = static_cast<int32_t>(adm[k]);
+  return static_cast<int64_t>(adm.size());
+}
+
+int32_t pref_preemption_victim(int32_t n, const double* base, const double* enq,
+                               const int64_t* res, const int64_t* id_rank, double now,
+                               double aging) {
+  std::vector<sched::QueueItem> act(n);
+  char buf[32];
+  for (int32_t i = 0; i < n; ++i) {
+    std::snprintf(buf, sizeof(buf), "q%08lld", static_cast<long long>(id_rank[i]));
+    act[i] = {buf, base[i], enq[i], res[i]};
+  }
+  return static_cast<int32_t>(sched::select_preemption_victim(act, now, aging));
+}
+
 }  // extern "C"
