@@ -416,6 +416,34 @@ int pyg_preemption_victim_dev(pyg_ctx* ctx, int32_t n_sets, const int64_t* d_off
                               const pyg_queue_item* d_items, double now, double aging_rate,
                               int32_t* d_victim);
 
+/* ------------------------------------------------------ forward staging (§8f-2) */
+#define PYG_STAGE_PROMOTE_TO_HOST 0   /* StageAction::Kind (manager.hpp) */
+#define PYG_STAGE_BACKGROUND_PREFILL 1
+#define PYG_STAGE_SKIP 2
+#define PYG_SKIP_NONE 0
+#define PYG_SKIP_UNRESOLVED 1         /* Skip reasons (manager.cpp:70-96) */
+#define PYG_SKIP_ALREADY_STAGED 2
+#define PYG_SKIP_GPU_BUSY 3
+#define PYG_SKIP_NO_REPLICA 4         /* no ready replica of the model (engine.cpp:1150) */
+
+typedef struct {
+  int32_t target;  /* replica index of this ctx (-1: none) */
+  int32_t kind;
+  int32_t reason;
+  int32_t pad;
+  int64_t from, to;
+} pyg_stage_action;
+
+/* Batched forward staging for successor prefixes (tokens CSR + boundary hashes): target =
+   ready candidate with the largest L2 prefix, ties to the lowest replica id (engine.cpp
+   fire_prefetch :1137-1166); action from lookup(prefix, &l3) on it (on_prefetch_requested,
+   manager.cpp:60-100).  d_gpu_idle[replica] = active and pool both empty. */
+int pyg_stage_plan_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                       const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t n_prefix,
+                       const int32_t* d_group, int32_t n_groups, const int32_t* d_cand_off,
+                       const int32_t* d_cand, int32_t max_cand, const int32_t* d_replica_id,
+                       const int8_t* d_gpu_idle, pyg_stage_action* d_out);
+
 /* ------------------------------------------------- host-buffer batch entry */
 /* The drop-in batch call for a C++ engine: host arrays in, host arrays out.  Copies the batch
    to the device (pinned host memory is fastest), runs K1..K5 exactly as the _dev sequence
