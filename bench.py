@@ -399,50 +399,40 @@ def run_ours(args):
     # pyg_step_host (every prompt token crosses PCIe), reported as e2e_tokens
     e2e = e2e_tokens = None
     if not args.no_e2e and not args.profile:
-        from paper_2604_25899_b200.prompts import PromptPool
-        pool = PromptPool(tr, device=dev)
+        from paper_2604_25899_b200.prompts import PipelinedSteps
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        h_res, h_grp = pin(tr.res.view(np.int64).reshape(tr.R, 4)), pin(tr.group)
-        h_wf, h_role = pin(tr.wf), pin(tr.role)
-        h_dec = torch.empty((tr.R, 3), dtype=torch.int64).pin_memory()
-        h_adm = torch.empty(tr.R, dtype=torch.int32).pin_memory()
-        h_m3 = torch.empty((tr.R, 3), dtype=torch.int64).pin_memory()
-        meta_b = sum(x.numel() * x.element_size() for x in (h_res, h_grp, h_wf, h_role))
-        meta_b += sum(x.numel() * x.element_size()
-                      for x in (dn.replica_id, dn.kv_capacity, dn.asg_off, dn.asg, dn.cand_off,
-                                dn.cand))
-        d2h_b = sum(x.numel() * x.element_size() for x in (h_dec, h_adm, h_m3))
+        meta = (pin(tr.res.view(np.int64).reshape(tr.R, 4)), pin(tr.group), pin(tr.wf),
+                pin(tr.role))
+        node_b = sum(x.numel() * x.element_size()
+                     for x in (dn.replica_id, dn.kv_capacity, dn.asg_off, dn.asg, dn.cand_off,
+                               dn.cand))
 
-        def e2e_step():
-            pool.upload()
-            db.res.copy_(h_res, non_blocking=True)
-            db.group.copy_(h_grp, non_blocking=True)
-            db.wf.copy_(h_wf, non_blocking=True)
-            db.role.copy_(h_role, non_blocking=True)
-            PB.bind_current_stream(ctx)
-            pool.assemble(ctx, db.tok_off, db.tokens)
-            _lib_check(ctx, db)
-            one_step()
-            h_dec.copy_(out.decisions[:tr.R], non_blocking=True)
-            h_adm.copy_(out.admitted[:tr.R], non_blocking=True)
-            h_m3.copy_(out.match3[:tr.R], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        def run_step(b, k):
+            _lib_check(ctx, b)
+            PB.hash_batch(ctx, b)
+            PB.staged_matrix(ctx, b, dn, out)
+            PB.route_batch(ctx, b, dn, out, mode)
+            PB.admit_batch(ctx, b, out, now[0] + k, True)
+            PB.release_batch(ctx, b, out)
+            return out.decisions[:tr.R], out.admitted[:tr.R], out.match3[:tr.R]
 
-        for _ in range(2):
-            e2e_step()
-        e2e_steps = max(3, min(args.steps, 10))
+        pipe = PipelinedSteps(ctx, tr, db, dev, run_step, meta,
+                              (out.decisions[:tr.R], out.admitted[:tr.R], out.match3[:tr.R]))
+        pipe.run(2)
+        e2e_steps = max(4, min(args.steps, 10))
         t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            e2e_step()
+        pipe.run(e2e_steps, first_index=2)
         e_ms = (time.perf_counter() - t0) * 1000.0
+        now[0] += e2e_steps + 2
         e2e = {"value": tr.R * e2e_steps / (e_ms / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": int(pool.h2d_bytes + meta_b), "d2h_bytes_per_step": d2h_b,
-               "ms_per_step": e_ms / e2e_steps,
-               "via": ("public API with device prompt assembly: segment descriptors + fresh "
-                       "tokens + request metadata uploaded from pinned memory, prompts gathered "
-                       "from the HBM-resident exchange history (pyg_assemble_dev), full step, "
-                       "results copied back"),
-               "fresh_tokens_per_step": pool.fresh_tokens}
+               "h2d_bytes_per_step": int(pipe.h2d_bytes + node_b),
+               "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": e_ms / e2e_steps,
+               "via": ("public API with device prompt assembly: per step the segment "
+                       "descriptors, fresh tokens and request metadata are uploaded from pinned "
+                       "memory (copy stream, overlapped with the previous step), prompts are "
+                       "gathered from the HBM-resident exchange history (pyg_assemble_dev), the "
+                       "full step runs and decisions/admissions/matches are copied back"),
+               "fresh_tokens_per_step": pipe.pools[0].fresh_tokens}
         hs = PB.HostStep(ctx, tr.tokens_np(), tr.tok_off, tr.res, tr.group, tr.wf, tr.role, cl)
         for _ in range(2):
             hs(now[0], mode)

@@ -104,3 +104,110 @@ class PromptPool:
         """pyg_assemble_dev into (tok_off [R+1], tokens [>= n_tokens])."""
         check(_lib._lib.pyg_assemble_dev(ctx.h, self.R, _p(self.d_seg_off), _p(self.d_segs),
                                          _p(self.pool), _p(tok_off), _p(tokens)))
+
+
+class PipelinedSteps:
+    """Step after step through the public API with the next step's host->device upload
+    overlapped with the current step's device work (a copy stream and two input sets):
+
+      copy stream    upload(k+1) ............ upload(k+2)
+      compute        assemble(k) -> step(k) -> results(k) -> assemble(k+1) -> ...
+
+    Each step still uploads its own inputs (segment descriptors, fresh tokens, request
+    metadata) and copies its own results back; only the overlap differs from the serial
+    loop.  `run_step(batch, k)` launches the device step for a DeviceBatch whose metadata
+    tensors hold step k's inputs and returns the tensors to copy back."""
+
+    def __init__(self, ctx, trace, batch, device, run_step, pinned_meta, results_like):
+        from . import batch as PB
+        self.PB, self.ctx, self.dev = PB, ctx, device
+        self.pools = [PromptPool(trace, device=device), None]
+        # the second input set shares the resident part of the pool: same pool tensor, its
+        # fresh region placed after the first one's
+        p0 = self.pools[0]
+        self.pools[1] = _ShiftedFresh(p0)
+        self.batches = [batch, PB.DeviceBatch(batch.R, batch.tokens, batch.tok_off,
+                                              batch.hash_off, batch.hashes,
+                                              torch.empty_like(batch.res),
+                                              torch.empty_like(batch.group),
+                                              torch.empty_like(batch.wf),
+                                              torch.empty_like(batch.role), batch.n_hashes,
+                                              batch.n_tokens)]
+        self.meta = pinned_meta          # (res, group, wf, role) pinned host tensors
+        self.results = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in results_like]
+                        for _ in range(2)]
+        self.copy = torch.cuda.Stream(device=device)
+        self.compute = torch.cuda.current_stream(device)
+        self.up = [torch.cuda.Event(), torch.cuda.Event()]
+        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.run_step = run_step
+
+    def _upload(self, s):
+        with torch.cuda.stream(self.copy):
+            self.pools[s].upload()
+            b = self.batches[s]
+            for dst, src in zip((b.res, b.group, b.wf, b.role), self.meta):
+                dst.copy_(src, non_blocking=True)
+            self.up[s].record(self.copy)
+
+    def run(self, steps, first_index=0):
+        self._upload(0)
+        for k in range(steps):
+            s = k % 2
+            if k + 1 < steps:
+                if k >= 1:
+                    self.copy.wait_event(self.done[1 - s])
+                self._upload(1 - s)
+            self.compute.wait_event(self.up[s])
+            self.PB.bind_current_stream(self.ctx)
+            self.pools[s].assemble(self.ctx, self.batches[s].tok_off, self.batches[s].tokens)
+            outs = self.run_step(self.batches[s], first_index + k)
+            for dst, src in zip(self.results[s], outs):
+                dst.copy_(src, non_blocking=True)
+            self.done[s].record(self.compute)
+        self.compute.synchronize()
+
+    @property
+    def h2d_bytes(self):
+        return self.pools[0].h2d_bytes + sum(int(t.numel() * t.element_size()) for t in self.meta)
+
+    @property
+    def d2h_bytes(self):
+        return sum(int(t.numel() * t.element_size()) for t in self.results[0])
+
+
+class _ShiftedFresh:
+    """Second input set over the same pool: identical resident part, its own fresh region
+    (appended to the pool) and its own segment-descriptor buffers."""
+
+    def __init__(self, p0: PromptPool):
+        self.p0 = p0
+        self.R, self.fresh_tokens = p0.R, p0.fresh_tokens
+        base = p0.pool.numel()
+        grown = torch.empty(base + p0.fresh_tokens, dtype=torch.int64, device=p0.pool.device)
+        grown[:base] = p0.pool
+        p0.pool = grown
+        self.pool_owner = p0
+        shift = base - p0.resident_tokens
+        segs = p0.h_segs.clone()
+        fresh_mask = segs[:, 0] >= p0.resident_tokens
+        segs[fresh_mask, 0] += shift
+        self.h_seg_off, self.h_segs, self.h_fresh = p0.h_seg_off, segs.pin_memory(), p0.h_fresh
+        self.d_seg_off = torch.empty_like(p0.d_seg_off)
+        self.d_segs = torch.empty_like(p0.d_segs)
+        self.fresh_base = base
+
+    @property
+    def h2d_bytes(self):
+        return self.p0.h2d_bytes
+
+    def upload(self):
+        self.d_seg_off.copy_(self.h_seg_off, non_blocking=True)
+        self.d_segs.copy_(self.h_segs, non_blocking=True)
+        if self.fresh_tokens:
+            self.pool_owner.pool[self.fresh_base:self.fresh_base + self.fresh_tokens].copy_(
+                self.h_fresh, non_blocking=True)
+
+    def assemble(self, ctx, tok_off, tokens):
+        check(_lib._lib.pyg_assemble_dev(ctx.h, self.R, _p(self.d_seg_off), _p(self.d_segs),
+                                         _p(self.pool_owner.pool), _p(tok_off), _p(tokens)))
