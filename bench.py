@@ -32,6 +32,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# FNV-1a arithmetic ceiling of one B200 (tools/k1/fnv_core.cu, profiles/r01_fnv_core.txt):
+# 513 Gtok/s with register-resident tokens = 4.11 TB/s of token bytes -- K1 is INT-bound there
+INT_CEILING_GBS = 4110.0
 METRIC = "routed requests/sec (prefix-match+evict+route) at 1/2/4/8 B200; % HBM peak"
 UNIT = "requests/s"
 
@@ -479,7 +482,11 @@ def run_ours(args):
                          "peak": peak, "unit": "GB/s", "frac": hash_gbs / peak,
                          "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": ab["hash"],
-                         "avg_launch_ms": phase_ms["hash"]},
+                         "avg_launch_ms": phase_ms["hash"],
+                         "int_ceiling": {"gbs": INT_CEILING_GBS,
+                                         "frac": hash_gbs / INT_CEILING_GBS,
+                                         "source": "profiles/r01_fnv_core.txt: FNV-1a core with "
+                                                   "register-resident tokens, 513 Gtok/s"}},
             "step_roofline": {"achieved": step_gbs, "frac": step_gbs / peak,
                               "algorithmic_bytes_per_step": ab["total"], "probes": ab["probes"]},
             "phase_ms": phase_ms,
