@@ -371,6 +371,9 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
       }
     }
     int done = base - 1;
+    // staged value of candidate `lane` for request pre_r, loaded one evaluation ahead
+    int pre_r = -1;
+    int32_t pre_v = 0;
     for (;;) {
       int first = INT32_MAX;
 #pragma unroll
@@ -397,8 +400,23 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
       // the staged row is read where it is needed (one L2 line per evaluated request);
       // staging every visited chunk's rows in shared memory cost more than it saved once
       // groups interleave (probe: tools/route_probe.py)
+      const int32_t own_v = (first == pre_r)
+                                ? pre_v
+                                : (lane < nc ? A.staged[static_cast<int64_t>(first) * A.max_cand + lane] : 0);
+      {  // load the next request of this group in the chunk now: its evaluation (usually the
+         // next one) then finds its staged value in a register instead of waiting on L2
+        int nx = INT32_MAX;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int r = base + lane * kPer + u;
+          if (mine[u] && r > first) nx = min(nx, r);
+        }
+        nx = __reduce_min_sync(kFull, nx);
+        pre_r = nx;
+        if (nx != INT32_MAX && lane < nc) pre_v = A.staged[static_cast<int64_t>(nx) * A.max_cand + lane];
+      }
       auto staged_of = [&](int j) -> int32_t {
-        return A.staged[static_cast<int64_t>(first) * A.max_cand + j];
+        return j == lane ? own_v : A.staged[static_cast<int64_t>(first) * A.max_cand + j];
       };
       // full sched::route over the group's candidates (router.cpp:24-43): the
       // reference's strict lexicographic running max on (headroom, staged, -replica_id) in
