@@ -158,3 +158,55 @@ def test_batch_config5_many_replicas(n_rep):
     tr = W.deep_research(n_workflows=6, seed=8, device="cpu")
     cl = W.make_cluster(n_rep, 2, kv=30_000, l2=30_000, seed=9, interleave=True, max_bg=1)
     _run(tr, cl, 16, SEQ_COMMIT, steps=1)
+
+
+def test_batch_edge_cases_empty_and_no_candidates():
+    """R = 0 through the device step and the host-buffer entry; a candidate group with no
+    replicas (every request of it waits); zero-length prompts."""
+    from paper_2604_25899_b200 import Context
+    from paper_2604_25899_b200 import batch as PB
+    from paper_2604_25899_b200 import workload as W
+    cl = W.make_cluster(4, 2, kv=20_000, l2=20_000, seed=1)
+    ctx = Context(4, cl.kv_capacity, cl.l2_capacity, 16)
+    empty = np.zeros(0, PB.RES_DTYPE)
+    z = np.zeros(0, np.int32)
+    db = PB.upload_batch(ctx, np.zeros(1, np.uint64), np.zeros(1, np.int64), empty, z, z, z)
+    dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand)
+    out = PB.alloc_out(ctx, db, dn)
+    PB.step(ctx, db, dn, out, 1.0)
+    torch.cuda.synchronize()
+    ctx.check_device_error()
+    # a group without candidates + empty prompts
+    tr = W.deep_research(n_workflows=3, seed=2, device="cpu")
+    grp = tr.group.copy()
+    grp[::3] = 2                                      # group 2 has no replicas
+    cand_off = np.concatenate([cl.cand_off, [cl.cand_off[-1]]]).astype(np.int32)
+    lens = np.diff(tr.tok_off)
+    lens[1::5] = 0
+    off = np.zeros(tr.R + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    toks = np.concatenate([tr.prompt(r)[:lens[r]] for r in range(tr.R)])
+    res = tr.res.copy()
+    res["prompt_len"] = lens
+    o = Restated(16)
+    caches = [o.new_cache(20_000, 20_000) for _ in range(4)]
+    l3, reg = o.new_l3(), o.new_registry()
+    db = PB.upload_batch(ctx, toks, off, res, grp, tr.wf, tr.role)
+    dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cand_off, cl.cand)
+    out = PB.alloc_out(ctx, db, dn)
+    PB.step(ctx, db, dn, out, 2.0)
+    torch.cuda.synchronize()
+    ctx.check_device_error()
+    got = out.host()
+    sub = W.Trace(torch.from_numpy(toks.view(np.int64)), off, res, grp, tr.wf, tr.role)
+
+    class Cl:  # the cluster with the extra empty group
+        pass
+    c2 = Cl()
+    c2.__dict__.update(cl.__dict__)
+    c2.cand_off = cand_off
+    want = oracle_step(o, caches, l3, reg, sub, c2, SEQ_COMMIT, 0.05, 2.0, True, True)
+    d = got["decisions"][:tr.R]
+    assert [int(x) for x in d["target"]] == [w[0] for w in want["decisions"]]
+    assert all(int(d["target"][r]) == -1 for r in range(0, tr.R, 3))
+    assert np.array_equal(got["admitted"][:tr.R], want["admitted"])
