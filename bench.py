@@ -411,7 +411,6 @@ def run_ours(args):
                                dn.cand))
 
         def run_step(b, k):
-            _lib_check(ctx, b)
             PB.hash_batch(ctx, b)
             PB.staged_matrix(ctx, b, dn, out)
             PB.route_batch(ctx, b, dn, out, mode)
@@ -432,9 +431,10 @@ def run_ours(args):
                "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": e_ms / e2e_steps,
                "via": ("public API with device prompt assembly: per step the segment "
                        "descriptors, fresh tokens and request metadata are uploaded from pinned "
-                       "memory (copy stream, overlapped with the previous step), prompts are "
-                       "gathered from the HBM-resident exchange history (pyg_assemble_dev), the "
-                       "full step runs and decisions/admissions/matches are copied back"),
+                       "memory (copy stream) and the prompts gathered from the HBM-resident "
+                       "exchange history (pyg_assemble_dev, assembly stream), both overlapped "
+                       "with the previous step; the full step runs and decisions/admissions/"
+                       "matches are copied back"),
                "fresh_tokens_per_step": pipe.pools[0].fresh_tokens}
         hs = PB.HostStep(ctx, tr.tokens_np(), tr.tok_off, tr.res, tr.group, tr.wf, tr.role, cl)
         for _ in range(2):

@@ -107,60 +107,73 @@ class PromptPool:
 
 
 class PipelinedSteps:
-    """Step after step through the public API with the next step's host->device upload
-    overlapped with the current step's device work (a copy stream and two input sets):
+    """Step after step through the public API, the next step's host->device upload AND its
+    prompt assembly overlapped with the current step's device work (two input sets, each
+    with its own token / hash buffers):
 
-      copy stream    upload(k+1) ............ upload(k+2)
-      compute        assemble(k) -> step(k) -> results(k) -> assemble(k+1) -> ...
+      copy stream      upload(k+1) ..................... upload(k+2)
+      assembly stream     assemble(k+1) + hash_off ...........  assemble(k+2)
+      compute          step(k) -> results(k) ........ step(k+1) -> results(k+1)
 
-    Each step still uploads its own inputs (segment descriptors, fresh tokens, request
-    metadata) and copies its own results back; only the overlap differs from the serial
-    loop.  `run_step(batch, k)` launches the device step for a DeviceBatch whose metadata
-    tensors hold step k's inputs and returns the tensors to copy back."""
+    Assembly is HBM-bound and K1 INT-bound, so they share the GPU well.  Assembly runs on
+    its own (replica-less) pyg_ctx so its scratch never races the step's.  Each step
+    still uploads its own inputs (segment descriptors, fresh tokens, request metadata)
+    and copies its own results back.  `run_step(batch, k)` launches the device step
+    (hash_off already computed) for a DeviceBatch holding step k's inputs and returns
+    the tensors to copy back."""
 
     def __init__(self, ctx, trace, batch, device, run_step, pinned_meta, results_like):
         from . import batch as PB
+        from ._lib import Context
         self.PB, self.ctx, self.dev = PB, ctx, device
         self.pools = [PromptPool(trace, device=device), None]
-        # the second input set shares the resident part of the pool: same pool tensor, its
-        # fresh region placed after the first one's
         p0 = self.pools[0]
         self.pools[1] = _ShiftedFresh(p0)
-        self.batches = [batch, PB.DeviceBatch(batch.R, batch.tokens, batch.tok_off,
-                                              batch.hash_off, batch.hashes,
-                                              torch.empty_like(batch.res),
-                                              torch.empty_like(batch.group),
-                                              torch.empty_like(batch.wf),
-                                              torch.empty_like(batch.role), batch.n_hashes,
-                                              batch.n_tokens)]
+        e = torch.empty_like
+        self.batches = [batch, PB.DeviceBatch(batch.R, e(batch.tokens), e(batch.tok_off),
+                                              e(batch.hash_off), e(batch.hashes), e(batch.res),
+                                              e(batch.group), e(batch.wf), e(batch.role),
+                                              batch.n_hashes, batch.n_tokens)]
         self.meta = pinned_meta          # (res, group, wf, role) pinned host tensors
         self.results = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in results_like]
                         for _ in range(2)]
         self.copy = torch.cuda.Stream(device=device)
+        self.asm = torch.cuda.Stream(device=device)
         self.compute = torch.cuda.current_stream(device)
+        idx = device.index if isinstance(device, torch.device) and device.index is not None \
+            else torch.cuda.current_device()
+        self.asm_ctx = Context(0, [], [], ctx.B, device=idx)
+        self.asm_ctx.set_stream(C.c_void_p(self.asm.cuda_stream))
         self.up = [torch.cuda.Event(), torch.cuda.Event()]
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
         self.done = [torch.cuda.Event(), torch.cuda.Event()]
         self.run_step = run_step
 
-    def _upload(self, s):
+    def _prepare(self, s, wait_done):
+        """upload + assemble input set s (after the step that last used it finished)."""
+        b = self.batches[s]
         with torch.cuda.stream(self.copy):
+            if wait_done:
+                self.copy.wait_event(self.done[s])
             self.pools[s].upload()
-            b = self.batches[s]
             for dst, src in zip((b.res, b.group, b.wf, b.role), self.meta):
                 dst.copy_(src, non_blocking=True)
             self.up[s].record(self.copy)
+        with torch.cuda.stream(self.asm):
+            self.asm.wait_event(self.up[s])
+            self.pools[s].assemble(self.asm_ctx, b.tok_off, b.tokens)
+            check(_lib._lib.pyg_hash_offsets_dev(self.asm_ctx.h, _p(b.tok_off), b.R,
+                                                 _p(b.hash_off), None))
+            self.ready[s].record(self.asm)
 
     def run(self, steps, first_index=0):
-        self._upload(0)
+        self._prepare(0, False)
         for k in range(steps):
             s = k % 2
             if k + 1 < steps:
-                if k >= 1:
-                    self.copy.wait_event(self.done[1 - s])
-                self._upload(1 - s)
-            self.compute.wait_event(self.up[s])
+                self._prepare(1 - s, k >= 1)
+            self.compute.wait_event(self.ready[s])
             self.PB.bind_current_stream(self.ctx)
-            self.pools[s].assemble(self.ctx, self.batches[s].tok_off, self.batches[s].tokens)
             outs = self.run_step(self.batches[s], first_index + k)
             for dst, src in zip(self.results[s], outs):
                 dst.copy_(src, non_blocking=True)
