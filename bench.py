@@ -579,56 +579,50 @@ def run_sharded(args, ws, rank, local, dev):
 
     # e2e through the public API with device prompt assembly (see run_ours): per step each
     # rank uploads its segment descriptors, fresh tokens and request metadata from pinned
-    # memory, assembles its prompts from its HBM-resident history, runs the sharded step and
-    # copies its requests' results back
+    # memory and assembles its prompts from its HBM-resident history -- both overlapped with
+    # the previous step (two input sets, each with its own ShardedStep exchange window) --
+    # runs the sharded step and copies its requests' results back
     e2e = None
     if not args.no_e2e and not args.profile:
-        from paper_2604_25899_b200.prompts import PromptPool
-        pool = PromptPool(tr, device=dev)
+        from paper_2604_25899_b200.prompts import PipelinedSteps, clone_batch
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        h_res, h_grp = pin(tr.res.view(np.int64).reshape(tr.R, 4)), pin(tr.group)
-        h_wf, h_role = pin(tr.wf), pin(tr.role)
-        h_dec = torch.empty((plan.R_local, 3), dtype=torch.int64).pin_memory()
-        h_adm = torch.empty(plan.R_local, dtype=torch.int32).pin_memory()
-        h_m3 = torch.empty((plan.R_local, 3), dtype=torch.int64).pin_memory()
-        meta = sum(x.numel() * x.element_size() for x in (h_res, h_grp, h_wf, h_role))
-        d2h = sum(x.numel() * x.element_size() for x in (h_dec, h_adm, h_m3))
+        meta = (pin(tr.res.view(np.int64).reshape(tr.R, 4)), pin(tr.group), pin(tr.wf),
+                pin(tr.role))
+        db1 = clone_batch(db)
+        for dst, src in ((db1.tok_off, db.tok_off), (db1.hash_off, db.hash_off)):
+            dst.copy_(src)
+        st1 = ShardedStep(ctx, plan, db1, dn, dev, cl.kv_capacity[base:base + n_loc], int(tt.item()))
+        steps_of = {id(db): st, id(db1): st1}
+        a0 = plan.req_base
 
-        def e2e_step():
-            pool.upload()
-            db.res.copy_(h_res, non_blocking=True)
-            db.group.copy_(h_grp, non_blocking=True)
-            db.wf.copy_(h_wf, non_blocking=True)
-            db.role.copy_(h_role, non_blocking=True)
-            PB.bind_current_stream(ctx)
-            pool.assemble(ctx, db.tok_off, db.tokens)
-            _lib_check(ctx, db)
-            o = st.step(now[0])
-            now[0] += 1.0
-            a = plan.req_base
-            h_dec.copy_(o["decisions"][a:a + plan.R_local], non_blocking=True)
-            h_adm.copy_(o["admitted"], non_blocking=True)
-            h_m3.copy_(o["match3"], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        def run_step(b, k):
+            o = steps_of[id(b)].step(now[0] + k)
+            return o["decisions"][a0:a0 + plan.R_local], o["admitted"], o["match3"]
 
-        e2e_step()
+        res_like = (torch.empty((plan.R_local, 3), dtype=torch.int64),
+                    torch.empty(plan.R_local, dtype=torch.int32),
+                    torch.empty((plan.R_local, 3), dtype=torch.int64))
+        pipe = PipelinedSteps(ctx, tr, db, dev, run_step, meta, res_like, second_batch=db1)
+        pipe.run(2)
         dist.barrier()
-        e_steps = max(3, min(args.steps, 10))
+        e_steps = max(4, min(args.steps, 10))
         t0 = time.perf_counter()
-        for _ in range(e_steps):
-            e2e_step()
+        pipe.run(e_steps, first_index=2)
         e_ms = (time.perf_counter() - t0) * 1000.0
+        now[0] += e_steps + 2
         t = torch.tensor([e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item())
-        hb = torch.tensor([pool.h2d_bytes + meta, pool.fresh_tokens], dtype=torch.int64, device=dev)
+        hb = torch.tensor([pipe.h2d_bytes, pipe.pools[0].fresh_tokens], dtype=torch.int64,
+                          device=dev)
         dist.all_reduce(hb)
         e2e = {"value": plan.R_total * e_steps / (e_ms / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": int(hb[0].item()), "d2h_bytes_per_step": int(d2h * ws),
-               "ms_per_step": e_ms / e_steps,
-               "via": ("ShardedStep through the public API with device prompt assembly (segment "
-                       "descriptors + fresh tokens + metadata uploaded per rank; bytes summed "
-                       "over ranks)"),
+               "h2d_bytes_per_step": int(hb[0].item()),
+               "d2h_bytes_per_step": int(pipe.d2h_bytes * ws), "ms_per_step": e_ms / e_steps,
+               "via": ("ShardedStep through the public API with device prompt assembly: per rank "
+                       "and step, segment descriptors + fresh tokens + metadata uploaded and "
+                       "prompts assembled on side streams overlapping the previous step; bytes "
+                       "summed over ranks"),
                "fresh_tokens_per_step": int(hb[1].item())}
     if rank == 0:
         line = {

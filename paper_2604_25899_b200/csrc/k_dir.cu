@@ -350,11 +350,12 @@ int pyg_set_shard(pyg_ctx* c, int32_t rep_base, int32_t n_global) {
     set_error("pyg_set_shard: need 0 <= rep_base, rep_base + n_replicas <= n_global <= 1024");
     return PYG_EINVAL;
   }
+  if (c->sharded && c->rep_base == rep_base && c->n_global == n_global) return PYG_OK;
   c->sharded = true;
   c->rep_base = rep_base;
   c->n_global = n_global;
   c->hd.rep_base = rep_base;
-  c->dir_dirty = true;
+  c->dir_dirty = true;  // the directory must now cover the whole cluster
   return PYG_OK;
 }
 

@@ -122,18 +122,15 @@ class PipelinedSteps:
     (hash_off already computed) for a DeviceBatch holding step k's inputs and returns
     the tensors to copy back."""
 
-    def __init__(self, ctx, trace, batch, device, run_step, pinned_meta, results_like):
+    def __init__(self, ctx, trace, batch, device, run_step, pinned_meta, results_like,
+                 second_batch=None):
         from . import batch as PB
         from ._lib import Context
         self.PB, self.ctx, self.dev = PB, ctx, device
         self.pools = [PromptPool(trace, device=device), None]
         p0 = self.pools[0]
         self.pools[1] = _ShiftedFresh(p0)
-        e = torch.empty_like
-        self.batches = [batch, PB.DeviceBatch(batch.R, e(batch.tokens), e(batch.tok_off),
-                                              e(batch.hash_off), e(batch.hashes), e(batch.res),
-                                              e(batch.group), e(batch.wf), e(batch.role),
-                                              batch.n_hashes, batch.n_tokens)]
+        self.batches = [batch, second_batch or clone_batch(batch)]
         self.meta = pinned_meta          # (res, group, wf, role) pinned host tensors
         self.results = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in results_like]
                         for _ in range(2)]
@@ -187,6 +184,14 @@ class PipelinedSteps:
     @property
     def d2h_bytes(self):
         return sum(int(t.numel() * t.element_size()) for t in self.results[0])
+
+
+def clone_batch(b):
+    """A second DeviceBatch with its own buffers of the same shapes."""
+    from . import batch as PB
+    e = torch.empty_like
+    return PB.DeviceBatch(b.R, e(b.tokens), e(b.tok_off), e(b.hash_off), e(b.hashes), e(b.res),
+                          e(b.group), e(b.wf), e(b.role), b.n_hashes, b.n_tokens)
 
 
 class _ShiftedFresh:
