@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
+    ap.add_argument("--free-sms", type=int, default=8,
+                    help="K1 of step k+1 overlaps steps k's route/admission on a second stream, "
+                         "its grid capped at (SMs - free_sms); -1 = no overlap (serial step)")
     return ap.parse_args()
 
 
@@ -337,22 +340,80 @@ def run_ours(args):
     now = [1.0]
 
     phases = ["hash", "staged", "route", "admit", "release"]
+    overlap = args.free_sms >= 0
+    S = torch.cuda.Stream(device=dev, priority=-1) if overlap else torch.cuda.current_stream(dev)
+    torch.cuda.set_stream(S)
+    PB.bind_current_stream(ctx)
+    if overlap:
+        # hashing needs no cache state: K1 of step k+1 runs on its own (replica-less) ctx and
+        # low-priority stream while step k routes and admits; two hash buffers
+        import copy
+        import ctypes
+        H = torch.cuda.Stream(device=dev, priority=0)
+        hctx = Context(0, [], [], args.block, device=local)
+        hctx.set_stream(ctypes.c_void_p(H.cuda_stream))
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
+        db2 = copy.copy(db)
+        db2.hashes = torch.empty_like(db.hashes)
+        bufs = [db, db2]
+        ev_h = [torch.cuda.Event() for _ in range(2)]
+        ev_k2 = torch.cuda.Event()
 
-    def one_step(evs=None):
-        fns = [lambda: PB.hash_batch(ctx, db), lambda: PB.staged_matrix(ctx, db, dn, out),
-               lambda: PB.route_batch(ctx, db, dn, out, mode),
-               lambda: PB.admit_batch(ctx, db, out, now[0], True),
-               lambda: PB.release_batch(ctx, db, out)]
-        for i, f in enumerate(fns):
-            if evs is not None:
-                evs[i].record()
-            f()
-        if evs is not None:
-            evs[len(fns)].record()
-        now[0] += 1.0
+    def run_steps(n, evs=None, hev=None):
+        """n steps; evs[s] = per-phase events on the step stream, hev[s] = (start, end) of
+        K1 on the hash stream (overlap mode)."""
+        if not overlap:
+            for k in range(n):
+                e = evs[k] if evs is not None else None
+                fns = [lambda: PB.hash_batch(ctx, db), lambda: PB.staged_matrix(ctx, db, dn, out),
+                       lambda: PB.route_batch(ctx, db, dn, out, mode),
+                       lambda: PB.admit_batch(ctx, db, out, now[0], True),
+                       lambda: PB.release_batch(ctx, db, out)]
+                for i, f in enumerate(fns):
+                    if e is not None:
+                        e[i].record(S)
+                    f()
+                if e is not None:
+                    e[len(fns)].record(S)
+                now[0] += 1.0
+            return
 
-    for _ in range(args.warmup):
-        one_step()
+        def hash_into(k):
+            H.wait_stream(S)   # after K2(k-1): step k-1 no longer needs the whole GPU, and
+            if hev is not None:  # release(k-2), the last reader of this buffer, is done
+                hev[k][0].record(H)
+            PB.hash_batch(hctx, bufs[k % 2])
+            if hev is not None:
+                hev[k][1].record(H)
+            ev_h[k % 2].record(H)
+
+        hash_into(0)
+        for k in range(n):
+            b = bufs[k % 2]
+            e = evs[k] if evs is not None else None
+            if e is not None:
+                e[0].record(S)
+            S.wait_event(ev_h[k % 2])
+            if e is not None:
+                e[1].record(S)
+            PB.staged_matrix(ctx, b, dn, out)
+            if e is not None:
+                e[2].record(S)
+            if k + 1 < n:
+                hash_into(k + 1)
+            PB.route_batch(ctx, b, dn, out, mode)
+            if e is not None:
+                e[3].record(S)
+            PB.admit_batch(ctx, b, out, now[0], True)
+            if e is not None:
+                e[4].record(S)
+            PB.release_batch(ctx, b, out)
+            if e is not None:
+                e[5].record(S)
+            now[0] += 1.0
+
+    run_steps(args.warmup)
     torch.cuda.synchronize()
     ctx.check_device_error()
 
@@ -362,22 +423,26 @@ def run_ours(args):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    launches0 = ctx.kernel_launches()
+    launches0 = ctx.kernel_launches() + (hctx.kernel_launches() if overlap else 0)
     ev_all = [[torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)]
               for _ in range(args.steps)]
+    hev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)] if overlap else None
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record()
-    for s in range(args.steps):
-        one_step(ev_all[s])
-    t_end.record()
+    t_start.record(S)
+    run_steps(args.steps, ev_all, hev)
+    t_end.record(S)
     torch.cuda.synchronize()
-    launches = ctx.kernel_launches() - launches0
+    launches = ctx.kernel_launches() + (hctx.kernel_launches() if overlap else 0) - launches0
     clk = clocks.stop()
     ctx.check_device_error()
     ms = t_start.elapsed_time(t_end)
     phase_ms = {p: sum(e[i].elapsed_time(e[i + 1]) for e in ev_all) / args.steps
                 for i, p in enumerate(phases)}
+    if overlap:  # K1 itself, timed on its own stream
+        phase_ms["hash"] = sum(a.elapsed_time(b) for a, b in hev) / args.steps
+        phase_ms["hash_wait"] = sum(e[0].elapsed_time(e[1]) for e in ev_all) / args.steps
     if ws > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -477,7 +542,10 @@ def run_ours(args):
                 "placed_per_step": n_placed, "admitted_per_step": n_admitted,
                 "l2_flush": "none needed: step inputs (tokens %.2f GB) exceed the 126 MB L2"
                             % (tr.n_tokens * 8 / 1e9),
-                "parallelism": f"replica shards x{ws} (weak)"},
+                "parallelism": f"replica shards x{ws} (weak)",
+                "k1_overlap": (f"K1 of step k+1 on a second stream (grid = SMs - {args.free_sms}) "
+                               "while step k routes/admits; every step still hashes its own "
+                               "burst inside the timed region") if overlap else "none (serial)"},
             "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1)", "achieved": hash_gbs,
                          "peak": peak, "unit": "GB/s", "frac": hash_gbs / peak,
                          "traffic": traffic, "peak_source": peak_src,
@@ -539,10 +607,55 @@ def run_sharded(args, ws, rank, local, dev):
     dist.all_reduce(tt)
     st = ShardedStep(ctx, plan, db, dn, dev, cl.kv_capacity[base:base + n_loc], int(tt.item()))
     st.build_directory()
+    overlap = args.free_sms >= 0
+    S = torch.cuda.Stream(device=dev, priority=-1) if overlap else torch.cuda.current_stream(dev)
+    torch.cuda.set_stream(S)
+    PB.bind_current_stream(ctx)
+    if overlap:
+        # as in run_ours: K1 of step k+1 on its own ctx/stream, launched once step k's route
+        # rows are all-gathered (every peer is done reading the other input set by then)
+        import copy
+        import ctypes
+        H = torch.cuda.Stream(device=dev, priority=0)
+        hctx = Context(0, [], [], args.block, device=local)
+        hctx.set_stream(ctypes.c_void_p(H.cuda_stream))
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
+        db2 = copy.copy(db)
+        db2.hashes = torch.empty_like(db.hashes)
+        st2 = ShardedStep(ctx, plan, db2, dn, dev, cl.kv_capacity[base:base + n_loc],
+                          int(tt.item()))
+        sts, bufs = [st, st2], [db, db2]
+        ev_h = [torch.cuda.Event() for _ in range(2)]
     now = [1.0]
-    for _ in range(args.warmup):
-        st.step(now[0])
-        now[0] += 1.0
+
+    def run_steps(n, evh=None):
+        if not overlap:
+            out = None
+            for k in range(n):
+                out = st.step(now[0], ev_hash=evh[k] if evh else None)
+                now[0] += 1.0
+            return out
+
+        def hash_into(k):
+            H.wait_stream(S)
+            if evh:
+                evh[k][0].record(H)
+            PB.hash_batch(hctx, bufs[k % 2])
+            if evh:
+                evh[k][1].record(H)
+            ev_h[k % 2].record(H)
+
+        hash_into(0)
+        out = None
+        for k in range(n):
+            S.wait_event(ev_h[k % 2])
+            nxt = (lambda kk=k + 1: hash_into(kk)) if k + 1 < n else None
+            out = sts[k % 2].step(now[0], prehashed=True, after_gather=nxt)
+            now[0] += 1.0
+        return out
+
+    run_steps(args.warmup)
     torch.cuda.synchronize()
     ctx.check_device_error()
     dist.barrier()
@@ -550,19 +663,16 @@ def run_sharded(args, ws, rank, local, dev):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    launches0 = ctx.kernel_launches()
+    launches0 = ctx.kernel_launches() + (hctx.kernel_launches() if overlap else 0)
     evh = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     t0e = torch.cuda.Event(enable_timing=True)
     t1e = torch.cuda.Event(enable_timing=True)
-    t0e.record()
-    n_here = 0
-    for s_ in range(args.steps):
-        out = st.step(now[0], ev_hash=evh[s_])
-        now[0] += 1.0
-    t1e.record()
+    t0e.record(S)
+    out = run_steps(args.steps, evh)
+    t1e.record(S)
     torch.cuda.synchronize()
-    launches = ctx.kernel_launches() - launches0
+    launches = ctx.kernel_launches() + (hctx.kernel_launches() if overlap else 0) - launches0
     clk = clocks.stop()
     ctx.check_device_error()
     ms = t0e.elapsed_time(t1e)
@@ -640,7 +750,9 @@ def run_sharded(args, ws, rank, local, dev):
                 "parallelism": (f"replica shards x{ws}: NCCL all-gather of route inputs; owner "
                                 f"GPUs pull placed requests' tokens/hashes and peers' L2/L3 "
                                 f"erase lists and results over NVLink P2P (CUDA IPC); one "
-                                f"NCCL stream barrier; no host sync in the step")},
+                                f"NCCL stream barrier; no host sync in the step"),
+                "k1_overlap": (f"K1 of step k+1 on a second stream (grid = SMs - {args.free_sms}) "
+                               "from step k's all-gather on") if overlap else "none (serial)"},
             "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1), rank 0",
                          "achieved": hash_gbs, "peak": peak, "unit": "GB/s",
                          "frac": hash_gbs / peak, "traffic": None, "peak_source": peak_src,

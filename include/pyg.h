@@ -183,6 +183,10 @@ int pyg_hash_offsets_dev(pyg_ctx* ctx, const int64_t* d_tok_off, int32_t n_req,
 /* K1: chain_boundary_hashes for every request of the batch. */
 int pyg_hash_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
                        int32_t n_req, const int64_t* d_hash_off, uint64_t* d_hashes);
+/* Caps K1's persistent grid at n_ctas CTAs (0 = one per SM, the default).  A hashing ctx
+   whose K1 overlaps another ctx's step on a second stream leaves SMs free for the step's
+   latency-bound kernels (route, admission) this way. */
+int pyg_set_hash_ctas(pyg_ctx* ctx, int32_t n_ctas);
 
 /* K2: staged matrix.  For request r and its j-th candidate replica cand[cand_off[g_r]+j]
    (g_r = d_group[r] < n_groups), d_staged[r*max_cand + j] = tier(L2).matched_prefix(prompt_r)

@@ -74,6 +74,7 @@ _sig("pyg_create", C.POINTER(Config), C.POINTER(vp))
 _sig("pyg_destroy", vp, res=None)
 _sig("pyg_last_error", res=C.c_char_p)
 _sig("pyg_set_stream", vp, vp)
+_sig("pyg_set_hash_ctas", vp, i32)
 _sig("pyg_synchronize", vp)
 _sig("pyg_kernel_launches", vp, res=i64)
 _sig("pyg_set_capacity", vp, i32, i64, i64)
@@ -204,6 +205,9 @@ class Context:
     # -- plumbing
     def set_stream(self, stream_ptr):
         check(_lib.pyg_set_stream(self.h, stream_ptr))
+
+    def set_hash_ctas(self, n):
+        check(_lib.pyg_set_hash_ctas(self.h, int(n)))
 
     def synchronize(self):
         check(_lib.pyg_synchronize(self.h))

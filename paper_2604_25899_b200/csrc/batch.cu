@@ -130,7 +130,7 @@ struct ChainGetB {
 //   erase_chain_span(L2, l1, l1 + l2_part)         (engine.cpp:825)
 //   [erase_chain_span(L3, max(l1,l2), reusable)]   deferred to k_l3_erase
 //   insert_chain(L1, seq, len, lineage, now, +1)   (engine.cpp:829)
-__global__ void __launch_bounds__(512) k_admit(CtxDev c, AdmitArgs a) {
+__global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t sm[64];
   __shared__ int64_t bc[4];

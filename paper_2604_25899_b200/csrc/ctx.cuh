@@ -42,6 +42,7 @@ struct pyg_ctx {
   int32_t n_global = 0;      // replicas in the cluster
   int32_t rep_base = 0;      // global index of this ctx's replica 0
   int64_t dir_admits = 0;    // admission calls since the last build (cleared bits accumulate)
+  int32_t hash_ctas = 0;     // K1 persistent grid cap (0 = one CTA per SM)
 };
 
 namespace pyg_host {

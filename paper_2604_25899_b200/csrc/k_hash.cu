@@ -10,7 +10,9 @@
 // length order (a 16-bit radix sort on ceil(len/4)) so lanes of a warp carry
 // equal work and the longest chains start first.
 //
-// Occupancy: ONE 8-warp CTA per SM (2 warps per scheduler).  The FNV chain is
+// Occupancy: ONE 8-warp CTA per SM (2 warps per scheduler), registers capped at 128
+// (no spills) so that while K1 hashes the NEXT burst on a second stream, the current
+// step's admission / routing CTAs can still be resident on the same SMs.  The FNV chain is
 // latency-bound per lane (~119 cycles/token measured, tools/k1/fnv_core.cu) and
 // the INT pipes cap the SM at ~512 Gtok/s (4.1 TB/s of token bytes); two warps
 // per scheduler already saturate issue, and more co-resident warps only slow
@@ -49,7 +51,7 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 // block boundary always coincides with the end of a chunk: the emit decision
 // is per chunk and warp-uniform (no per-token test).  The last, partial chunk
 // and B % 16 != 0 take the generic per-token path.
-__global__ void __launch_bounds__(kWarps * 32, 1)
+__global__ void __launch_bounds__(kWarps * 32, 2)
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
               uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task) {
@@ -202,12 +204,19 @@ int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_to
   const int tasks = (R + 31) / 32;
   static int n_sm = 0;
   if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
-  const int grid = std::min((tasks + kWarps - 1) / kWarps, n_sm);  // persistent: 1 CTA/SM
+  const int cap = c->hash_ctas > 0 ? std::min(c->hash_ctas, n_sm) : n_sm;
+  const int grid = std::min((tasks + kWarps - 1) / kWarps, cap);  // persistent: 1 CTA/SM
   auto* ctr = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
   PYG_CUDA(cudaMemsetAsync(ctr, 0, 4, c->stream));
   k_hash_staged<<<grid, per_block, kSmemBytes, c->stream>>>(
       d_tokens, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr);
   PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_set_hash_ctas(pyg_ctx* c, int32_t n_ctas) {
+  if (!c || n_ctas < 0) return PYG_EINVAL;
+  c->hash_ctas = n_ctas;
   return PYG_OK;
 }
 

@@ -226,8 +226,12 @@ class ShardedStep:
 
     # ---------------------------------------------------------------- the step
     def step(self, now: float, speculative=True, release=True, mode=1, ev_hash=None,
-             marks=None):
-        """marks: optional list; (name, cuda event, host time) appended at phase ends."""
+             marks=None, prehashed=False, after_gather=None):
+        """marks: optional list; (name, cuda event, host time) appended at phase ends.
+        prehashed: the batch's boundary hashes are already in batch.hashes (K1 ran on another
+        stream).  after_gather: called once the all-gather of the route rows is enqueued --
+        from there on every rank has finished the previous step, so peers no longer read
+        this rank's other input set (the next step's K1 may overwrite it)."""
         ctx, plan, b, nodes, PB = self.ctx, self.plan, self.b, self.nodes, self.PB
 
         def mark(name):
@@ -242,11 +246,12 @@ class ShardedStep:
         lib = _lib._lib
         W = plan.world
         # 1-2: local hash + staged rows
-        if ev_hash:
-            ev_hash[0].record()
-        PB.hash_batch(ctx, b)
-        if ev_hash:
-            ev_hash[1].record()
+        if not prehashed:
+            if ev_hash:
+                ev_hash[0].record()
+            PB.hash_batch(ctx, b)
+            if ev_hash:
+                ev_hash[1].record()
         check(lib.pyg_staged_matrix_dev(ctx.h, _ptr(b.tokens), _ptr(b.tok_off), _ptr(b.hash_off),
                                         _ptr(b.hashes), plan.R_local, _ptr(b.group),
                                         nodes.n_groups, _ptr(nodes.cand_off), _ptr(nodes.cand),
@@ -262,6 +267,8 @@ class ShardedStep:
         check(lib.pyg_shard_unpack_dev(ctx.h, _ptr(g_rows), plan.R_total, mc, self.s16,
                                        _ptr(self.g_res), _ptr(self.g_group), _ptr(self.g_staged)))
         g_res, g_group, g_staged = self.g_res, self.g_group, self.g_staged
+        if after_gather is not None:
+            after_gather()
         mark("allgather")
         # 4: route the whole burst (identical on every rank)
         ns = nodes.struct()
