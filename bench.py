@@ -475,9 +475,10 @@ def run_ours(args):
                      for x in (dn.replica_id, dn.kv_capacity, dn.asg_off, dn.asg, dn.cand_off,
                                dn.cand))
 
-        def run_step(b, k):
-            PB.hash_batch(ctx, b)
+        def run_step(b, k, after_gather):
+            # K1 already ran on the pipeline's prep stream
             PB.staged_matrix(ctx, b, dn, out)
+            after_gather()
             PB.route_batch(ctx, b, dn, out, mode)
             PB.admit_batch(ctx, b, out, now[0] + k, True)
             PB.release_batch(ctx, b, out)
@@ -496,10 +497,10 @@ def run_ours(args):
                "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": e_ms / e2e_steps,
                "via": ("public API with device prompt assembly: per step the segment "
                        "descriptors, fresh tokens and request metadata are uploaded from pinned "
-                       "memory (copy stream) and the prompts gathered from the HBM-resident "
-                       "exchange history (pyg_assemble_dev, assembly stream), both overlapped "
-                       "with the previous step; the full step runs and decisions/admissions/"
-                       "matches are copied back"),
+                       "memory (copy stream), the prompts gathered from the HBM-resident "
+                       "exchange history and hashed in one fused pass (pyg_assemble_hash_dev) on a prep stream, "
+                       "all overlapped with earlier steps (3 staging sets, 2 batch sets); the "
+                       "rest of the step runs and decisions/admissions/matches are copied back"),
                "fresh_tokens_per_step": pipe.pools[0].fresh_tokens}
         hs = PB.HostStep(ctx, tr.tokens_np(), tr.tok_off, tr.res, tr.group, tr.wf, tr.role, cl)
         for _ in range(2):
@@ -705,8 +706,8 @@ def run_sharded(args, ws, rank, local, dev):
         steps_of = {id(db): st, id(db1): st1}
         a0 = plan.req_base
 
-        def run_step(b, k):
-            o = steps_of[id(b)].step(now[0] + k)
+        def run_step(b, k, after_gather):
+            o = steps_of[id(b)].step(now[0] + k, prehashed=True, after_gather=after_gather)
             return o["decisions"][a0:a0 + plan.R_local], o["admitted"], o["match3"]
 
         res_like = (torch.empty((plan.R_local, 3), dtype=torch.int64),
@@ -730,9 +731,9 @@ def run_sharded(args, ws, rank, local, dev):
                "h2d_bytes_per_step": int(hb[0].item()),
                "d2h_bytes_per_step": int(pipe.d2h_bytes * ws), "ms_per_step": e_ms / e_steps,
                "via": ("ShardedStep through the public API with device prompt assembly: per rank "
-                       "and step, segment descriptors + fresh tokens + metadata uploaded and "
-                       "prompts assembled on side streams overlapping the previous step; bytes "
-                       "summed over ranks"),
+                       "and step, segment descriptors + fresh tokens + metadata uploaded, "
+                       "prompts assembled and hashed (K1) on side streams overlapping earlier "
+                       "steps; bytes summed over ranks"),
                "fresh_tokens_per_step": int(hb[1].item())}
     if rank == 0:
         line = {

@@ -397,6 +397,17 @@ typedef struct {
 int pyg_assemble_dev(pyg_ctx* ctx, int32_t n_req, const int64_t* d_seg_off,
                      const pyg_segment* d_segs, const uint64_t* d_pool, int64_t* d_tok_off,
                      uint64_t* d_tokens);
+/* Prompt assembly fused with K1: the same d_tok_off / d_tokens as pyg_assemble_dev, plus
+   d_hash_off[n_req+1] (exclusive scan of ceil(len/B)) and the boundary hashes d_hashes of
+   pyg_hash_batch_dev (chain_boundary_hashes, hierarchy.cpp:21-30), in one pass over the
+   pool: the hashing kernel stages each request's tokens from the pool segments and writes
+   them to d_tokens as it hashes.  n_segs = d_seg_off[n_req] and n_tokens >= the total prompt
+   length size its work buffers (the host knows both: it built the descriptors); a device
+   error is flagged if the batch exceeds them. */
+int pyg_assemble_hash_dev(pyg_ctx* ctx, int32_t n_req, const int64_t* d_seg_off,
+                          const pyg_segment* d_segs, int64_t n_segs, const uint64_t* d_pool,
+                          int64_t n_tokens, int64_t* d_tok_off, uint64_t* d_tokens,
+                          int64_t* d_hash_off, uint64_t* d_hashes);
 
 /* ----------------------------------------- worker batch formation / preemption (§8f-3) */
 /* sched::QueueItem (worker.hpp:11-16) with the request id replaced by its rank in the

@@ -79,6 +79,7 @@ _sig("pyg_synchronize", vp)
 _sig("pyg_kernel_launches", vp, res=i64)
 _sig("pyg_set_capacity", vp, i32, i64, i64)
 _sig("pyg_assemble_dev", vp, i32, vp, vp, vp, vp, vp)
+_sig("pyg_assemble_hash_dev", vp, i32, vp, vp, i64, vp, i64, vp, vp, vp, vp)
 _sig("pyg_form_batch_dev", vp, i32, vp, vp, vp, vp, dbl, dbl, vp, vp)
 _sig("pyg_preemption_victim_dev", vp, i32, vp, vp, dbl, dbl, vp)
 _sig("pyg_stage_plan_dev", vp, vp, vp, vp, vp, i32, vp, i32, vp, vp, i32, vp, vp, vp)

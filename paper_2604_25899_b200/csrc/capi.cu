@@ -67,6 +67,21 @@ int scratch(pyg_ctx* c, size_t bytes, void** out) {
   return PYG_OK;
 }
 
+int aux(pyg_ctx* c, size_t bytes, void** out) {
+  if (bytes > c->d_aux_size) {
+    if (c->d_aux) {
+      PYG_CUDA(cudaStreamSynchronize(c->stream));
+      PYG_CUDA(cudaFree(c->d_aux));
+      c->d_aux = nullptr;
+    }
+    size_t sz = std::max<size_t>(bytes + bytes / 8, 1 << 20);
+    PYG_CUDA(cudaMalloc(&c->d_aux, sz));
+    c->d_aux_size = sz;
+  }
+  *out = c->d_aux;
+  return PYG_OK;
+}
+
 }  // namespace pyg_host
 
 using namespace pyg_host;
@@ -261,6 +276,7 @@ void pyg_destroy(pyg_ctx* c) {
   cudaFree(c->hd.reg_present);
   cudaFree(c->hd.reg_mask);
   cudaFree(c->d_scratch);
+  cudaFree(c->d_aux);
   cudaFree(c->d_list);
   cudaFree(c->dir_mem);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);

@@ -43,6 +43,8 @@ struct pyg_ctx {
   int32_t rep_base = 0;      // global index of this ctx's replica 0
   int64_t dir_admits = 0;    // admission calls since the last build (cleared bits accumulate)
   int32_t hash_ctas = 0;     // K1 persistent grid cap (0 = one CTA per SM)
+  void* d_aux = nullptr;     // second on-demand buffer (fused assembly's chunk sources)
+  size_t d_aux_size = 0;
 };
 
 namespace pyg_host {
@@ -52,7 +54,10 @@ int tier_index(pyg_ctx* c, int32_t replica, int32_t tier, bool hierarchy_level, 
 int ensure_capacity(pyg_ctx* c, int ti, int64_t k_new);
 int read_tier(pyg_ctx* c, int ti, pyg::TierDev* out);
 int scratch(pyg_ctx* c, size_t bytes, void** out);
+int aux(pyg_ctx* c, size_t bytes, void** out);
 inline void dir_touch(pyg_ctx* c) { c->dir_dirty = true; }
+int assemble_offsets(pyg_ctx* c, int32_t R, const int64_t* d_seg_off, const pyg_segment* d_segs,
+                     int64_t* d_tok_off);
 inline void count_launch(pyg_ctx* c, int n = 1) { c->launches += n; }
 }  // namespace pyg_host
 

@@ -37,7 +37,16 @@ constexpr int kChunk = 16;                      // tokens per staged chunk
 constexpr int kRowBytes = kChunk * 8 + 16;      // 144: padded row
 constexpr int kStageBytes = 32 * kRowBytes;     // one warp, one stage
 constexpr int kWarps = 8;                       // warps per CTA
-constexpr int kSmemBytes = kWarps * 2 * kStageBytes;
+// per warp (fused assembly): 2 staging buffers, the destination base of each of its 32
+// requests and 4 rotating slots of their packed chunk sources (8 B each).  Slot entries of
+// request l sit at position perm(l) = (l & 1) * 16 + (l >> 1), so the 16 requests a
+// half-warp loads (l = 2t + sub) are 128 contiguous bytes: 8 broadcast LDS.128.
+constexpr int kMetaBytes = 5 * 32 * 8;
+constexpr int kSmemBytes = kWarps * (2 * kStageBytes + kMetaBytes);
+// packed chunk source: pointer | (valid tokens in the chunk, 0..16) << 59
+constexpr int kVShift = 59;
+constexpr unsigned long long kPtrMask = (1ull << kVShift) - 1;
+__device__ __forceinline__ int perm_slot(int l) { return (l & 1) * 16 + (l >> 1); }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -47,17 +56,101 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
+// Prompt source of K1.  kGather = false: the token CSR (tokens + tok_off).  kGather =
+// true: K1 fused with prompt assembly (pyg_assemble_hash_dev) -- request r's tokens are
+// the concatenation of its segments of a device token pool.  k_chunk_src first resolves
+// every 16-token chunk of every request to ONE source pointer: the pool position of the
+// chunk's first token when the chunk lies inside one segment (the common case), else a
+// private 16-token copy in a side buffer (chunks that straddle segment boundaries; at most
+// one per segment).  The K1 loader then reads chunk c of request r at src[c] + q exactly
+// like the CSR path, with the pointers prefetched two chunks ahead by the request's own
+// lane, and the warp writes each staged chunk back to the token CSR (coalesced) while it
+// hashes.  Chunk table index of (r, c) = tok_off[r] / 16 + r + c (no scan needed: request
+// r owns ceil(len/16) <= tok_off[r+1]/16 - tok_off[r]/16 + 1 slots).
+struct GatherSrc {
+  const unsigned long long* chunk_src;  // packed (pointer | valid << 59)
+  uint64_t* tokens_out;
+};
+
+__global__ void k_chunk_src(int R, const int64_t* __restrict__ seg_off,
+                            const pyg_segment* __restrict__ segs, const uint64_t* __restrict__ pool,
+                            const int64_t* __restrict__ tok_off, unsigned long long* tab,
+                            int64_t tab_cap, uint64_t* side, int64_t side_cap,
+                            unsigned long long* side_ctr, int32_t* error) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < R; r += warps) {
+    const int64_t s = tok_off[r], n = tok_off[r + 1] - s;
+    const int64_t nch = (n + kChunk - 1) / kChunk;
+    const int64_t base = s / kChunk + r;
+    if (base + nch > tab_cap) {
+      if (lane == 0) atomicExch(error, 4);  // caller's n_tokens bound too small
+      continue;
+    }
+    const int64_t k1 = seg_off[r + 1];
+    int64_t k = seg_off[r], ps = 0;  // this lane's cursor: segment k covers [ps, ps + len)
+    for (int64_t c0 = 0; c0 < nch; c0 += 32) {
+      const int64_t c = c0 + lane;
+      const bool act = c < nch;
+      const int64_t p0 = c * kChunk, p1 = min(p0 + kChunk, n);
+      pyg_segment sg{0, 0};
+      bool straddle = false;
+      if (act) {
+        while (k < k1) {
+          sg = segs[k];
+          if (ps + sg.len > p0) break;
+          ps += sg.len;
+          ++k;
+        }
+        straddle = p1 > ps + sg.len;
+      }
+      const unsigned m = __ballot_sync(kFull, straddle);
+      unsigned long long b0 = 0;
+      if (m && lane == __ffs(m) - 1) b0 = atomicAdd(side_ctr, static_cast<unsigned long long>(__popc(m)));
+      b0 = __shfl_sync(kFull, b0, __ffs(m ? m : 1) - 1);
+      if (!act) continue;
+      if (!straddle) {
+        tab[base + c] = reinterpret_cast<unsigned long long>(pool + sg.src + (p0 - ps)) |
+                        (static_cast<unsigned long long>(p1 - p0) << kVShift);
+      } else {
+        const int64_t idx = static_cast<int64_t>(b0) + __popc(m & ((1u << lane) - 1));
+        if (idx >= side_cap) {
+          atomicExch(error, 4);
+          continue;
+        }
+        uint64_t* dst = side + idx * kChunk;
+        int64_t kk = k, pp = ps;
+        pyg_segment g = sg;
+        for (int64_t p = p0; p < p1; ++p) {
+          while (p >= pp + g.len) {
+            pp += g.len;
+            g = segs[++kk];
+          }
+          dst[p - p0] = pool[g.src + (p - pp)];
+        }
+        tab[base + c] = reinterpret_cast<unsigned long long>(dst) |
+                        (static_cast<unsigned long long>(p1 - p0) << kVShift);
+      }
+    }
+  }
+}
+
 // Chunks are aligned to each request's own first token, so with B % 16 == 0 a
 // block boundary always coincides with the end of a chunk: the emit decision
 // is per chunk and warp-uniform (no per-token test).  The last, partial chunk
 // and B % 16 != 0 take the generic per-token path.
+template <bool kGather>
 __global__ void __launch_bounds__(kWarps * 32, 2)
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
-              uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task) {
+              uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task, GatherSrc g) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbuf = smem + warp * 2 * kStageBytes;
+  // fused assembly: wbase[32] destination bases, lsl[4][32] packed chunk sources
+  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(
+      smem + kWarps * 2 * kStageBytes + warp * kMetaBytes);
+  unsigned long long* lsl = wbase + 32;
   const int ntasks = (R + 31) / 32;
   // persistent: each warp pulls 32-request tasks, longest first, until none are left
   for (;;) {
@@ -78,18 +171,82 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   const int cpb = fast ? B / kChunk : 1;  // chunks per block (fast path)
   int cc = cpb;
 
+  // fused assembly: chunk c's packed source of every request of the warp sits in smem slot
+  // lsl[c % 4][perm(request)]; each lane prefetches its own request's entry for chunk c + 2
+  // with cp.async in chunk c's copy group (complete before issue(c + 2) runs), and the
+  // slot of chunk c survives until write_out(c) has used its valid counts
+  const unsigned long long* csrc = nullptr;
   const int sub = lane >> 4, q = lane & 15;  // 2 requests per instruction, 16 lanes x 8 B
+  const int me = perm_slot(lane);
+  if (kGather) {
+    __syncwarp();  // the previous task's readers of the slots are done
+    wbase[me] = reinterpret_cast<unsigned long long>(g.tokens_out + s);
+    csrc = g.chunk_src + (valid ? s / kChunk + r : 0);
+    lsl[me] = nch > 0 ? csrc[0] : 0ull;
+    lsl[32 + me] = nch > 1 ? csrc[1] : 0ull;
+    __syncwarp();
+  }
+
   auto issue = [&](int c) {
     unsigned char* st = wbuf + (c & 1) * kStageBytes;
+    const int64_t pos = static_cast<int64_t>(c) * kChunk + q;
+    if (kGather) {
+      const unsigned long long* slot = lsl + (c & 3) * 32 + sub * 16;
+      unsigned long long e[16];
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) {
-      const int jj = j + sub;
-      const int64_t sj = __shfl_sync(kFull, s, jj);
-      const int64_t nj = __shfl_sync(kFull, n, jj);
-      const int64_t pos = static_cast<int64_t>(c) * kChunk + q;
-      if (pos < nj) cp_async8(st + jj * kRowBytes + q * 8, tokens + sj + pos, 8);
+      for (int t = 0; t < 16; t += 2) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(slot + t);
+        e[t] = v.x;
+        e[t + 1] = v.y;
+      }
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        if (q < static_cast<int>(e[t] >> kVShift))
+          cp_async8(st + (2 * t + sub) * kRowBytes + q * 8,
+                    reinterpret_cast<const uint64_t*>(e[t] & kPtrMask) + q, 8);
+      }
+      unsigned long long* nxt = lsl + ((c + 2) & 3) * 32 + me;
+      if (c + 2 < nch)
+        cp_async8(nxt, csrc + c + 2, 8);
+      else
+        *nxt = 0ull;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const int jj = j + sub;
+        const int64_t sj = __shfl_sync(kFull, s, jj);
+        const int64_t nj = __shfl_sync(kFull, n, jj);
+        if (pos < nj) cp_async8(st + jj * kRowBytes + q * 8, tokens + sj + pos, 8);
+      }
     }
     cp_commit();
+  };
+  // fused assembly: write staged chunk c of the warp's 32 requests to the token CSR
+  auto write_out = [&](int c) {
+    const unsigned char* st = wbuf + (c & 1) * kStageBytes;
+    const unsigned long long* slot = lsl + (c & 3) * 32 + sub * 16;
+    const unsigned long long* wb = wbase + sub * 16;
+#pragma unroll
+    for (int h8 = 0; h8 < 16; h8 += 8) {
+      unsigned long long e[8], d[8];
+      uint64_t v[8];
+#pragma unroll
+      for (int t = 0; t < 8; t += 2) {
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(slot + h8 + t);
+        const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(wb + h8 + t);
+        e[t] = a.x;
+        e[t + 1] = a.y;
+        d[t] = b.x;
+        d[t + 1] = b.y;
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        v[t] = *reinterpret_cast<const uint64_t*>(st + (2 * (h8 + t) + sub) * kRowBytes + q * 8);
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (q < static_cast<int>(e[t] >> kVShift))
+          reinterpret_cast<uint64_t*>(d[t])[static_cast<int64_t>(c) * kChunk + q] = v[t];
+    }
   };
 
   uint64_t h = kFnvOffset;
@@ -102,6 +259,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
       cp_commit();
     cp_wait1();
     __syncwarp();
+    if (kGather) write_out(c);
     if (c < nch) {
       const unsigned char* row = wbuf + (c & 1) * kStageBytes + lane * kRowBytes;
       const int64_t rem = n - static_cast<int64_t>(c) * kChunk;
@@ -170,11 +328,12 @@ int pyg_hash_offsets_dev(pyg_ctx* c, const int64_t* d_tok_off, int32_t R, int64_
   return PYG_OK;
 }
 
-int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off, int32_t R,
-                       const int64_t* d_hash_off, uint64_t* d_hashes) {
-  if (!c || R < 0) return PYG_EINVAL;
-  if (R == 0) return PYG_OK;
-  // length sort (descending) for warp balance
+}  // extern "C"
+
+// length sort (descending, for warp balance) + the persistent K1 launch
+template <bool kGather>
+static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_off, int32_t R,
+                       const int64_t* d_hash_off, uint64_t* d_hashes, GatherSrc g) {
   size_t tmp = 0;
   PYG_CUDA(cub::DeviceRadixSort::SortPairsDescending(
       nullptr, tmp, static_cast<uint16_t*>(nullptr), static_cast<uint16_t*>(nullptr),
@@ -197,7 +356,8 @@ int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_to
   PYG_LAUNCHED(c);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_hash_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(k_hash_staged<kGather>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBytes);
     attr = true;
   }
   const int per_block = kWarps * 32;
@@ -208,10 +368,48 @@ int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_to
   const int grid = std::min((tasks + kWarps - 1) / kWarps, cap);  // persistent: 1 CTA/SM
   auto* ctr = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
   PYG_CUDA(cudaMemsetAsync(ctr, 0, 4, c->stream));
-  k_hash_staged<<<grid, per_block, kSmemBytes, c->stream>>>(
-      d_tokens, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr);
+  k_hash_staged<kGather><<<grid, per_block, kSmemBytes, c->stream>>>(
+      d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr, g);
   PYG_LAUNCHED(c);
   return PYG_OK;
+}
+
+extern "C" {
+
+int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off, int32_t R,
+                       const int64_t* d_hash_off, uint64_t* d_hashes) {
+  if (!c || R < 0) return PYG_EINVAL;
+  if (R == 0) return PYG_OK;
+  return hash_launch<false>(c, d_tokens, d_tok_off, R, d_hash_off, d_hashes, GatherSrc{});
+}
+
+int pyg_assemble_hash_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
+                          const pyg_segment* d_segs, int64_t n_segs, const uint64_t* d_pool,
+                          int64_t n_tokens, int64_t* d_tok_off, uint64_t* d_tokens,
+                          int64_t* d_hash_off, uint64_t* d_hashes) {
+  if (!c || R < 0 || n_segs < 0 || n_tokens < 0) return PYG_EINVAL;
+  int rc = pyg_host::assemble_offsets(c, R, d_seg_off, d_segs, d_tok_off);
+  if (rc) return rc;
+  rc = pyg_hash_offsets_dev(c, d_tok_off, R, d_hash_off, nullptr);
+  if (rc || R == 0) return rc;
+  // chunk source table + side buffer for boundary-straddling chunks
+  const int64_t tab_cap = n_tokens / kChunk + R + 1;
+  const int64_t side_cap = std::max<int64_t>(n_segs, 1);
+  const size_t tb = (static_cast<size_t>(tab_cap) * 8 + 255) & ~size_t{255};
+  void* ap;
+  rc = aux(c, tb + static_cast<size_t>(side_cap) * kChunk * 8 + 256, &ap);
+  if (rc) return rc;
+  auto* tab = static_cast<unsigned long long*>(ap);
+  auto* side = reinterpret_cast<uint64_t*>(static_cast<char*>(ap) + tb);
+  auto* ctr = reinterpret_cast<unsigned long long*>(side + side_cap * kChunk);
+  PYG_CUDA(cudaMemsetAsync(ctr, 0, 8, c->stream));
+  static int n_sm = 0;
+  if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
+  k_chunk_src<<<std::min((R + 7) / 8, 16 * n_sm), 256, 0, c->stream>>>(
+      R, d_seg_off, d_segs, d_pool, d_tok_off, tab, tab_cap, side, side_cap, ctr, c->hd.error);
+  PYG_LAUNCHED(c);
+  return hash_launch<true>(c, d_pool, d_tok_off, R, d_hash_off, d_hashes,
+                           GatherSrc{tab, d_tokens});
 }
 
 int pyg_set_hash_ctas(pyg_ctx* c, int32_t n_ctas) {

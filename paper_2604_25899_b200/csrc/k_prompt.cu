@@ -40,7 +40,19 @@ __global__ void k_gather(int R, const int64_t* seg_off, const pyg_segment* segs,
     for (int64_t k = seg_off[r]; k < seg_off[r + 1]; ++k) {
       const pyg_segment sg = segs[k];
       const uint64_t* src = pool + sg.src;
-      for (int64_t i = threadIdx.x; i < sg.len; i += blockDim.x) tokens[dst + i] = src[i];
+      uint64_t* out = tokens + dst;
+      const int64_t bd = blockDim.x;
+      int64_t i = threadIdx.x;
+      // up to four independent 8-byte loads in flight per thread before their stores
+      for (; i < sg.len; i += 4 * bd) {
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i + u * bd < sg.len) v[u] = __ldg(src + i + u * bd);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i + u * bd < sg.len) out[i + u * bd] = v[u];
+      }
       dst += sg.len;
     }
   }
@@ -48,10 +60,10 @@ __global__ void k_gather(int R, const int64_t* seg_off, const pyg_segment* segs,
 
 }  // namespace
 
-extern "C" int pyg_assemble_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
-                                const pyg_segment* d_segs, const uint64_t* d_pool,
-                                int64_t* d_tok_off, uint64_t* d_tokens) {
-  if (!c || R < 0) return PYG_EINVAL;
+namespace pyg_host {
+// request lengths (sum of segment lengths) and their exclusive scan -> d_tok_off[R+1]
+int assemble_offsets(pyg_ctx* c, int32_t R, const int64_t* d_seg_off, const pyg_segment* d_segs,
+                     int64_t* d_tok_off) {
   size_t tmp = 0;
   PYG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, static_cast<int64_t*>(nullptr), d_tok_off,
                                          R + 1, c->stream));
@@ -65,6 +77,16 @@ extern "C" int pyg_assemble_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
   PYG_CUDA(cub::DeviceScan::ExclusiveSum(static_cast<char*>(sp) + lb, tmp, lens, d_tok_off, R + 1,
                                          c->stream));
   PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+}  // namespace pyg_host
+
+extern "C" int pyg_assemble_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
+                                const pyg_segment* d_segs, const uint64_t* d_pool,
+                                int64_t* d_tok_off, uint64_t* d_tokens) {
+  if (!c || R < 0) return PYG_EINVAL;
+  int rc = assemble_offsets(c, R, d_seg_off, d_segs, d_tok_off);
+  if (rc) return rc;
   if (R) {
     static int n_sm = 0;
     if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);

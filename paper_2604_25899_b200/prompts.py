@@ -105,77 +105,147 @@ class PromptPool:
         check(_lib._lib.pyg_assemble_dev(ctx.h, self.R, _p(self.d_seg_off), _p(self.d_segs),
                                          _p(self.pool), _p(tok_off), _p(tokens)))
 
+    def assemble_hash(self, ctx, b):
+        """pyg_assemble_hash_dev: prompts, hash offsets and boundary hashes of DeviceBatch b
+        in one pass (K1 fused with the gather)."""
+        check(_lib._lib.pyg_assemble_hash_dev(ctx.h, self.R, _p(self.d_seg_off),
+                                              _p(self.d_segs), int(self.h_segs.shape[0]),
+                                              _p(self.pool), self.n_tokens, _p(b.tok_off),
+                                              _p(b.tokens), _p(b.hash_off), _p(b.hashes)))
+
 
 class PipelinedSteps:
-    """Step after step through the public API, the next step's host->device upload AND its
-    prompt assembly overlapped with the current step's device work (two input sets, each
-    with its own token / hash buffers):
+    """Step after step through the public API with a three-stage pipeline, so a step's
+    host->device upload, its prompt assembly and its chain hashing (K1) all overlap earlier
+    steps' device work:
 
-      copy stream      upload(k+1) ..................... upload(k+2)
-      assembly stream     assemble(k+1) + hash_off ...........  assemble(k+2)
-      compute          step(k) -> results(k) ........ step(k+1) -> results(k+1)
+      copy stream    upload(k+2) ............................ upload(k+3)
+      prep stream       assemble+K1(k+1) ....................... assemble+K1(k+2)
+      compute        step(k) [K2 | route, admit, release] ... step(k+1) ...
+      d2h stream                                  results(k) ...
 
-    Assembly is HBM-bound and K1 INT-bound, so they share the GPU well.  Assembly runs on
-    its own (replica-less) pyg_ctx so its scratch never races the step's.  Each step
-    still uploads its own inputs (segment descriptors, fresh tokens, request metadata)
-    and copies its own results back.  `run_step(batch, k)` launches the device step
-    (hash_off already computed) for a DeviceBatch holding step k's inputs and returns
-    the tensors to copy back."""
+    * staging sets (3): a step's uploaded inputs -- segment descriptors, fresh tokens,
+      request metadata.  upload(k) only waits for assembly(k-3) to have consumed its set.
+    * batch sets (2): tokens, offsets, boundary hashes, metadata.  prep(k+1) starts at step
+      k's `after_gather` point: for one GPU right after step k's K2 (so K2 keeps the whole
+      GPU), for the sharded step once step k's route rows are all-gathered -- by then every
+      rank has finished step k-1, so no peer still reads batch set (k+1) % 2 over NVLink.
+    * assembly and K1 are one kernel (pyg_assemble_hash_dev: the gather's HBM traffic hides
+      under the INT-bound hashing), run on the prep stream's own (replica-less) pyg_ctx with
+      its grid capped below the SM count, leaving SMs to the step's latency-bound kernels.
+    * results: the step's outputs are snapshotted on the compute stream (device copies)
+      and copied to pinned host memory on their own stream.
+
+    Every step still uploads its own inputs and copies its own results back.
+    `run_step(batch, k, after_gather)` launches the device step for a DeviceBatch whose
+    hashes are already computed, calls `after_gather()` at its safe point and returns the
+    tensors to copy back."""
+
+    STAGING = 3
 
     def __init__(self, ctx, trace, batch, device, run_step, pinned_meta, results_like,
-                 second_batch=None):
+                 second_batch=None, hash_ctas=None):
         from . import batch as PB
         from ._lib import Context
         self.PB, self.ctx, self.dev = PB, ctx, device
-        self.pools = [PromptPool(trace, device=device), None]
-        p0 = self.pools[0]
-        self.pools[1] = _ShiftedFresh(p0)
+        p0 = PromptPool(trace, device=device)
+        self.pools = [p0] + [_ShiftedFresh(p0) for _ in range(self.STAGING - 1)]
         self.batches = [batch, second_batch or clone_batch(batch)]
         self.meta = pinned_meta          # (res, group, wf, role) pinned host tensors
+        self.st_meta = [[torch.empty(t.shape, dtype=t.dtype, device=device) for t in pinned_meta]
+                        for _ in range(self.STAGING)]
         self.results = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in results_like]
                         for _ in range(2)]
+        self.snap = [[torch.empty(t.shape, dtype=t.dtype, device=device) for t in results_like]
+                     for _ in range(2)]
         self.copy = torch.cuda.Stream(device=device)
-        self.asm = torch.cuda.Stream(device=device)
+        self.prep = torch.cuda.Stream(device=device)
+        self.d2h = torch.cuda.Stream(device=device)
         self.compute = torch.cuda.current_stream(device)
         idx = device.index if isinstance(device, torch.device) and device.index is not None \
             else torch.cuda.current_device()
-        self.asm_ctx = Context(0, [], [], ctx.B, device=idx)
-        self.asm_ctx.set_stream(C.c_void_p(self.asm.cuda_stream))
-        self.up = [torch.cuda.Event(), torch.cuda.Event()]
-        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
-        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.prep_ctx = Context(0, [], [], ctx.B, device=idx)
+        self.prep_ctx.set_stream(C.c_void_p(self.prep.cuda_stream))
+        if hash_ctas is None:
+            n_sm = torch.cuda.get_device_properties(idx).multi_processor_count
+            hash_ctas = max(1, n_sm - 8)
+        self.prep_ctx.set_hash_ctas(hash_ctas)
+        E = torch.cuda.Event
+        self.up = [E() for _ in range(self.STAGING)]
+        self.consumed = [E() for _ in range(self.STAGING)]
+        self.ready = [E() for _ in range(2)]
+        self.snapped = [E() for _ in range(2)]
+        self.fetched = [E() for _ in range(2)]
         self.run_step = run_step
+        self.marks = None  # experiments: a list -> (stage, step, stream event) appended
 
-    def _prepare(self, s, wait_done):
-        """upload + assemble input set s (after the step that last used it finished)."""
-        b = self.batches[s]
+    def _mark(self, name, k, stream):
+        if self.marks is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            self.marks.append((name, k, e))
+
+    def _upload(self, k):
+        j = k % self.STAGING
         with torch.cuda.stream(self.copy):
-            if wait_done:
-                self.copy.wait_event(self.done[s])
-            self.pools[s].upload()
-            for dst, src in zip((b.res, b.group, b.wf, b.role), self.meta):
+            if k >= self.STAGING:
+                self.copy.wait_event(self.consumed[j])
+            self._mark("upload0", k, self.copy)
+            self.pools[j].upload()
+            for dst, src in zip(self.st_meta[j], self.meta):
                 dst.copy_(src, non_blocking=True)
-            self.up[s].record(self.copy)
-        with torch.cuda.stream(self.asm):
-            self.asm.wait_event(self.up[s])
-            self.pools[s].assemble(self.asm_ctx, b.tok_off, b.tokens)
-            check(_lib._lib.pyg_hash_offsets_dev(self.asm_ctx.h, _p(b.tok_off), b.R,
-                                                 _p(b.hash_off), None))
-            self.ready[s].record(self.asm)
+            self._mark("upload1", k, self.copy)
+            self.up[j].record(self.copy)
+
+    def _prepare(self, k):
+        """assembly + metadata + hash offsets + K1 of step k into batch set k % 2 (prep
+        stream, ordered after everything issued on the compute stream so far)."""
+        j, b = k % self.STAGING, self.batches[k % 2]
+        with torch.cuda.stream(self.prep):
+            self.prep.wait_stream(self.compute)
+            self.prep.wait_event(self.up[j])
+            self._mark("prep0", k, self.prep)
+            for dst, src in zip((b.res, b.group, b.wf, b.role), self.st_meta[j]):
+                dst.copy_(src, non_blocking=True)
+            # prompt assembly fused with K1: one pass over the pool
+            self.pools[j].assemble_hash(self.prep_ctx, b)
+            self.consumed[j].record(self.prep)
+            self._mark("prep1", k, self.prep)
+            self.ready[k % 2].record(self.prep)
 
     def run(self, steps, first_index=0):
-        self._prepare(0, False)
+        for k in range(min(steps, self.STAGING)):
+            self._upload(k)
+        self._prepare(0)
         for k in range(steps):
             s = k % 2
-            if k + 1 < steps:
-                self._prepare(1 - s, k >= 1)
             self.compute.wait_event(self.ready[s])
+            self._mark("step0", k, self.compute)
             self.PB.bind_current_stream(self.ctx)
-            outs = self.run_step(self.batches[s], first_index + k)
-            for dst, src in zip(self.results[s], outs):
+            called = []
+
+            def nxt(kk=k + 1):
+                if not called and kk < steps:
+                    self._prepare(kk)
+                called.append(1)
+            outs = self.run_step(self.batches[s], first_index + k, nxt)
+            nxt()  # a run_step without a safe point: prepare after the whole step
+            self._mark("step1", k, self.compute)
+            if k >= 2:  # snapshot set s was read back two steps ago
+                self.compute.wait_event(self.fetched[s])
+            for dst, src in zip(self.snap[s], outs):
                 dst.copy_(src, non_blocking=True)
-            self.done[s].record(self.compute)
+            self.snapped[s].record(self.compute)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(self.snapped[s])
+                for dst, src in zip(self.results[s], self.snap[s]):
+                    dst.copy_(src, non_blocking=True)
+                self.fetched[s].record(self.d2h)
+                self._mark("d2h1", k, self.d2h)
+            if k + self.STAGING < steps:
+                self._upload(k + self.STAGING)
         self.compute.synchronize()
+        self.d2h.synchronize()
 
     @property
     def h2d_bytes(self):
@@ -229,3 +299,10 @@ class _ShiftedFresh:
     def assemble(self, ctx, tok_off, tokens):
         check(_lib._lib.pyg_assemble_dev(ctx.h, self.R, _p(self.d_seg_off), _p(self.d_segs),
                                          _p(self.pool_owner.pool), _p(tok_off), _p(tokens)))
+
+    def assemble_hash(self, ctx, b):
+        check(_lib._lib.pyg_assemble_hash_dev(ctx.h, self.R, _p(self.d_seg_off),
+                                              _p(self.d_segs), int(self.h_segs.shape[0]),
+                                              _p(self.pool_owner.pool), self.p0.n_tokens,
+                                              _p(b.tok_off), _p(b.tokens), _p(b.hash_off),
+                                              _p(b.hashes)))
