@@ -332,6 +332,21 @@ int pyg_shard_pack_dev(pyg_ctx* ctx, const pyg_reservation* d_req, const int32_t
 int pyg_shard_unpack_dev(pyg_ctx* ctx, const int32_t* d_rows, int32_t n_req, int32_t max_cand,
                          int32_t staged16, pyg_reservation* d_req, int32_t* d_group,
                          int32_t* d_staged);
+/* The all-gather's NVLink replacement: rebuilds the whole burst's reservations, groups and
+   staged rows straight from every shard's packed rows (d_rows_of[k] = shard k's d_rows as
+   mapped in this process; shard k holds requests [d_req_off[k], d_req_off[k+1])). */
+int pyg_shard_unpack_peer_dev(pyg_ctx* ctx, const int64_t* d_rows_of, int32_t world,
+                              const int64_t* d_req_off, int32_t n_req_total, int32_t max_cand,
+                              int32_t staged16, pyg_reservation* d_req, int32_t* d_group,
+                              int32_t* d_staged);
+/* Cross-GPU stream barrier over peer memory (replaces a one-element NCCL all-reduce).
+   signal: after a system-scope fence, writes seq into slot `me` of every shard's flag array
+   (d_flag_of[k] = shard k's int64 flags[world], mapped here).  wait: blocks this stream until
+   every slot of this shard's own flags (d_flags) is >= seq; a peer that never signals flags a
+   device error after ~10 s instead of hanging. */
+int pyg_shard_signal_dev(pyg_ctx* ctx, const int64_t* d_flag_of, int32_t world, int32_t me,
+                         int64_t seq);
+int pyg_shard_wait_dev(pyg_ctx* ctx, const int64_t* d_flags, int32_t world, int64_t seq);
 /* Pull the received requests' tokens and hashes from their origin shards (peer loads). */
 int pyg_shard_pull_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world,
                        const int64_t* d_req_off, const int32_t* d_recv_gidx,

@@ -125,6 +125,9 @@ _sig("pyg_block_next_use_dev", vp, i32, i32, vp, i32, vp, i32, vp, i64, vp)
 _sig("pyg_registry_from_cursors_dev", vp, i32, i32, vp, vp, vp, vp)
 _sig("pyg_ipc_import", vp, vp, i64, vp)
 _sig("pyg_shard_recv_plan_dev", vp, i32, vp, vp, i32, vp, i64, vp, vp, vp, vp, vp, vp)
+_sig("pyg_shard_unpack_peer_dev", vp, vp, i32, vp, i32, i32, i32, vp, vp, vp)
+_sig("pyg_shard_signal_dev", vp, vp, i32, i32, i64)
+_sig("pyg_shard_wait_dev", vp, vp, i32, i64)
 _sig("pyg_shard_pack_dev", vp, vp, vp, vp, i32, i32, i32, vp)
 _sig("pyg_shard_unpack_dev", vp, vp, i32, i32, i32, vp, vp, vp)
 _sig("pyg_shard_pull_dev", vp, vp, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64)

@@ -146,6 +146,66 @@ __global__ void k_unpack(const int32_t* rows, int R, int mc, int s16, pyg_reserv
   }
 }
 
+// Unpack the whole burst's route rows straight from every shard's row buffer over NVLink
+// (rows_of[k] = shard k's rows, mapped in this process): the NCCL all-gather's replacement.
+__global__ void k_unpack_peer(const int64_t* rows_of, int world, const int64_t* req_off, int R,
+                              int mc, int s16, pyg_reservation* req, int32_t* group,
+                              int32_t* staged) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int k = src_of(req_off, world, r);
+  const int wd = 5 + (s16 ? (mc + 1) / 2 : mc);
+  const int32_t* o = reinterpret_cast<const int32_t*>(rows_of[k]) +
+                     static_cast<int64_t>(r - req_off[k]) * wd;
+  const int64_t t = (static_cast<int64_t>(o[1]) << 32) | static_cast<uint32_t>(o[0]);
+  const int64_t ab = (static_cast<int64_t>(o[3]) << 32) | static_cast<uint32_t>(o[2]);
+  req[r] = pyg_reservation{t, 0, __longlong_as_double(ab), 0};
+  group[r] = o[4];
+  int32_t* st = staged + static_cast<int64_t>(r) * mc;
+  if (s16) {
+    for (int j = 0; j < mc; ++j)
+      st[j] = static_cast<int32_t>((static_cast<uint32_t>(o[5 + j / 2]) >> (16 * (j & 1))) & 0xffffu);
+  } else {
+    for (int j = 0; j < mc; ++j) st[j] = o[5 + j];
+  }
+}
+
+// Cross-GPU stream barrier over peer memory.  signal: after a system-scope fence (this
+// stream's earlier writes -- rows, lists -- are visible to the peers first), store seq into
+// slot [me] of every shard's flag array with release semantics.  wait: spin (acquire) until
+// all `world` slots of this shard's own flag array reach seq; a peer that never arrives
+// (timeout ~10 s) raises the device error instead of hanging the GPU.
+__global__ void k_signal(const int64_t* flag_of, int world, int me, int64_t seq) {
+  const int k = threadIdx.x;
+  __threadfence_system();
+  if (k < world) {
+    int64_t* f = reinterpret_cast<int64_t*>(flag_of[k]) + me;
+    asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(f), "l"(seq) : "memory");
+  }
+}
+
+__global__ void k_wait(const int64_t* flags, int world, int64_t seq, int32_t* err) {
+  const int k = threadIdx.x;
+  if (k < world) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      int64_t v;
+      asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(flags + k) : "memory");
+      if (v >= seq) break;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) {
+        atomicExch(err, 5);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
 __global__ void k_pull(const pyg_peer* peers, int world, const int64_t* req_off,
                        const int32_t* gidx, const int64_t* count, const int64_t* toff,
                        const int64_t* hoff, uint64_t* tok_out, uint64_t* hash_out,
@@ -387,6 +447,32 @@ int pyg_shard_unpack_dev(pyg_ctx* c, const int32_t* d_rows, int32_t R, int32_t m
   if (!c || R < 0 || mc < 0) return PYG_EINVAL;
   if (!R) return PYG_OK;
   k_unpack<<<(R + 255) / 256, 256, 0, c->stream>>>(d_rows, R, mc, s16, d_req, d_group, d_staged);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_shard_unpack_peer_dev(pyg_ctx* c, const int64_t* d_rows_of, int32_t world,
+                              const int64_t* d_req_off, int32_t R, int32_t mc, int32_t s16,
+                              pyg_reservation* d_req, int32_t* d_group, int32_t* d_staged) {
+  if (!c || R < 0 || mc < 0 || world < 1) return PYG_EINVAL;
+  if (!R) return PYG_OK;
+  k_unpack_peer<<<(R + 255) / 256, 256, 0, c->stream>>>(d_rows_of, world, d_req_off, R, mc, s16,
+                                                        d_req, d_group, d_staged);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_shard_signal_dev(pyg_ctx* c, const int64_t* d_flag_of, int32_t world, int32_t me,
+                         int64_t seq) {
+  if (!c || world < 1 || world > 1024 || me < 0 || me >= world) return PYG_EINVAL;
+  k_signal<<<1, 32 * ((world + 31) / 32), 0, c->stream>>>(d_flag_of, world, me, seq);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_shard_wait_dev(pyg_ctx* c, const int64_t* d_flags, int32_t world, int64_t seq) {
+  if (!c || world < 1 || world > 1024) return PYG_EINVAL;
+  k_wait<<<1, 32 * ((world + 31) / 32), 0, c->stream>>>(d_flags, world, seq, c->hd.error);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

@@ -33,6 +33,7 @@ libpyg_b200.so.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -209,6 +210,21 @@ class ShardedStep:
         self.row_words = 5 + ((mc + 1) // 2 if self.s16 else mc)
         self.rows = z(max(R, 1), self.row_words, dt=i32)
         self.g_res = z(max(Rt, 1), 4)
+        # NVLink exchange of the route rows (no NCCL on the step's path): double-buffered
+        # row buffers and a flag array [2 phases][world] per shard, mapped into every peer
+        W = plan.world
+        self.p2p = (W > 1 and dist.is_initialized() and dist.get_backend() == "nccl"
+                    and os.environ.get("PYG_SHARD_NCCL", "0") != "1")
+        self.seq = 0
+        if self.p2p:
+            self.rows_buf = [self.rows, z(max(R, 1), self.row_words, dt=i32)]
+            self.flags = z(2 * W)
+            wins2 = exchange_windows([t.data_ptr() for t in self.rows_buf + [self.flags]],
+                                     export, import_)
+            self.rows_of = [torch.tensor([wins2[k][b] for k in range(W)], dtype=i64,
+                                         device=device) for b in (0, 1)]
+            self.flag_of = [torch.tensor([wins2[k][2] + 8 * W * ph for k in range(W)],
+                                         dtype=i64, device=device) for ph in (0, 1)]
         self.g_group = z(max(Rt, 1), dt=i32)
         self.g_staged = z(max(Rt, 1), mc, dt=i32)
 
@@ -260,12 +276,27 @@ class ShardedStep:
         # 3: all-gather compact route rows (also the barrier that frees last step's shared
         # buffers); every rank unpacks the whole burst's reservations, groups, staged rows
         mc = max(nodes.max_cand, 1)
-        check(lib.pyg_shard_pack_dev(ctx.h, _ptr(b.res), _ptr(b.group), _ptr(self.staged),
-                                     plan.R_local, mc, self.s16, _ptr(self.rows)))
-        g_rows = (allgather_var(self.rows[:plan.R_local], self.req_counts)
-                  if dist.is_initialized() else self.rows[:plan.R_local])
-        check(lib.pyg_shard_unpack_dev(ctx.h, _ptr(g_rows), plan.R_total, mc, self.s16,
-                                       _ptr(self.g_res), _ptr(self.g_group), _ptr(self.g_staged)))
+        self.seq += 1
+        if self.p2p:
+            # pack into this step's row buffer, signal the peers, wait for all of them (every
+            # shard has then finished the previous step), unpack their rows over NVLink
+            par = self.seq % 2
+            check(lib.pyg_shard_pack_dev(ctx.h, _ptr(b.res), _ptr(b.group), _ptr(self.staged),
+                                         plan.R_local, mc, self.s16, _ptr(self.rows_buf[par])))
+            check(lib.pyg_shard_signal_dev(ctx.h, _ptr(self.flag_of[0]), W, plan.rank, self.seq))
+            check(lib.pyg_shard_wait_dev(ctx.h, _ptr(self.flags), W, self.seq))
+            check(lib.pyg_shard_unpack_peer_dev(ctx.h, _ptr(self.rows_of[par]), W,
+                                                _ptr(self.req_off_d), plan.R_total, mc, self.s16,
+                                                _ptr(self.g_res), _ptr(self.g_group),
+                                                _ptr(self.g_staged)))
+        else:
+            check(lib.pyg_shard_pack_dev(ctx.h, _ptr(b.res), _ptr(b.group), _ptr(self.staged),
+                                         plan.R_local, mc, self.s16, _ptr(self.rows)))
+            g_rows = (allgather_var(self.rows[:plan.R_local], self.req_counts)
+                      if dist.is_initialized() else self.rows[:plan.R_local])
+            check(lib.pyg_shard_unpack_dev(ctx.h, _ptr(g_rows), plan.R_total, mc, self.s16,
+                                           _ptr(self.g_res), _ptr(self.g_group),
+                                           _ptr(self.g_staged)))
         g_res, g_group, g_staged = self.g_res, self.g_group, self.g_staged
         if after_gather is not None:
             after_gather()
@@ -302,7 +333,11 @@ class ShardedStep:
                                       _ptr(self.counts)))
         mark("admit")
         # 7: every shard applies every shard's L3 erasures and L2-directory clears
-        barrier_on_stream(self.dev)
+        if self.p2p:
+            check(lib.pyg_shard_signal_dev(ctx.h, _ptr(self.flag_of[1]), W, plan.rank, self.seq))
+            check(lib.pyg_shard_wait_dev(ctx.h, _ptr(self.flags[W:]), W, self.seq))
+        else:
+            barrier_on_stream(self.dev)
         check(lib.pyg_shard_apply_lists_dev(ctx.h, _ptr(self.peers), W, plan.rank))
         mark("l2l3_lists")
         # 8: release on the owner; results of my requests from their owners
