@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libpyg_b200.so")
+# PYG_SO: experiments only (A/B of two builds on one box)
+SO_PATH = os.environ.get("PYG_SO") or os.path.join(HERE, "libpyg_b200.so")
 
 if not os.path.exists(SO_PATH):
     raise ImportError(f"{SO_PATH} is not built; run paper_2604_25899_b200/build.py "
