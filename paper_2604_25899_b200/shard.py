@@ -8,8 +8,11 @@ the burst (global issue order = rank order, then index).  One step:
   1. K1  hash the local requests                        (local)
   2. K2  staged row of every local request against ALL its candidates, through the
          replicated L2 directory (one walk per request)  (local)
-  3. NCCL all-gather of compact per-request route rows (tokens(), alpha, group, 16-bit
-         staged row: 52 B at 16 candidates) -> every rank holds the whole burst's K3 inputs
+  3. exchange of compact per-request route rows (tokens(), alpha, group, 16-bit staged
+         row: 52 B at 16 candidates): each rank packs its rows into a double-buffered
+         window, signals every peer through a flag array in peer memory, waits for all
+         of them and reads their rows in place over NVLink -> every rank holds the whole
+         burst's K3 inputs (PYG_SHARD_NCCL=1: NCCL all-gather instead)
   4. K3  sequential-commit route of the whole burst over the global node table,
          identically on every rank (engine.cpp:650-692 order; decisions bit-equal)
   5. the owner of each target replica PULLS the placed requests' tokens and boundary
@@ -18,7 +21,7 @@ the burst (global issue order = rank order, then index).  One step:
   6. K4/K5 admission on the owner, per replica in global placement order
          (engine.cpp:799-829); it exports the L2 blocks it erases and the L3 chain
          hashes it promotes
-  7. one NCCL stream barrier, then every rank reads every peer's lists in place:
+  7. a second flag barrier, then every rank reads every peer's lists in place:
          clears the directory bits and erases the union from its replica of the
          shared L3 (erasures commute)
   8. release (unpin) on the owner; each origin reads its requests' admission results
