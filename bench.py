@@ -481,9 +481,12 @@ def run_ours(args):
                                dn.cand))
 
         def run_step(b, k, after_gather):
-            # K1 already ran on the pipeline's prep stream
+            # K1 already ran on the pipeline's prep stream; the next step's assembly + K1
+            # may start with this step (its input set was last read by the previous step)
+            if args.k1_after == "start":
+                after_gather()
             PB.staged_matrix(ctx, b, dn, out)
-            after_gather()
+            after_gather()  # no-op when already called
             PB.route_batch(ctx, b, dn, out, mode)
             PB.admit_batch(ctx, b, out, now[0] + k, True)
             PB.release_batch(ctx, b, out)

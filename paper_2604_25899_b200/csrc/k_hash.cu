@@ -189,8 +189,26 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
 
   auto issue = [&](int c) {
     unsigned char* st = wbuf + (c & 1) * kStageBytes;
+#ifdef PYG_K1_SHFL_LOADER
     const int64_t pos = static_cast<int64_t>(c) * kChunk + q;
+#endif
+    if (!kGather) {
+      // CSR path: each lane publishes its own request's packed chunk source; the loader
+      // below is then shared with the fused path (8 broadcast LDS.128 per half-warp
+      // instead of 64 shuffles per chunk)
+      const int64_t left = n - static_cast<int64_t>(c) * kChunk;
+      const unsigned long long v = left <= 0 ? 0ull : left >= kChunk ? kChunk : left;
+      __syncwarp();
+      lsl[(c & 3) * 32 + me] =
+          (reinterpret_cast<unsigned long long>(tokens + s + static_cast<int64_t>(c) * kChunk) &
+           kPtrMask) | (v << kVShift);
+      __syncwarp();
+    }
+#ifndef PYG_K1_SHFL_LOADER
+    {
+#else
     if (kGather) {
+#endif
       const unsigned long long* slot = lsl + (c & 3) * 32 + sub * 16;
       unsigned long long e[16];
 #pragma unroll
@@ -205,12 +223,16 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
           cp_async8(st + (2 * t + sub) * kRowBytes + q * 8,
                     reinterpret_cast<const uint64_t*>(e[t] & kPtrMask) + q, 8);
       }
-      unsigned long long* nxt = lsl + ((c + 2) & 3) * 32 + me;
-      if (c + 2 < nch)
-        cp_async8(nxt, csrc + c + 2, 8);
-      else
-        *nxt = 0ull;
-    } else {
+      if (kGather) {
+        unsigned long long* nxt = lsl + ((c + 2) & 3) * 32 + me;
+        if (c + 2 < nch)
+          cp_async8(nxt, csrc + c + 2, 8);
+        else
+          *nxt = 0ull;
+      }
+    }
+#ifdef PYG_K1_SHFL_LOADER
+    else {
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
         const int jj = j + sub;
@@ -219,6 +241,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
         if (pos < nj) cp_async8(st + jj * kRowBytes + q * 8, tokens + sj + pos, 8);
       }
     }
+#endif
     cp_commit();
   };
   // fused assembly: write staged chunk c of the warp's 32 requests to the token CSR

@@ -1,6 +1,6 @@
 # A/B of two builds on one box: PYG_SO=libpyg_old.so (experiments) vs the in-tree build
-timeout 900 python -m pytest -x -q tests/test_gpu_parity.py tests/test_gpu_batch.py 2>&1 | tail -2
-for i in 1; do
+timeout 900 python -m pytest -x -q tests/test_gpu_batch.py tests/test_gpu_prompts.py 2>&1 | tail -2
+for i in 1 2; do
 for v in old new; do
   if [ $v = old ]; then export PYG_SO=/root/repo/libpyg_old.so; else unset PYG_SO; fi
   for f in -1 8; do
