@@ -139,11 +139,19 @@ __global__ void k_chunk_src(int R, const int64_t* __restrict__ seg_off,
 // block boundary always coincides with the end of a chunk: the emit decision
 // is per chunk and warp-uniform (no per-token test).  The last, partial chunk
 // and B % 16 != 0 take the generic per-token path.
+//
+// Long-prompt tail: the chain of one request is serial, ~119 cycles/token when its warp
+// has a scheduler to itself but ~2x that when it shares one.  The first iso_ctas CTAs
+// therefore run only 4 warps (one per scheduler), each on one of the longest tasks
+// (tasks are sorted longest-first; those whose longest prompt reaches iso_min_key * 4
+// tokens), and the persistent pool starts after them.  Config 2 (prompts < 2,700
+// tokens) never qualifies; config 4's 32k-token prompts do.
 template <bool kGather>
 __global__ void __launch_bounds__(kWarps * 32, 2)
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
-              uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task, GatherSrc g) {
+              uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task, GatherSrc g,
+              const uint16_t* __restrict__ sorted_keys, int iso_ctas, int iso_min_key) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbuf = smem + warp * 2 * kStageBytes;
@@ -152,11 +160,32 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
       smem + kWarps * 2 * kStageBytes + warp * kMetaBytes);
   unsigned long long* lsl = wbase + 32;
   const int ntasks = (R + 31) / 32;
+  // isolated long tasks: [0, n_long)
+  int n_long = 0;
+  if (iso_ctas > 0 && sorted_keys) {
+    for (int b = 0; b < iso_ctas * 4; b += 32) {  // 32 candidate tasks per ballot
+      const int tt = b + lane;
+      const bool lng = tt < iso_ctas * 4 && tt < ntasks &&
+                       static_cast<int>(sorted_keys[static_cast<int64_t>(tt) * 32]) >= iso_min_key;
+      n_long += __popc(__ballot_sync(kFull, lng));
+    }
+  }
+  int iso_task = -1;
+  if (static_cast<int>(blockIdx.x) * 4 < n_long) {
+    if (warp >= 4) return;
+    iso_task = blockIdx.x * 4 + warp;
+    if (iso_task >= n_long) return;
+  }
   // persistent: each warp pulls 32-request tasks, longest first, until none are left
-  for (;;) {
+  for (int it = 0;; ++it) {
   int task = 0;
-  if (lane == 0) task = atomicAdd(next_task, 1);
-  task = __shfl_sync(kFull, task, 0);
+  if (iso_task >= 0) {
+    if (it > 0) break;
+    task = iso_task;
+  } else {
+    if (lane == 0) task = n_long + atomicAdd(next_task, 1);
+    task = __shfl_sync(kFull, task, 0);
+  }
   if (task >= ntasks) break;
   const int idx = task * 32 + lane;
   const bool valid = idx < R;
@@ -391,8 +420,10 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   const int grid = std::min((tasks + kWarps - 1) / kWarps, cap);  // persistent: 1 CTA/SM
   auto* ctr = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
   PYG_CUDA(cudaMemsetAsync(ctr, 0, 4, c->stream));
+  // isolate the longest tasks (>= 8192-token prompts) on 16 SMs, one warp per scheduler
+  const int iso = grid >= 64 ? 16 : 0;
   k_hash_staged<kGather><<<grid, per_block, kSmemBytes, c->stream>>>(
-      d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr, g);
+      d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr, g, k_out, iso, 8192 / 4);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

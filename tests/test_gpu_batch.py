@@ -131,6 +131,34 @@ def test_hash_batch_all_lengths(B):
         assert np.array_equal(got[hoff[r]:hoff[r + 1]], want), (r, lens[r])
 
 
+@pytest.mark.parametrize("B", [16, 64])
+def test_hash_batch_long_prompts_isolated(B):
+    """K1's isolated long-task path: more than one task of prompts >= 8192 tokens (they run
+    one warp per scheduler on their own SMs) mixed with a persistent pool of short ones."""
+    from paper_2604_25899_b200 import Context
+    from paper_2604_25899_b200 import batch as PB
+    rng = np.random.default_rng(100 + B)
+    lens = np.concatenate([rng.integers(8192, 12000, 70), [8192, 8191, 16384],
+                           rng.integers(0, 3000, 2400)])
+    rng.shuffle(lens)
+    off = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    toks = rng.integers(0, 1 << 63, size=int(off[-1]), dtype=np.uint64)
+    ctx = Context(1, 1000, 1000, B)
+    z = np.zeros(len(lens), np.int32)
+    res = np.zeros(len(lens), PB.RES_DTYPE)
+    db = PB.upload_batch(ctx, toks, off, res, z, z, z)
+    PB.bind_current_stream(ctx)
+    PB.hash_batch(ctx, db)
+    torch.cuda.synchronize()
+    got = db.hashes.cpu().numpy().view(np.uint64)
+    hoff = db.hash_off.cpu().numpy()
+    o = Restated(B)
+    for r in range(len(lens)):
+        want = o.chain_hashes(toks[off[r]:off[r + 1]])
+        assert np.array_equal(got[hoff[r]:hoff[r + 1]], want), (r, lens[r])
+
+
 def test_batch_config4_bursty_shape():
     """Config 4 shape: lognormal prompt lengths up to 32k, 4 models interleaved over the
     replicas, 10% unprofiled (alpha 0) reservations."""
