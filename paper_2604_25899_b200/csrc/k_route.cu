@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
   __shared__ int32_t s_rid[kMaxSeqCand];
   __shared__ int32_t s_node[kMaxSeqCand];
   __shared__ int32_t s_cnt[kMaxSeqCand];
+  __shared__ int32_t s_stg[kMaxSeqCand];  // staged row of the evaluated request (nc > 32)
   const int g = blockIdx.x;
   const int lane = threadIdx.x;
   const int c0 = A.cand_off[g], nc = min(A.cand_off[g + 1] - c0, kMaxSeqCand);
@@ -415,7 +416,28 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
         pre_r = nx;
         if (nx != INT32_MAX && lane < nc) pre_v = A.staged[static_cast<int64_t>(nx) * A.max_cand + lane];
       }
+      if (nc > 32) {
+        // wide groups: the whole staged row into shared memory with 8 independent loads
+        // in flight per lane, instead of one dependent L2 round trip per candidate
+        const int32_t* row = A.staged + static_cast<int64_t>(first) * A.max_cand;
+        __syncwarp();  // the previous evaluation's readers of s_stg are done
+        for (int jb = 0; jb < nc; jb += 256) {
+          int32_t v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j = jb + lane + 32 * i;
+            v[i] = j < nc ? row[j] : 0;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j = jb + lane + 32 * i;
+            if (j < nc) s_stg[j] = v[i];
+          }
+        }
+        __syncwarp();
+      }
       auto staged_of = [&](int j) -> int32_t {
+        if (nc > 32) return s_stg[j];
         return j == lane ? own_v : A.staged[static_cast<int64_t>(first) * A.max_cand + j];
       };
       // full sched::route over the group's candidates (router.cpp:24-43): the
