@@ -2,13 +2,16 @@
 //
 // FNV-1a is a serial chain per request, so parallelism comes from requests:
 // one lane owns one request.  To keep HBM reads coalesced, each warp stages
-// its 32 requests' tokens through shared memory in 16-token chunks with 16-byte
-// cp.async copies (8 lanes x 16 B = one request's chunk, 4 requests per warp
-// instruction), double-buffered, and each lane then hashes its own row with
-// conflict-free LDS.128 (row stride 144 B: lanes i and i+8 share a bank group,
-// 4 wavefronts per 512 B = the minimum).  Requests are processed in descending
-// length order (a 16-bit radix sort on ceil(len/4)) so lanes of a warp carry
-// equal work and the longest chains start first.
+// its 32 requests' tokens through shared memory in 16-token chunks: every lane
+// publishes its request's chunk source (pointer | valid tokens, 8 B) in a smem
+// slot, each half-warp reads the 16 slots of its requests with 8 broadcast
+// LDS.128 and copies one request's 128-byte chunk per instruction with 8-byte
+// cp.async (16 lanes x 8 B, 2 requests per warp instruction), double-buffered;
+// each lane then hashes its own row with conflict-free LDS.128 (row stride
+// 144 B).  Requests are processed in descending length order (a 16-bit radix
+// sort on ceil(len/4)) so lanes of a warp carry equal work and the longest
+// chains start first.  The same loader serves prompt assembly fused with K1
+// (kGather): chunk sources then come from a precomputed table over the pool.
 //
 // Occupancy: ONE 8-warp CTA per SM (2 warps per scheduler), registers capped at 128
 // (no spills) so that while K1 hashes the NEXT burst on a second stream, the current
@@ -218,9 +221,6 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
 
   auto issue = [&](int c) {
     unsigned char* st = wbuf + (c & 1) * kStageBytes;
-#ifdef PYG_K1_SHFL_LOADER
-    const int64_t pos = static_cast<int64_t>(c) * kChunk + q;
-#endif
     if (!kGather) {
       // CSR path: each lane publishes its own request's packed chunk source; the loader
       // below is then shared with the fused path (8 broadcast LDS.128 per half-warp
@@ -233,11 +233,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
            kPtrMask) | (v << kVShift);
       __syncwarp();
     }
-#ifndef PYG_K1_SHFL_LOADER
     {
-#else
-    if (kGather) {
-#endif
       const unsigned long long* slot = lsl + (c & 3) * 32 + sub * 16;
       unsigned long long e[16];
 #pragma unroll
@@ -260,17 +256,6 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
           *nxt = 0ull;
       }
     }
-#ifdef PYG_K1_SHFL_LOADER
-    else {
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const int jj = j + sub;
-        const int64_t sj = __shfl_sync(kFull, s, jj);
-        const int64_t nj = __shfl_sync(kFull, n, jj);
-        if (pos < nj) cp_async8(st + jj * kRowBytes + q * 8, tokens + sj + pos, 8);
-      }
-    }
-#endif
     cp_commit();
   };
   // fused assembly: write staged chunk c of the warp's 32 requests to the token CSR
