@@ -278,7 +278,10 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
   __shared__ int32_t s_rid[kMaxSeqCand];
   __shared__ int32_t s_node[kMaxSeqCand];
   __shared__ int32_t s_cnt[kMaxSeqCand];
-  __shared__ int32_t s_stg[kMaxSeqCand];  // staged row of the evaluated request (nc > 32)
+  // wide groups (nc > 32): staged rows of the evaluated request and of the next one,
+  // prefetched with cp.async one evaluation ahead
+  __shared__ int32_t s_stg[2][kMaxSeqCand];
+  int wide_buf = 0, wide_pre = -1;
   const int g = blockIdx.x;
   const int lane = threadIdx.x;
   const int c0 = A.cand_off[g], nc = min(A.cand_off[g + 1] - c0, kMaxSeqCand);
@@ -401,43 +404,60 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
       // the staged row is read where it is needed (one L2 line per evaluated request);
       // staging every visited chunk's rows in shared memory cost more than it saved once
       // groups interleave (probe: tools/route_probe.py)
-      const int32_t own_v = (first == pre_r)
-                                ? pre_v
-                                : (lane < nc ? A.staged[static_cast<int64_t>(first) * A.max_cand + lane] : 0);
-      {  // load the next request of this group in the chunk now: its evaluation (usually the
-         // next one) then finds its staged value in a register instead of waiting on L2
-        int nx = INT32_MAX;
+      int32_t own_v = 0;
+      int nx = INT32_MAX;  // the next request of this group in the chunk
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int r = base + lane * kPer + u;
-          if (mine[u] && r > first) nx = min(nx, r);
-        }
-        nx = __reduce_min_sync(kFull, nx);
+      for (int u = 0; u < kPer; ++u) {
+        const int r = base + lane * kPer + u;
+        if (mine[u] && r > first) nx = min(nx, r);
+      }
+      nx = __reduce_min_sync(kFull, nx);
+      if (nc <= 32) {
+        // load the next request's value now: its evaluation (usually the next one) then
+        // finds its staged value in a register instead of waiting on L2
+        own_v = (first == pre_r)
+                    ? pre_v
+                    : (lane < nc ? A.staged[static_cast<int64_t>(first) * A.max_cand + lane] : 0);
         pre_r = nx;
         if (nx != INT32_MAX && lane < nc) pre_v = A.staged[static_cast<int64_t>(nx) * A.max_cand + lane];
-      }
-      if (nc > 32) {
-        // wide groups: the whole staged row into shared memory with 8 independent loads
-        // in flight per lane, instead of one dependent L2 round trip per candidate
-        const int32_t* row = A.staged + static_cast<int64_t>(first) * A.max_cand;
-        __syncwarp();  // the previous evaluation's readers of s_stg are done
-        for (int jb = 0; jb < nc; jb += 256) {
-          int32_t v[8];
+      } else {
+        // wide groups: the row was prefetched into s_stg[wide_buf] if `first` is the
+        // request predicted last time, else it is loaded now (8 loads in flight per lane)
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncwarp();
+        if (first != wide_pre) {
+          const int32_t* row = A.staged + static_cast<int64_t>(first) * A.max_cand;
+          for (int jb = 0; jb < nc; jb += 256) {
+            int32_t v[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j = jb + lane + 32 * i;
-            v[i] = j < nc ? row[j] : 0;
-          }
+            for (int i = 0; i < 8; ++i) {
+              const int j = jb + lane + 32 * i;
+              v[i] = j < nc ? row[j] : 0;
+            }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j = jb + lane + 32 * i;
-            if (j < nc) s_stg[j] = v[i];
+            for (int i = 0; i < 8; ++i) {
+              const int j = jb + lane + 32 * i;
+              if (j < nc) s_stg[wide_buf][j] = v[i];
+            }
           }
         }
         __syncwarp();
+        // prefetch the next request's row into the other buffer (read one evaluation ago)
+        wide_pre = nx;
+        if (nx != INT32_MAX) {
+          const int32_t* row = A.staged + static_cast<int64_t>(nx) * A.max_cand;
+          int32_t* dst = s_stg[wide_buf ^ 1];
+          for (int j = lane; j < nc; j += 32) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + j));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(row + j));
+          }
+          asm volatile("cp.async.commit_group;\n" ::);
+        }
       }
+      const int32_t* stg = s_stg[wide_buf];
+      if (nc > 32) wide_buf ^= 1;  // the prefetched row becomes current next time
       auto staged_of = [&](int j) -> int32_t {
-        if (nc > 32) return s_stg[j];
+        if (nc > 32) return stg[j];
         return j == lane ? own_v : A.staged[static_cast<int64_t>(first) * A.max_cand + j];
       };
       // full sched::route over the group's candidates (router.cpp:24-43): the
@@ -445,9 +465,15 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
       // input order == argmax of (h, s, -id, -pos); tiebreak <=> first position with
       // headroom H precedes the first with (H, S)
       RouteAcc best{0, 0, 0, -1};
+      // classes 0 / 1: headroom order is free-capacity order (tt is fixed per request),
+      // so the winners are the bound-feasible nodes whose free capacity equals F0 / Fa
+      // (the class maxima refresh() keeps); only that tie set is scanned for staged / id.
+      // "Other" alphas need bound_loop per node: full scan.
+      const bool by_max = cl < 2;
+      const int64_t F = cl == 0 ? F0 : Fa;
       for (int j = lane; j < nc; j += 32) {
         const int64_t fr = s_free[j];
-        if (tt > fr) continue;
+        if (by_max ? (fr != F || tt > fr) : tt > fr) continue;
         if (bound_of(j, cl, a) > A.eps) continue;
         RouteAcc x{fr - tt, staged_of(j), s_rid[j], j};
         if (acc_better(x, best)) best = x;
