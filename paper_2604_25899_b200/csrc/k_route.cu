@@ -405,11 +405,16 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
       // staging every visited chunk's rows in shared memory cost more than it saved once
       // groups interleave (probe: tools/route_probe.py)
       int32_t own_v = 0;
-      int nx = INT32_MAX;  // the next request of this group in the chunk
+      // the next request of this group in the chunk (narrow groups) / the next one that
+      // could fit under the current state (wide groups: a mispredicted row costs a full
+      // L2 round trip there)
+      int nx = INT32_MAX;
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         const int r = base + lane * kPer + u;
-        if (mine[u] && r > first) nx = min(nx, r);
+        if (!mine[u] || r <= first) continue;
+        const int cls = cl4[u];
+        if (nc <= 32 || (cls == 0 ? t[u] <= F0 : (cls == 1 ? t[u] <= Fa : true))) nx = min(nx, r);
       }
       nx = __reduce_min_sync(kFull, nx);
       if (nc <= 32) {
