@@ -10,3 +10,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_|Radix|Sca
 echo "launches rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:k_hash_staged -s 3 -c 1 -o gpurun_out/final_k1 $CMD > gpurun_out/ncu_k1.log 2>&1
 echo "k1 ncu rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:k_route_seq -s 3 -c 1 -o gpurun_out/final_k3 $CMD > gpurun_out/ncu_k3.log 2>&1
+echo "k3 ncu rc=$?"
