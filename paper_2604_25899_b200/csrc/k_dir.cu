@@ -3,7 +3,8 @@
 //   k_dir_export   alive L2 blocks of this ctx -> DirRecord list (a shard's share)
 //   k_dir_build    DirRecords of every shard -> main / rver / rlen tables
 //   k_group_pos    candidate groups -> replica bitmask + replica -> column map
-//   k_staged_dir   one thread per request: ONE walk of its boundary hashes
+//   k_staged_dir   one thread per request (one warp per request for walks of
+//                  >= 128 boundaries): ONE walk of its boundary hashes
 //                  yields matched_prefix on the L2 of every candidate replica
 //                  (node_view, engine.cpp:640-648; TierStore::matched_prefix,
 //                  hierarchy.cpp:84-104)
@@ -14,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ctx.cuh"
@@ -178,10 +180,93 @@ __device__ __forceinline__ void emit_drop(const StagedDirArgs& A, int64_t m, int
   (void)pos_g;
 }
 
+// Long walks (>= min_nh boundary hashes): one warp per request.  The probes of a
+// walk are independent loads, so lane l probes boundary d0 + l and the warp
+// prefix-ANDs the presence masks: replica n drops at the first boundary it
+// misses, exactly where the per-thread walk below would drop it, and every
+// lane emits the drops (aligned match + ragged extension) of its own boundary.
+// One probe latency per 32 boundaries instead of one per boundary.
 template <int W>
-__global__ void __launch_bounds__(128) k_staged_dir(StagedDirArgs A) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void staged_walk_warp(const StagedDirArgs& A, int r) {
+  const int lane = threadIdx.x & 31;
+  const int g = A.group[r];
+  const int nc = A.cand_off[g + 1] - A.cand_off[g];
+  int32_t* row = A.staged + static_cast<int64_t>(r) * A.max_cand;
+  for (int j = nc + lane; j < A.max_cand; j += 32) row[j] = 0;
+  uint64_t alive[W];
+  load_mask<W>(A.gmask + static_cast<int64_t>(g) * W, alive);
+  const int32_t* posrow = A.pos + static_cast<int64_t>(g) * A.d.n_global;
+  const int64_t L = A.tok_off[r + 1] - A.tok_off[r];
+  const uint64_t* tok = A.tokens + A.tok_off[r];
+  const uint64_t* hs = A.hashes + A.hash_off[r];
+  const int64_t nh = A.hash_off[r + 1] - A.hash_off[r];
+  const int B = A.c.B;
+  for (int64_t d0 = 0; d0 < nh; d0 += 32) {
+    uint64_t any_alive = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) any_alive |= alive[w];
+    if (!any_alive) break;  // warp-uniform: every lane holds the same alive mask
+    const int64_t d = d0 + lane;
+    // slot of this lane's boundary; -1 = absent (present nowhere), -2 = past the
+    // last boundary (nobody drops there)
+    const int64_t sl =
+        d < nh ? dir_slot_find(A.d.main, A.d.main_mask, A.d.stride, dir_key(hs[d])) : -2;
+    const uint64_t* pm = A.d.main + (sl >= 0 ? sl : 0) * A.d.stride + 1;
+    uint64_t drop[W];
+    bool any_drop = false;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {  // one mask word at a time keeps W = 16 in registers
+      uint64_t acc = sl >= 0 ? pm[w] : (sl == -1 ? 0ULL : ~0ULL);
+      uint64_t dr = alive[w] & ~acc;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix-AND over the lanes
+        const uint64_t v = __shfl_up_sync(0xffffffffu, acc, off);
+        if (lane >= off) acc &= v;
+      }
+      const uint64_t before = __shfl_up_sync(0xffffffffu, acc, 1);
+      if (lane > 0) dr &= before;
+      drop[w] = dr;
+      any_drop |= dr != 0;
+      alive[w] &= __shfl_sync(0xffffffffu, acc, 31);
+    }
+    if (any_drop) emit_drop<W>(A, d * B, L, tok, hs, drop, nullptr, posrow, row);
+  }
+  // still matching after the last boundary: matched = L (lane w takes mask word w)
+  for (int w = lane; w < W; w += 32) {
+    uint64_t b = 0;
+#pragma unroll
+    for (int x = 0; x < W; ++x)
+      if (x == w) b = alive[x];
+    while (b) {
+      const int k = __ffsll(static_cast<long long>(b)) - 1;
+      b &= b - 1;
+      row[posrow[w * 64 + k]] = static_cast<int32_t>(L);
+    }
+  }
+}
+
+// Blocks [0, warp_blocks) take the long walks (launched first: they are the
+// kernel's tail): warp k finds the long requests among requests [32k, 32k+32)
+// by ballot and walks them one after the other; the rest of the grid walks the
+// short ones one thread per request.
+template <int W>
+__global__ void __launch_bounds__(128, W >= 8 ? 4 : 6) k_staged_dir(StagedDirArgs A, int min_nh, int warp_blocks) {
+  if (static_cast<int>(blockIdx.x) < warp_blocks) {
+    const int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+    if (r0 >= A.R) return;
+    const int me = r0 + (threadIdx.x & 31);
+    const bool is_long = me < A.R && A.hash_off[me + 1] - A.hash_off[me] >= min_nh;
+    unsigned todo = __ballot_sync(0xffffffffu, is_long);
+    while (todo) {
+      const int k = __ffs(todo) - 1;
+      todo &= todo - 1;
+      staged_walk_warp<W>(A, r0 + k);
+    }
+    return;
+  }
+  const int r = (blockIdx.x - warp_blocks) * blockDim.x + threadIdx.x;
   if (r >= A.R) return;
+  if (A.hash_off[r + 1] - A.hash_off[r] >= min_nh) return;  // a warp walks it
   const int g = A.group[r];
   const int nc = A.cand_off[g + 1] - A.cand_off[g];
   int32_t* row = A.staged + static_cast<int64_t>(r) * A.max_cand;
@@ -410,13 +495,18 @@ int pyg_staged_matrix_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d
   }
   StagedDirArgs a{c->hd, d, d_tokens, d_tok_off, d_hash_off, d_hashes, R, d_group,
                   d_cand_off, gmask, pos, max_cand, d_staged};
-  const unsigned grid = (R + 127) / 128;
+  // walks of >= min_nh boundaries go to a warp each (PYG_K2_WARP_MIN overrides;
+  // a huge value keeps every walk on one thread)
+  int min_nh = 128;
+  if (const char* e = getenv("PYG_K2_WARP_MIN")) min_nh = std::max(0, atoi(e));
+  const int warp_blocks = min_nh >= (1 << 30) ? 0 : (R + 127) / 128;
+  const unsigned grid = warp_blocks + (R + 127) / 128;
   switch (d.W) {
-    case 1: k_staged_dir<1><<<grid, 128, 0, c->stream>>>(a); break;
-    case 2: k_staged_dir<2><<<grid, 128, 0, c->stream>>>(a); break;
-    case 4: k_staged_dir<4><<<grid, 128, 0, c->stream>>>(a); break;
-    case 8: k_staged_dir<8><<<grid, 128, 0, c->stream>>>(a); break;
-    default: k_staged_dir<16><<<grid, 128, 0, c->stream>>>(a); break;
+    case 1: k_staged_dir<1><<<grid, 128, 0, c->stream>>>(a, min_nh, warp_blocks); break;
+    case 2: k_staged_dir<2><<<grid, 128, 0, c->stream>>>(a, min_nh, warp_blocks); break;
+    case 4: k_staged_dir<4><<<grid, 128, 0, c->stream>>>(a, min_nh, warp_blocks); break;
+    case 8: k_staged_dir<8><<<grid, 128, 0, c->stream>>>(a, min_nh, warp_blocks); break;
+    default: k_staged_dir<16><<<grid, 128, 0, c->stream>>>(a, min_nh, warp_blocks); break;
   }
   PYG_LAUNCHED(c);
   return PYG_OK;

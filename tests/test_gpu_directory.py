@@ -3,7 +3,9 @@ every (request, candidate replica) pair must equal TierStore::matched_prefix on 
 replica's L2 (hierarchy.cpp:84-104) as the oracle computes it.  Stress: many
 replicas (1..4 mask words), shared prefixes with ragged tails, direct orphan puts
 (short and > 63 tokens), erasures and re-puts between calls (stale directory),
-zero-length prompts."""
+zero-length prompts; walks on one thread, on one warp (forced with
+PYG_K2_WARP_MIN=0) and mixed, with prompts up to ~100 blocks so a warp walk
+spans several 32-boundary rounds."""
 import numpy as np
 import pytest
 import torch
@@ -24,15 +26,19 @@ def _random_prompts(rng, n, base, B):
     return out
 
 
-@pytest.mark.parametrize("n_rep,B", [(5, 16), (70, 16), (200, 8), (33, 64)])
-def test_staged_matrix_directory(n_rep, B):
+@pytest.mark.parametrize("warp_min", [None, "0", "2000000000"])
+@pytest.mark.parametrize("n_rep,B,nb", [(5, 16, 12), (70, 16, 12), (200, 8, 12), (33, 64, 12),
+                                        (40, 16, 100), (300, 8, 60)])
+def test_staged_matrix_directory(n_rep, B, nb, warp_min, monkeypatch):
+    if warp_min is not None:
+        monkeypatch.setenv("PYG_K2_WARP_MIN", warp_min)
     from paper_2604_25899_b200 import Context
     from paper_2604_25899_b200 import batch as PB
     rng = np.random.default_rng(n_rep * 100 + B)
     o = Restated(B)
     caches = [o.new_cache(200_000, 200_000) for _ in range(n_rep)]
     ctx = Context(n_rep, [200_000] * n_rep, [200_000] * n_rep, B)
-    base = [rng.integers(1, 1 << 40, size=int(rng.integers(1, 12 * B)), dtype=np.uint64)
+    base = [rng.integers(1, 1 << 40, size=int(rng.integers(1, nb * B)), dtype=np.uint64)
             for _ in range(12)]
     # L2 contents: prefixes of shared bases with ragged ends
     for n in range(n_rep):
