@@ -50,21 +50,39 @@ __global__ void k_lookup_batch(CtxDev c, const uint64_t* __restrict__ tokens,
 }
 
 // ---------------------------------------------------------------- K4 + K5
-// First missing block of a chain in a tier, whole CTA (TierStore::matched_prefix
-// aligned walk, hierarchy.cpp:88-91).  sm: >= 64 int64.
-__device__ int64_t block_walk(const TierDev& t, const uint64_t* hashes, int64_t nh, int64_t* sm) {
-  for (int64_t base = 0; base < nh; base += blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const bool miss = i < nh && idx_find(t, hashes[i]) < 0;
+// First missing block of a chain (TierStore::matched_prefix aligned walk,
+// hierarchy.cpp:88-91) on L1, L2 and L3 at once, whole CTA (blockDim.x == 512,
+// sm: >= 64 int64): warps 0-3 probe L1, 4-7 L2, 8-11 L3, 128 boundaries per
+// tier per round, so the three walks of a placed request cost one probe latency
+// per round instead of three.
+__device__ void block_walk3(const TierDev& t0, const TierDev& t1, const TierDev& t2,
+                            const uint64_t* hashes, int64_t nh, int64_t* sm, int64_t (&kb)[3]) {
+  constexpr int S = 128;
+  const int tier = threadIdx.x / S;  // 3: idle warps
+  kb[0] = kb[1] = kb[2] = nh;
+  bool done[3] = {false, false, false};
+  for (int64_t base = 0; base < nh; base += S) {
+    const int64_t i = base + (threadIdx.x % S);
+    bool miss = false;
+    if (tier < 3 && !done[tier] && i < nh) {
+      const TierDev& t = tier == 0 ? t0 : tier == 1 ? t1 : t2;
+      miss = idx_find(t, hashes[i]) < 0;
+    }
     const unsigned m = __ballot_sync(kFull, miss);
-    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m ? base + (threadIdx.x & ~31) + __ffs(m) - 1 : INT64_MAX;
+    if ((threadIdx.x & 31) == 0)
+      sm[threadIdx.x >> 5] = m ? base + ((threadIdx.x % S) & ~31) + __ffs(m) - 1 : INT64_MAX;
     __syncthreads();
-    int64_t first = INT64_MAX;
-    for (int w = 0; w < (blockDim.x + 31) / 32; ++w) first = min(first, sm[w]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int64_t first = min(min(sm[4 * j], sm[4 * j + 1]), min(sm[4 * j + 2], sm[4 * j + 3]));
+      if (!done[j] && first != INT64_MAX) {
+        kb[j] = first;
+        done[j] = true;
+      }
+    }
     __syncthreads();
-    if (first != INT64_MAX) return first;
+    if (done[0] && done[1] && done[2]) break;
   }
-  return nh;
 }
 
 // Erase a present, unpinned block by key; safe under concurrent claims of the
@@ -144,14 +162,24 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     const uint64_t* tok = a.tokens + a.tok_off[r];
     const uint64_t* hs = a.hashes + a.hash_off[r];
     const int64_t nh = a.hash_off[r + 1] - a.hash_off[r];
+    // the three aligned walks in one CTA-wide pass, then the three ragged
+    // extensions at once, one warp's lane 0 per tier (each is a serial FNV run over <= 63 tokens)
     int64_t m[3];
-    for (int tier = 0; tier < 3; ++tier) {
-      const TierDev t = tier == 0 ? *t1p : tier == 1 ? *t2p : t3;
-      const int64_t kb = block_walk(t, hs, nh, sm);
-      const int64_t mm = kb ? matched_from_blocks(kb, L, c.B) : 0;
-      if (threadIdx.x == 0) bc[0] = ragged_extend(t, t.log, tok, L, hs, mm, c.B);
+    {
+      int64_t kb[3];
+      block_walk3(*t1p, *t2p, t3, hs, nh, sm, kb);
+      for (int tier = 0; tier < 3; ++tier) m[tier] = kb[tier] ? matched_from_blocks(kb[tier], L, c.B) : 0;
+    }
+    {
+      const int tier = threadIdx.x >> 5;
+      if (tier < 3 && (threadIdx.x & 31) == 0) {
+        const TierDev& t = tier == 0 ? *t1p : tier == 1 ? *t2p : t3;
+        bc[tier] = ragged_extend(t, t.log, tok, L, hs, m[tier], c.B);
+      }
       __syncthreads();
-      m[tier] = bc[0];
+      m[0] = bc[0];
+      m[1] = bc[1];
+      m[2] = bc[2];
       __syncthreads();
     }
     // evict_for_space(L1, needed): base = l1_occupancy() (manager.cpp:106)

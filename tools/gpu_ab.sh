@@ -1,5 +1,5 @@
 # A/B of two builds on one box: PYG_SO=libpyg_old.so (experiments) vs the in-tree build
-timeout 900 python -m pytest -x -q tests/test_gpu_batch.py tests/test_gpu_parity.py tests/test_gpu_directory.py 2>&1 | tail -2
+timeout 900 python -m pytest -x -q tests/test_gpu_batch.py tests/test_gpu_parity.py tests/test_gpu_directory.py tests/test_gpu_shard.py tests/test_gpu_prompts.py 2>&1 | tail -2
 for v in old new; do
   if [ $v = old ]; then export PYG_SO=/root/repo/libpyg_old.so; else unset PYG_SO; fi
   for w in "deep_research 125000 32" "bursty 125000 256" "bursty 125000 1024"; do
