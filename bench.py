@@ -756,12 +756,15 @@ def run_sharded(args, ws, rank, local, dev):
                 "placed_on_rank0_per_step": int(out["recv_count"].item()),
                 "l2_flush": "none needed: step inputs (tokens %.2f GB/GPU) exceed the 126 MB L2"
                             % (tr.n_tokens * 8 / 1e9),
-                "parallelism": (f"replica shards x{ws}: NCCL all-gather of route inputs; owner "
-                                f"GPUs pull placed requests' tokens/hashes and peers' L2/L3 "
-                                f"erase lists and results over NVLink P2P (CUDA IPC); one "
-                                f"NCCL stream barrier; no host sync in the step"),
+                "parallelism": (f"replica shards x{ws}: "
+                                + ("route rows exchanged over NVLink peer memory behind a flag "
+                                   "barrier (no NCCL in the step)" if st.p2p else
+                                   "NCCL all-gather of route inputs + one NCCL stream barrier")
+                                + "; owner GPUs pull placed requests' tokens/hashes and peers' "
+                                  "L2/L3 erase lists and results over NVLink P2P (CUDA IPC); "
+                                  "no host sync in the step"),
                 "k1_overlap": (f"K1 of step k+1 on a second stream (grid = SMs - {args.free_sms}) "
-                               "from step k's all-gather on") if overlap else "none (serial)"},
+                               "from step k's route-row exchange on") if overlap else "none (serial)"},
             "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1), rank 0",
                          "achieved": hash_gbs, "peak": peak, "unit": "GB/s",
                          "frac": hash_gbs / peak, "traffic": None, "peak_source": peak_src,
