@@ -92,6 +92,10 @@ int pyg_set_stream(pyg_ctx* ctx, void* cuda_stream);
 int pyg_synchronize(pyg_ctx* ctx);
 /* number of kernels this ctx has launched (for the bench's gpu_launches claim) */
 int64_t pyg_kernel_launches(pyg_ctx* ctx);
+/* Counters since creation / the last reset (synchronizes the ctx stream): out[0] blocks
+   evicted by evict_for_space, out[1] their tokens, out[2] evictions that had work
+   (excess > 0), out[3] of those unsatisfied. */
+int pyg_stats(pyg_ctx* ctx, int64_t* out, int32_t reset);
 /* (Re)sets a replica's tier capacities -- CacheHierarchy(l1_capacity, l2_capacity)
    (hierarchy.hpp:100) for a replica slot the engine provisions later (engine.cpp:197, 1482). */
 int pyg_set_capacity(pyg_ctx* ctx, int32_t replica, int64_t l1_capacity, int64_t l2_capacity);
@@ -257,24 +261,49 @@ int pyg_release_batch_dev(pyg_ctx* ctx, const int64_t* d_tok_off, const int64_t*
                           const uint64_t* d_hashes, int32_t n_req, const int32_t* d_placed_off,
                           const int32_t* d_placed, const int32_t* d_admitted);
 
+/* Node-table bookkeeping between bursts (the steady-state step): d_out holds, per replica,
+   the base reservations then the reservations d_req[d_placed[j]] of the requests a burst
+   placed there (d_placed_off/d_placed from pyg_route_batch_dev), in placement order -- the
+   pool order of reservation_of (engine.cpp:616-628, 686).  d_placed_off may be NULL (base
+   only).  d_out_off[n] = d_base_off[n] + d_placed_off[n]; d_out needs base + placed entries. */
+int pyg_nodes_compose_dev(pyg_ctx* ctx, int32_t n_rep, const int64_t* d_base_off,
+                          const pyg_reservation* d_base, const int32_t* d_placed_off,
+                          const int32_t* d_placed, const pyg_reservation* d_req,
+                          int64_t* d_out_off, pyg_reservation* d_out);
+/* FutureRegistry::update (manager.cpp:13-23) for n DISTINCT workflows at once (a burst's
+   issue-time updates, engine.cpp:605-609, last write per workflow); max_wf >= every id. */
+int pyg_registry_update_batch_dev(pyg_ctx* ctx, int32_t n, const int32_t* d_wf,
+                                  const uint64_t* d_mask, int32_t max_wf);
+
 /* ------------------------------------------------------ sharded step (multi-GPU) */
 /* With pyg_set_shard, pyg_route_batch_dev routes over the WHOLE cluster: the node table,
    candidate lists and placed CSR ([n_global+1]) use global replica indices, and every shard
    runs the same route over the all-gathered batch (bit-identical decisions everywhere).
    Admission then runs on the owner shard only, over a local batch of the requests placed on
-   its replicas (local replica indices).  pyg_admit_shard_dev is pyg_admit_batch_dev that
-   (a) exports the L2 blocks it erases (DirRecords, so other shards clear their directory
-   bits with pyg_dir_clear_dev) and (b) does NOT erase promoted L3 spans itself but lists
-   their chain hashes: the shared L3 (hierarchy.hpp:76-85) is replicated on every shard and
-   each shard applies the union with pyg_l3_erase_hashes_dev (erasures commute).
-   d_counts[0] = L2 records written, d_counts[1] = L3 hashes written. */
+   its replicas (local replica indices), in two calls:
+   pyg_admit_shard_dev = start_prefill except the L3 promotion: L1/L2 lookups, eviction, the
+   promoted L2 span erase (exported as DirRecords so other shards clear their directory bits
+   with pyg_dir_clear_dev / pyg_shard_apply_lists_dev), insert_chain.  d_counts[0] = L2
+   records written.
+   pyg_shard_l3_resolve_dev = the L3 part, in engine order (engine.cpp:742-746, 806,
+   826-828): admission p of this shard sees the live L3 as left by every admission before p.
+   The shared L3 (hierarchy.hpp:76-85) is replicated on every shard; call it once the L3
+   erase lists of every LOWER shard (lower global replicas = earlier admissions) have been
+   applied to this shard's replica (pyg_shard_apply_lists_range_dev).  It lists the chain
+   hashes this shard's admissions erase (d_counts[1]) instead of erasing them, writes the
+   L3 matches and clamps both counts to their caps (overflow sets device error 4). */
 int pyg_admit_shard_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
                         const int64_t* d_hash_off, const uint64_t* d_hashes,
                         const int32_t* d_wf, const int32_t* d_role, int32_t n_req,
                         const int32_t* d_placed_off, const int32_t* d_placed, double now,
                         int32_t speculative, int32_t* d_admitted, int64_t* d_match3,
-                        void* d_l2_erased, int64_t l2_cap, uint64_t* d_l3_hashes, int64_t l3_cap,
-                        int64_t* d_counts);
+                        void* d_l2_erased, int64_t l2_cap, int64_t* d_counts);
+int pyg_shard_l3_resolve_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                             const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t n_req,
+                             const int32_t* d_placed_off, const int32_t* d_placed,
+                             const int32_t* d_admitted, int64_t* d_match3,
+                             uint64_t* d_l3_hashes, int64_t l3_cap, int64_t l2_cap,
+                             int64_t* d_counts);
 /* n is an upper bound; d_count (device, optional) holds the actual count (no host sync) */
 int pyg_dir_clear_dev(pyg_ctx* ctx, const void* d_records, int64_t n, const int64_t* d_count);
 int pyg_l3_erase_hashes_dev(pyg_ctx* ctx, const uint64_t* d_hashes, int64_t n,
@@ -360,6 +389,10 @@ int pyg_shard_local_placed_dev(pyg_ctx* ctx, const int32_t* d_placed_off, const 
 /* After a cross-GPU barrier: erase every shard's listed L3 hashes from this shard's L3 replica
    and clear the other shards' erased L2 blocks from the directory. */
 int pyg_shard_apply_lists_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world, int32_t me);
+/* The same for a subset: L3 erase lists of peers [l3_lo, l3_hi), and (with_l2) the L2
+   directory clears of every peer except me. */
+int pyg_shard_apply_lists_range_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world,
+                                    int32_t me, int32_t l3_lo, int32_t l3_hi, int32_t with_l2);
 /* Admission results of this shard's own requests, read from their owner shards. */
 int pyg_shard_results_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world,
                           const int64_t* d_rep_off, const pyg_decision* d_dec, int64_t req_base,

@@ -23,6 +23,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 BLOCK_DTYPE = np.dtype([("id", "<u8"), ("hash", "<u8"), ("s", "<i8"), ("e", "<i8"),
                         ("wf", "<i4"), ("role", "<i4"), ("la", "<f8"), ("pin", "<i4"),
                         ("alive", "<i4")])
+DEC_DTYPE = np.dtype([("target", "<i4"), ("tiebreak", "<i4"), ("headroom", "<i8"),
+                      ("oom_bound", "<f8")])
 RES_DTYPE = np.dtype([("prompt_len", "<i8"), ("upper", "<i8"), ("alpha", "<f8"),
                       ("tokens_generated", "<i8")])
 
@@ -309,6 +311,9 @@ class Reference(_Backend):
         s("pref_erase_chain_span", None, vp, vp, i32, vp, i64, i64, i64)
         s("pref_step", i64, vp, i32, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
           vp, i32, dbl, dbl, i32, vp, vp)
+        s("pref_burst", i64, vp, i32, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp,
+          vp, vp, i32, dbl, dbl, i32, i32, vp, vp, vp, vp)
+        s("pref_release", None, vp, vp, vp, i32, vp, vp)
 
     def fnv1a_u64(self, v, h=1469598103934665603):
         return self.lib.pref_fnv1a_u64(v, h)
@@ -455,6 +460,49 @@ class Reference(_Backend):
                                _p(ao), _p(a), _p(co), _p(cd), mode, eps, now, int(release),
                                _p(dec) if want_out else None, _p(adm) if want_out else None)
         return n, dec[:R], adm[:R]
+
+    def burst(self, caches, l3, reg, speculative, tokens, tok_off, res, group, wf, role,
+              replica_id, kv_capacity, asg_off, asg, cand_off, cand, eps, now, hash_once=True,
+              threads=1, want_staged=False):
+        """pref_burst: one burst of the steady-state bench through the reference's calls
+        (node table given as a CSR; no release).  Returns (decisions, admitted, match3,
+        staged or None)."""
+        R = len(tok_off) - 1
+        arr = (C.c_void_p * len(caches))(*caches)
+        t = _u64(tokens)
+        off = np.ascontiguousarray(tok_off, np.int64)
+        rs = np.ascontiguousarray(res, RES_DTYPE)
+        g = np.ascontiguousarray(group, np.int32)
+        w = np.ascontiguousarray(wf, np.int32)
+        ro = np.ascontiguousarray(role, np.int32)
+        a = np.ascontiguousarray(asg, RES_DTYPE) if len(asg) else np.zeros(1, RES_DTYPE)
+        rid = np.ascontiguousarray(replica_id, np.int32)
+        kv = np.ascontiguousarray(kv_capacity, np.int64)
+        ao = np.ascontiguousarray(asg_off, np.int64)
+        co = np.ascontiguousarray(cand_off, np.int32)
+        cd = np.ascontiguousarray(cand, np.int32)
+        G = len(co) - 1
+        mc = max(1, int(np.max(np.diff(co))) if G else 1)
+        dec = np.zeros(max(R, 1), DEC_DTYPE)
+        adm = np.zeros(max(R, 1), np.int32)
+        m3 = np.zeros((max(R, 1), 3), np.int64)
+        st = np.zeros((max(R, 1), mc), np.int32) if want_staged else None
+        self.lib.pref_burst(C.cast(arr, C.c_void_p), len(caches), l3, reg, int(speculative),
+                            _p(t), _p(off), R, _p(rs), _p(g), _p(w), _p(ro), _p(rid), _p(kv),
+                            _p(ao), _p(a), _p(co), _p(cd), G, eps, now, int(bool(hash_once)),
+                            int(threads), _p(dec), _p(adm), _p(m3),
+                            _p(st) if st is not None else None)
+        return dec[:R], adm[:R], m3[:R], (st[:R] if st is not None else None)
+
+    def release(self, caches, tokens, tok_off, rep, admitted):
+        """pref_release: unpin_chain of an earlier burst's admitted requests."""
+        arr = (C.c_void_p * len(caches))(*caches)
+        t = _u64(tokens)
+        R = len(tok_off) - 1
+        self.lib.pref_release(C.cast(arr, C.c_void_p), _p(t),
+                              _p(np.ascontiguousarray(tok_off, np.int64)), R,
+                              _p(np.ascontiguousarray(rep, np.int32)),
+                              _p(np.ascontiguousarray(admitted, np.int32)))
 
     def future_mask(self, expr, history):
         m = C.c_uint64()

@@ -13,6 +13,8 @@
 // Lineage ints are turned into the strings "w<k>" / "r<k>"; FutureRegistry
 // masks into sets of those role names.
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -20,6 +22,7 @@
 #include <memory>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "pythia/cache/hierarchy.hpp"
@@ -354,7 +357,7 @@ void pref_erase_chain_span(void* c, void* l3, int32_t tier, const uint64_t* toke
 //   node_view per candidate: staged = cache.lookup(prompt, nullptr).l2   engine.cpp:640-648
 //   sched::route in issue order; SEQ_COMMIT pushes to the pool first     engine.cpp:650-692
 //   per replica, per placed request: start_prefill cache side            engine.cpp:799-829
-//     (L3 lookups against the L3 as of the start of admission)
+//     (one at a time against the live L3, as the engine's admit_on loop)
 //   release: unpin_chain(seq, len)                                        hierarchy.cpp:132-142
 // Returns the number of placed requests.
 int64_t pref_step(void** caches, int32_t n_rep, void* l3v, void* regv, int32_t spec,
@@ -405,14 +408,13 @@ int64_t pref_step(void** caches, int32_t n_rep, void* l3v, void* regv, int32_t s
       }
     }
   }
-  SharedL3 l3snap = *l3;
   std::vector<std::pair<int, int32_t>> admitted;
   for (int n = 0; n < n_rep; ++n) {
     auto* c = static_cast<CacheHierarchy*>(caches[n]);
     for (int32_t r : placed[n]) {
       workflow::TokenSeq seq(tokens + tok_off[r], tokens + tok_off[r + 1]);
       const int64_t len = static_cast<int64_t>(seq.size());
-      auto m = c->lookup(seq, &l3snap);
+      auto m = c->lookup(seq, l3);  // live L3, as start_prefill (engine.cpp:806)
       auto ev = cache::evict_for_space(*c, Tier::L1, len - m.l1, *reg, spec != 0);
       if (!ev.satisfied) continue;
       const int64_t reusable = std::max({m.l1, m.l2, m.l3});
@@ -433,6 +435,143 @@ int64_t pref_step(void** caches, int32_t n_rep, void* l3v, void* regv, int32_t s
     }
   }
   return n_placed;
+}
+
+// One burst of the steady-state bench (paper_2604_25899_b200/steady.py, bench.py): the
+// reference engine's hot-path calls for a burst of R requests, with
+//   - the node table given as a CSR (background load + earlier bursts' placements, pool
+//     order), routed in issue order with sequential commit (engine.cpp:650-692);
+//   - staged values: hash_once == 0 -> cache.lookup(prompt, nullptr).l2 per candidate, the
+//     engine's node_view (engine.cpp:640-648, one rehash per candidate); hash_once != 0 ->
+//     chain_boundary_hashes once + tier(L2).matched_prefix per candidate (hierarchy.hpp:44,
+//     64-65: the same reference functions without the repeated hashing).  Computed over
+//     n_threads host threads: nothing mutates L2 while a burst routes, so every order gives
+//     the same values;
+//   - admission per replica in placement order against the live L3 (engine.cpp:742-746,
+//     799-829);
+//   - no release: pref_release unpins an earlier burst.
+// out_m3 [3R] (optional) = the admission lookups; out_staged [R * max_cand] (optional).
+int64_t pref_burst(void** caches, int32_t n_rep, void* l3v, void* regv, int32_t spec,
+                   const uint64_t* tokens, const int64_t* tok_off, int32_t R, const pref_res* res,
+                   const int32_t* group, const int32_t* wf, const int32_t* role,
+                   const int32_t* replica_id, const int64_t* kv_cap, const int64_t* asg_off,
+                   const pref_res* asg, const int32_t* cand_off, const int32_t* cand,
+                   int32_t n_groups, double eps, double now, int32_t hash_once,
+                   int32_t n_threads, pref_decision* out_dec, int32_t* out_adm, int64_t* out_m3,
+                   int32_t* out_staged) {
+  auto* l3 = static_cast<SharedL3*>(l3v);
+  auto* reg = static_cast<cache::FutureRegistry*>(regv);
+  int32_t max_cand = 1;
+  for (int g = 0; g < n_groups; ++g) max_cand = std::max(max_cand, cand_off[g + 1] - cand_off[g]);
+  std::vector<int32_t> staged(static_cast<size_t>(R) * max_cand, 0);
+  auto stage = [&](int32_t lo, int32_t hi) {
+    for (int32_t r = lo; r < hi; ++r) {
+      workflow::TokenSeq prompt(tokens + tok_off[r], tokens + tok_off[r + 1]);
+      const int g = group[r];
+      if (g < 0 || g >= n_groups) continue;
+      std::vector<uint64_t> hs;
+      if (hash_once) hs = cache::chain_boundary_hashes(prompt);
+      for (int32_t j = cand_off[g]; j < cand_off[g + 1]; ++j) {
+        const auto* c = static_cast<const CacheHierarchy*>(caches[cand[j]]);
+        const int64_t v = hash_once ? c->tier(Tier::L2).matched_prefix(prompt, hs)
+                                    : c->lookup(prompt, nullptr).l2;
+        staged[static_cast<size_t>(r) * max_cand + (j - cand_off[g])] = static_cast<int32_t>(v);
+      }
+    }
+  };
+  const int nt = std::max(1, std::min<int32_t>(n_threads, std::max(1, R / 64)));
+  if (nt == 1) {
+    stage(0, R);
+  } else {
+    std::vector<std::thread> th;
+    std::atomic<int32_t> next{0};
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&] {
+        for (;;) {
+          const int32_t a = next.fetch_add(64);
+          if (a >= R) break;
+          stage(a, std::min(R, a + 64));
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  if (out_staged) std::memcpy(out_staged, staged.data(), staged.size() * sizeof(int32_t));
+  std::vector<std::vector<sched::Reservation>> pools(static_cast<size_t>(n_rep));
+  for (int n = 0; n < n_rep; ++n)
+    for (int64_t k = asg_off[n]; k < asg_off[n + 1]; ++k)
+      pools[n].push_back({asg[k].prompt_len, asg[k].upper, asg[k].alpha, asg[k].tokens_generated});
+  std::vector<std::vector<int32_t>> placed(static_cast<size_t>(n_rep));
+  int64_t n_placed = 0;
+  for (int32_t r = 0; r < R; ++r) {
+    const int g = group[r];
+    std::vector<sched::NodeView> views;
+    if (g >= 0 && g < n_groups) {
+      for (int32_t j = cand_off[g]; j < cand_off[g + 1]; ++j) {
+        const int n = cand[j];
+        sched::NodeView v;
+        v.replica_id = replica_id[n];
+        v.kv_capacity = kv_cap[n];
+        v.assigned = pools[n];
+        v.staged_l2_prefix = staged[static_cast<size_t>(r) * max_cand + (j - cand_off[g])];
+        views.push_back(std::move(v));
+      }
+    }
+    sched::Reservation q{res[r].prompt_len, res[r].upper, res[r].alpha, res[r].tokens_generated};
+    auto d = sched::route(views, q, eps);
+    pref_decision od{};
+    od.target = d.target ? *d.target : -1;
+    od.tiebreak = d.cache_tiebreak_used;
+    od.headroom = d.headroom;
+    od.oom_bound = d.oom_bound;
+    if (out_dec) out_dec[r] = od;
+    if (out_adm) out_adm[r] = 0;
+    if (out_m3) out_m3[3 * r] = out_m3[3 * r + 1] = out_m3[3 * r + 2] = 0;
+    if (d.target) {
+      for (int32_t j = cand_off[g]; j < cand_off[g + 1]; ++j) {
+        if (replica_id[cand[j]] == *d.target) {
+          pools[cand[j]].push_back(q);
+          placed[cand[j]].push_back(r);
+          ++n_placed;
+          break;
+        }
+      }
+    }
+  }
+  for (int n = 0; n < n_rep; ++n) {
+    auto* c = static_cast<CacheHierarchy*>(caches[n]);
+    for (int32_t r : placed[n]) {
+      workflow::TokenSeq seq(tokens + tok_off[r], tokens + tok_off[r + 1]);
+      const int64_t len = static_cast<int64_t>(seq.size());
+      auto m = c->lookup(seq, l3);
+      if (out_m3) {
+        out_m3[3 * r] = m.l1;
+        out_m3[3 * r + 1] = m.l2;
+        out_m3[3 * r + 2] = m.l3;
+      }
+      auto ev = cache::evict_for_space(*c, Tier::L1, len - m.l1, *reg, spec != 0);
+      if (!ev.satisfied) continue;
+      const int64_t reusable = std::max({m.l1, m.l2, m.l3});
+      const int64_t l2_part = std::max<int64_t>(std::min(reusable, m.l2) - m.l1, 0);
+      const int64_t l3_part = std::max<int64_t>(reusable - std::max(m.l1, m.l2), 0);
+      if (l2_part > 0) pref_erase_chain_span(c, nullptr, 1, seq.data(), len, m.l1, m.l1 + l2_part);
+      if (l3_part > 0)
+        pref_erase_chain_span(c, l3, 2, seq.data(), len, std::max(m.l1, m.l2), reusable);
+      c->insert_chain(Tier::L1, seq, len, {wf_name(wf[r]), role_name(role[r])}, now, +1);
+      if (out_adm) out_adm[r] = 1;
+    }
+  }
+  return n_placed;
+}
+
+// unpin_chain(seq, len) of every admitted request of an earlier burst on its replica
+// (hierarchy.cpp:132-142); rep[r] = replica index or -1.
+void pref_release(void** caches, const uint64_t* tokens, const int64_t* tok_off, int32_t R,
+                  const int32_t* rep, const int32_t* admitted) {
+  for (int32_t r = 0; r < R; ++r) {
+    if (rep[r] < 0 || !admitted[r]) continue;
+    workflow::TokenSeq seq(tokens + tok_off[r], tokens + tok_off[r + 1]);
+    static_cast<CacheHierarchy*>(caches[rep[r]])->unpin_chain(seq, static_cast<int64_t>(seq.size()));
+  }
 }
 
 // ---- path analysis over a flattened tree (preorder node arrays, the layout of

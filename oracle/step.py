@@ -7,8 +7,8 @@ pattern for a burst of requests (SURVEY.md CS-1 + CS-2):
   route(views, reservation_r, eps) for r in issue order          engine.cpp:650-692
       SEQ_COMMIT: the placement joins the target's pool before r+1
   per replica in order, per placed request in order: start_prefill cache side
-      (lookup(seq,&l3) with L3 as of the start of admission; promoted L3 spans
-       erased in the live L3 -- erasures commute)                 engine.cpp:799-829
+      (lookup(seq,&l3) against the live L3, promoted spans erased at once,
+       exactly the engine's one-at-a-time admission)              engine.cpp:799-829
   release: unpin_chain(seq, len) of admitted requests             hierarchy.cpp:132-142
 """
 import numpy as np
@@ -52,16 +52,16 @@ def oracle_step(o, caches, l3, reg, trace, cl, mode, eps, now, spec, release):
             if mode == SEQ_COMMIT:
                 pools[n].append(req)
     placed = [[r for r in range(R) if t_idx[r] == n] for n in range(cl.n_replicas)]
-    l3snap = o.clone_l3(l3)
     admitted = np.zeros(R, np.int32)
     match3 = np.zeros((R, 3), np.int64)
     for n in range(cl.n_replicas):
         for r in placed[n]:
-            ok, m = o.admit(caches[n], l3snap, l3, reg, spec, prompts[r], int(trace.wf[r]),
+            # the live L3: a later admission no longer sees the L3 spans an earlier one
+            # promoted (engine.cpp:806, 826-828; the engine admits one request at a time)
+            ok, m = o.admit(caches[n], l3, l3, reg, spec, prompts[r], int(trace.wf[r]),
                             int(trace.role[r]), now)
             admitted[r] = int(ok)
             match3[r] = m
-    o.free_l3(l3snap)
     if release:
         for n in range(cl.n_replicas):
             for r in placed[n]:
@@ -103,6 +103,13 @@ def apply_warm_oracle(o, caches, l3, reg, trace, ops):
             o.l3_dead_sweep(l3, w, mask)
         elif op[0] == "reg":
             o.reg_update(reg, op[1], op[2])
+        elif op[0] == "esp":
+            _, n, tier, r, frm, to = op
+            o.erase_chain_span(caches[n], None, tier, trace.prompt(r), frm, to)
+        elif op[0] == "drop":
+            o.reg_drop(reg, op[1])
+        else:
+            raise ValueError(op)
 
 
 def apply_warm_gpu(ctx, trace, ops):

@@ -115,8 +115,8 @@ _sig("pyg_set_shard", vp, i32, i32)
 _sig("pyg_dir_export_cap", vp, res=i64)
 _sig("pyg_dir_export_dev", vp, vp, i64, vp)
 _sig("pyg_dir_build_dev", vp, vp, i64)
-_sig("pyg_admit_shard_dev", vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, dbl, i32, vp, vp, vp, i64, vp,
-     i64, vp)
+_sig("pyg_admit_shard_dev", vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, dbl, i32, vp, vp, vp, i64, vp)
+_sig("pyg_shard_l3_resolve_dev", vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i64, i64, vp)
 _sig("pyg_dir_clear_dev", vp, vp, i64, vp)
 _sig("pyg_l3_erase_hashes_dev", vp, vp, i64, vp)
 _sig("pyg_gather_csr_dev", vp, vp, vp, vp, i64, vp, vp)
@@ -133,7 +133,11 @@ _sig("pyg_shard_pack_dev", vp, vp, vp, vp, i32, i32, i32, vp)
 _sig("pyg_shard_unpack_dev", vp, vp, i32, i32, i32, vp, vp, vp)
 _sig("pyg_shard_pull_dev", vp, vp, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64)
 _sig("pyg_shard_local_placed_dev", vp, vp, vp, vp, vp, vp, vp)
+_sig("pyg_stats", vp, vp, i32)
+_sig("pyg_nodes_compose_dev", vp, i32, vp, vp, vp, vp, vp, vp, vp)
+_sig("pyg_registry_update_batch_dev", vp, i32, vp, vp, i32)
 _sig("pyg_shard_apply_lists_dev", vp, vp, i32, i32)
+_sig("pyg_shard_apply_lists_range_dev", vp, vp, i32, i32, i32, i32, i32)
 _sig("pyg_shard_results_dev", vp, vp, i32, vp, vp, i64, i32, vp, vp)
 _sig("pyg_lookup_batch_dev", vp, vp, vp, vp, vp, i32, vp, i32, vp)
 _sig("pyg_route_batch_dev", vp, i32, C.POINTER(NodesDev), vp, i32, vp, i32, vp, vp, i32, vp,
@@ -222,6 +226,13 @@ class Context:
 
     def check_device_error(self):
         check(_lib.pyg_check_device_error(self.h))
+
+    def stats(self, reset=False) -> dict:
+        """pyg_stats: eviction counters (synchronizes the ctx stream)."""
+        out = np.zeros(4, np.int64)
+        check(_lib.pyg_stats(self.h, out.ctypes.data, int(bool(reset))))
+        return {"evicted_blocks": int(out[0]), "evicted_tokens": int(out[1]),
+                "evictions": int(out[2]), "unsatisfied": int(out[3])}
 
     # -- hashing
     def chain_hashes(self, tokens):

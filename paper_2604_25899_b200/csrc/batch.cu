@@ -102,6 +102,15 @@ __device__ __forceinline__ int64_t erase_claim(const TierDev& t, uint64_t key,
   return b.e - b.s;
 }
 
+// Per admission position p (index into the placed CSR = global admission order:
+// replica order, then placement order, engine.cpp:742-746): what the ordered L3
+// resolution needs.  l3s = L3 match against the L3 of the start of the call,
+// kb3 = its aligned block count, l3v = the match with earlier admissions'
+// promoted L3 spans erased (the engine's sequential start_prefill).
+struct L3Rec {
+  int64_t l12, kb3, l3s, l3v;
+};
+
 struct AdmitArgs {
   const uint64_t* tokens;
   const int64_t* tok_off;
@@ -115,7 +124,7 @@ struct AdmitArgs {
   int spec;
   int32_t* admitted;
   int64_t* match3;
-  int64_t* l3_span;  // [2R] deferred L3 erase span per request
+  L3Rec* l3rec;  // [n_placed] per admission position
   // sharded step: L2 blocks erased here are exported so every shard's directory follows
   DirRecord* l2_out;
   int64_t l2_cap;
@@ -164,11 +173,12 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     const int64_t nh = a.hash_off[r + 1] - a.hash_off[r];
     // the three aligned walks in one CTA-wide pass, then the three ragged
     // extensions at once, one warp's lane 0 per tier (each is a serial FNV run over <= 63 tokens)
-    int64_t m[3];
+    int64_t m[3], kb3;
     {
       int64_t kb[3];
       block_walk3(*t1p, *t2p, t3, hs, nh, sm, kb);
       for (int tier = 0; tier < 3; ++tier) m[tier] = kb[tier] ? matched_from_blocks(kb[tier], L, c.B) : 0;
+      kb3 = kb[2];
     }
     {
       const int tier = threadIdx.x >> 5;
@@ -192,7 +202,7 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
         a.match3[3 * r] = m[0];
         a.match3[3 * r + 1] = m[1];
         a.match3[3 * r + 2] = m[2];
-        a.l3_span[2 * r] = a.l3_span[2 * r + 1] = 0;
+        a.l3rec[k] = L3Rec{max(m[0], m[1]), kb3, m[2], m[2]};
       }
       __syncthreads();
       continue;
@@ -200,7 +210,6 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     const int64_t reusable = max(m[0], max(m[1], m[2]));
     const int64_t l2_part = max(min(reusable, m[1]) - m[0], int64_t{0});
     const int64_t l12 = max(m[0], m[1]);
-    const int64_t l3_part = max(reusable - l12, int64_t{0});
     if (l2_part > 0) {  // erase_chain_span(L2, seq, l1, l1 + l2_part)
       const TierDev t2 = *t2p;
       int64_t freed = 0, cnt = 0;
@@ -254,53 +263,214 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
       a.match3[3 * r] = m[0];
       a.match3[3 * r + 1] = m[1];
       a.match3[3 * r + 2] = m[2];
-      a.l3_span[2 * r] = l3_part > 0 ? l12 : 0;
-      a.l3_span[2 * r + 1] = l3_part > 0 ? reusable : 0;
+      a.l3rec[k] = L3Rec{l12, kb3, m[2], m[2]};
     }
     __syncthreads();
   }
 }
 
-// Deferred erase_chain_span(L3, seq, max(l1,l2), reusable) of every admitted
-// request (engine.cpp:826-828).  Erasures commute, so all requests go in
-// parallel; the slot CAS makes each block's erase happen once.
-__global__ void k_l3_erase(CtxDev c, const int64_t* tok_off, const int64_t* hash_off,
-                           const uint64_t* hashes, int R, const int32_t* admitted,
-                           const int64_t* l3_span, uint64_t* list, int64_t list_cap,
-                           unsigned long long* list_count) {
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// ------------------------------------------------ ordered L3 (engine order)
+// The engine admits one request at a time (start_prefill, engine.cpp:799-829):
+// request p looks up the LIVE L3, so it no longer sees the L3 blocks that an
+// earlier admission promoted (erase_chain_span(L3, max(l1,l2), reusable),
+// engine.cpp:826-828).  k_admit computes every admission's L1/L2 part exactly
+// (per replica, in order) and its L3 match against the L3 as of the start of
+// the call (nothing touches L3 until here).  The L3 part is a triangular
+// system -- p's live L3 match depends only on the erase spans of admissions
+// before p -- solved by Jacobi rounds:
+//   claim(t): every admitted p erases span(l12, max(l12, l3v)); each L3 block
+//             in it records min p as claim = (epoch t, p)          (k_l3_claim)
+//   walk(t):  l3v[p] = matched_prefix over the L3 blocks not claimed by an
+//             earlier position (aligned walk + ragged check)        (k_l3_walk)
+// A round that changes no l3v has reached the fixpoint, which is unique for a
+// triangular system, i.e. the sequential result.  After kL3Rounds rounds
+// without convergence, k_l3_fixup finishes in order on one CTA from the first
+// position that still changed (the prefix before it is a fixpoint of its own
+// subsystem, hence exact).  k_l3_final then erases the final spans (or lists
+// them, sharded step) and writes the L3 matches.
+constexpr int kL3Rounds = 3;
+
+struct L3Args {
+  const uint64_t* tokens;
+  const int64_t* tok_off;
+  const int64_t* hash_off;
+  const uint64_t* hashes;
+  const int32_t* placed_off;
+  const int32_t* placed;
+  const int32_t* admitted;
+  L3Rec* rec;
+  unsigned long long* claim;  // [L3 log_cap], (~epoch << 32) | position, min wins
+  int32_t* ctl;               // [1 + t] round t changed something; [16 + t] first change
+  int32_t n_rep;
+};
+
+__device__ __forceinline__ unsigned long long claim_pack(uint32_t epoch, int p) {
+  return (static_cast<unsigned long long>(0xFFFFFFFFu - epoch) << 32) | static_cast<uint32_t>(p);
+}
+
+struct ClaimVis {  // block li is visible to position p: no earlier position erases it
+  const unsigned long long* claim;
+  uint32_t epoch;
+  int p;
+  __device__ __forceinline__ bool operator()(int64_t li) const {
+    const unsigned long long v = __ldcg(claim + li);
+    return !((v >> 32) == (0xFFFFFFFFu - epoch) && static_cast<int>(v & 0xffffffffu) < p);
+  }
+};
+
+// L3 match of admission position p with earlier positions' claims hidden (one warp).
+__device__ int64_t l3_visible_match(const CtxDev& c, const L3Args& a, const L3Rec& q, int p,
+                                    uint32_t epoch) {
   const int lane = threadIdx.x & 31;
-  if (r >= R || admitted[r] != 1) return;
-  const int64_t from = l3_span[2 * r], to = l3_span[2 * r + 1];
-  if (to <= from) return;
-  TierDev* tp = c.tiers + 2 * c.n_rep;
-  const TierDev t = *tp;
-  const int64_t L = tok_off[r + 1] - tok_off[r];
-  const uint64_t* hs = hashes + hash_off[r];
-  const int64_t nh = hash_off[r + 1] - hash_off[r];
-  int64_t freed = 0, cnt = 0;
-  for (int64_t i = lane; i < nh; i += 32) {
-    const int64_t e = min((i + 1) * c.B, L);
-    if (e <= from || e > to) continue;
-    if (list) {  // sharded step: the shared L3 is replicated, every shard applies the union
-      const unsigned long long k = atomicAdd(list_count, 1ULL);
-      if (static_cast<int64_t>(k) < list_cap) list[k] = hs[i];
-      else atomicExch(c.error, 4);
-      continue;
+  const int r = a.placed[p];
+  const TierDev& t3 = c.tiers[2 * c.n_rep];
+  const int64_t L = a.tok_off[r + 1] - a.tok_off[r];
+  const uint64_t* hs = a.hashes + a.hash_off[r];
+  const ClaimVis vis{a.claim, epoch, p};
+  int64_t first = q.kb3;
+  for (int64_t base = 0; base < q.kb3; base += 32) {
+    const int64_t i = base + lane;
+    bool inv = false;
+    if (i < q.kb3) {
+      const int64_t li = idx_find(t3, hs[i]);
+      inv = li < 0 || !vis(li);
     }
-    const int64_t sz = erase_claim(t, hs[i]);
-    if (sz >= 0) {
-      freed += sz;
-      cnt += 1;
+    const unsigned m = __ballot_sync(kFull, inv);
+    if (m) {
+      first = base + __ffs(m) - 1;
+      break;
     }
   }
-  freed = warp_sum(freed);
-  cnt = warp_sum(cnt);
-  if (lane == 0 && cnt) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(&tp->occupancy),
-              static_cast<unsigned long long>(-freed));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&tp->n_alive),
-              static_cast<unsigned long long>(-cnt));
+  const int64_t aligned = first ? matched_from_blocks(first, L, c.B) : 0;
+  if (first == q.kb3 && q.l3s == aligned) return q.l3s;
+  int64_t v = 0;
+  if (lane == 0)
+    v = ragged_extend(t3, t3.log, a.tokens + a.tok_off[r], L, hs, aligned, c.B, vis);
+  return __shfl_sync(kFull, v, 0);
+}
+
+// p's erase span claims (one warp): blocks of p's chain with span_end in (l12, reusable]
+// present and unpinned in L3 (erase_chain_span, engine.cpp:849-861).
+__device__ void l3_claim_span(const CtxDev& c, const L3Args& a, const L3Rec& q, int p,
+                              uint32_t epoch) {
+  const int64_t reusable = max(q.l12, q.l3v);
+  if (reusable <= q.l12) return;
+  const int r = a.placed[p];
+  const TierDev& t3 = c.tiers[2 * c.n_rep];
+  const int64_t L = a.tok_off[r + 1] - a.tok_off[r];
+  const uint64_t* hs = a.hashes + a.hash_off[r];
+  const int64_t nh = a.hash_off[r + 1] - a.hash_off[r];
+  const unsigned long long v = claim_pack(epoch, p);
+  for (int64_t i = (q.l12 / c.B) + (threadIdx.x & 31); i < nh; i += 32) {
+    const int64_t e = min((i + 1) * c.B, L);
+    if (e <= q.l12) continue;
+    if (e > reusable) break;
+    const int64_t li = idx_find(t3, hs[i]);
+    if (li >= 0 && t3.log[li].pin <= 0) atomicMin(a.claim + li, v);
+  }
+}
+
+__device__ __forceinline__ bool l3_converged_before(const L3Args& a, int t) {
+  for (int u = 0; u < t; ++u)
+    if (a.ctl[1 + u] == 0) return true;
+  return false;
+}
+
+__global__ void k_l3_claim(CtxDev c, L3Args a, uint32_t epoch, int t) {
+  if (l3_converged_before(a, t)) return;
+  const int n = a.placed_off[a.n_rep];
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += nw) {
+    if (a.admitted[a.placed[p]] != 1) continue;
+    l3_claim_span(c, a, a.rec[p], p, epoch);
+  }
+}
+
+__global__ void k_l3_walk(CtxDev c, L3Args a, uint32_t epoch, int t) {
+  if (l3_converged_before(a, t)) return;
+  const int n = a.placed_off[a.n_rep];
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += nw) {
+    L3Rec& q = a.rec[p];
+    if (q.l3s == 0) continue;  // erasures only shrink matches
+    const int64_t v = l3_visible_match(c, a, q, p, epoch);
+    if ((threadIdx.x & 31) == 0 && v != q.l3v) {
+      q.l3v = v;
+      a.ctl[1 + t] = 1;
+      atomicMin(a.ctl + 16 + t, p);
+    }
+  }
+}
+
+// Not converged after kL3Rounds: finish in order on one CTA from the first position that
+// still changed (epoch = a fresh one: the prefix re-claims, then one position at a time).
+__global__ void k_l3_fixup(CtxDev c, L3Args a, uint32_t epoch) {
+  if (l3_converged_before(a, kL3Rounds)) return;
+  const int n = a.placed_off[a.n_rep];
+  const int k0 = a.ctl[16 + kL3Rounds - 1];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int p = w; p < k0; p += nw)
+    if (a.admitted[a.placed[p]] == 1) l3_claim_span(c, a, a.rec[p], p, epoch);
+  __threadfence();
+  __syncthreads();
+  if (w != 0) return;
+  for (int p = k0; p < n; ++p) {
+    L3Rec& q = a.rec[p];
+    if (q.l3s == 0) continue;
+    const int64_t v = l3_visible_match(c, a, q, p, epoch);
+    if ((threadIdx.x & 31) == 0) q.l3v = v;
+    __syncwarp();
+    if (a.admitted[a.placed[p]] == 1) l3_claim_span(c, a, q, p, epoch);
+    __threadfence();
+    __syncwarp();
+  }
+}
+
+// The final spans: erase (or list, sharded step: the shared L3 is replicated and every
+// shard applies the union) and report the L3 matches.  Erasing in any order gives the
+// sequential result: a block in p's span that an earlier admission already erased is
+// erased either way.
+__global__ void k_l3_final(CtxDev c, L3Args a, int64_t* match3, uint64_t* list, int64_t list_cap,
+                           unsigned long long* list_count) {
+  const int n = a.placed_off[a.n_rep];
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  TierDev* tp = c.tiers + 2 * c.n_rep;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += nw) {
+    const int r = a.placed[p];
+    const L3Rec q = a.rec[p];
+    if (lane == 0) match3[3 * r + 2] = q.l3v;
+    if (a.admitted[r] != 1) continue;
+    const int64_t reusable = max(q.l12, q.l3v);
+    if (reusable <= q.l12) continue;
+    const TierDev t = *tp;
+    const int64_t L = a.tok_off[r + 1] - a.tok_off[r];
+    const uint64_t* hs = a.hashes + a.hash_off[r];
+    const int64_t nh = a.hash_off[r + 1] - a.hash_off[r];
+    int64_t freed = 0, cnt = 0;
+    for (int64_t i = (q.l12 / c.B) + lane; i < nh; i += 32) {
+      const int64_t e = min((i + 1) * c.B, L);
+      if (e <= q.l12 || e > reusable) continue;
+      if (list) {
+        const unsigned long long k = atomicAdd(list_count, 1ULL);
+        if (static_cast<int64_t>(k) < list_cap) list[k] = hs[i];
+        else atomicExch(c.error, 4);
+        continue;
+      }
+      const int64_t sz = erase_claim(t, hs[i]);
+      if (sz >= 0) {
+        freed += sz;
+        cnt += 1;
+      }
+    }
+    freed = warp_sum(freed);
+    cnt = warp_sum(cnt);
+    if (lane == 0 && cnt) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&tp->occupancy),
+                static_cast<unsigned long long>(-freed));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&tp->n_alive),
+                static_cast<unsigned long long>(-cnt));
+    }
   }
 }
 
@@ -368,6 +538,26 @@ __global__ void k_dir_clear(CtxDev c, const DirRecord* rec, int64_t n, const int
                   r.replica);
 }
 
+// Node table of the next burst: per replica the base reservations, then the reservations
+// of the requests the last burst placed there, in placement order (the pool order of
+// reservation_of, engine.cpp:616-628, 686).  out_off = base_off + placed_off.
+__global__ void k_nodes_compose(int32_t n_rep, const int64_t* base_off,
+                                const pyg_reservation* base, const int32_t* placed_off,
+                                const int32_t* placed, const pyg_reservation* req,
+                                int64_t* out_off, pyg_reservation* out) {
+  const int n = blockIdx.x;
+  const int64_t b0 = base_off[n], nb = base_off[n + 1] - b0;
+  const int64_t p0 = placed_off ? placed_off[n] : 0;
+  const int64_t np = placed_off ? placed_off[n + 1] - p0 : 0;
+  const int64_t o = b0 + p0;
+  for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) out[o + i] = base[b0 + i];
+  for (int64_t i = threadIdx.x; i < np; i += blockDim.x) out[o + nb + i] = req[placed[p0 + i]];
+  if (threadIdx.x == 0) {
+    out_off[n] = o;
+    if (n == n_rep - 1) out_off[n_rep] = o + nb + np;
+  }
+}
+
 // dst segment k = src segment idx[k] (CSR gather of uint64 rows: tokens / hashes)
 __global__ void k_gather_csr(const uint64_t* src, const int64_t* src_off, const int64_t* idx,
                              int64_t n_idx, const int64_t* dst_off, uint64_t* dst) {
@@ -395,6 +585,15 @@ int pyg_check_device_error(pyg_ctx* c) {
   return PYG_OK;
 }
 
+int pyg_stats(pyg_ctx* c, int64_t* out, int32_t reset) {
+  if (!c || !out) return PYG_EINVAL;
+  PYG_CUDA(cudaSetDevice(c->device));
+  PYG_CUDA(cudaMemcpyAsync(out, c->hd.stats, 32, cudaMemcpyDeviceToHost, c->stream));
+  if (reset) PYG_CUDA(cudaMemsetAsync(c->hd.stats, 0, 32, c->stream));
+  PYG_CUDA(cudaStreamSynchronize(c->stream));
+  return PYG_OK;
+}
+
 int pyg_lookup_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
                          const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t R,
                          const int32_t* d_rep, int32_t with_l3, int64_t* d_match3) {
@@ -406,33 +605,94 @@ int pyg_lookup_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_
   return PYG_OK;
 }
 
-static int admit_impl(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
+// scratch layout of one admission call: L3Rec[R] | ctl[32] (kept until the L3 stage ran)
+static int admit_scratch(pyg_ctx* c, int32_t R, L3Rec** rec, int32_t** ctl) {
+  void* sp;
+  int rc = scratch(c, static_cast<size_t>(R) * sizeof(L3Rec) + 256, &sp);
+  if (rc) return rc;
+  *rec = static_cast<L3Rec*>(sp);
+  *ctl = reinterpret_cast<int32_t*>(static_cast<char*>(sp) + static_cast<size_t>(R) * sizeof(L3Rec));
+  return PYG_OK;
+}
+
+// k_admit: everything of start_prefill except the L3 promotion (see l3_stage)
+static int admit_core(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
                       const int64_t* d_hash_off, const uint64_t* d_hashes, const int32_t* d_wf,
                       const int32_t* d_role, int32_t R, const int32_t* d_placed_off,
                       const int32_t* d_placed, double now, int32_t speculative,
                       int32_t* d_admitted, int64_t* d_match3, void* l2_out, int64_t l2_cap,
-                      uint64_t* l3_out, int64_t l3_cap, int64_t* d_counts) {
+                      int64_t* d_counts) {
   if (!c || R < 0) return PYG_EINVAL;
+  PYG_CUDA(cudaSetDevice(c->device));
   if (d_counts) PYG_CUDA(cudaMemsetAsync(d_counts, 0, 16, c->stream));
   if (R == 0 || c->n_rep == 0) return PYG_OK;
-  void* sp;
-  int rc = scratch(c, static_cast<size_t>(R) * 16 + 64, &sp);
+  L3Rec* rec;
+  int32_t* ctl;
+  int rc = admit_scratch(c, R, &rec, &ctl);
   if (rc) return rc;
-  auto* l3span = static_cast<int64_t*>(sp);
   PYG_CUDA(cudaMemsetAsync(d_admitted, 0, static_cast<size_t>(R) * 4, c->stream));
   PYG_CUDA(cudaMemsetAsync(d_match3, 0, static_cast<size_t>(R) * 24, c->stream));
   auto* cnt = reinterpret_cast<unsigned long long*>(d_counts);
   AdmitArgs a{d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, d_placed_off, d_placed,
-              now, speculative, d_admitted, d_match3, l3span,
+              now, speculative, d_admitted, d_match3, rec,
               static_cast<DirRecord*>(l2_out), l2_cap, cnt};
   const size_t smem = kSmemSortCap * 12;
-  cudaFuncSetAttribute(k_admit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  PYG_CUDA(cudaFuncSetAttribute(k_admit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_admit<<<c->n_rep, 512, smem, c->stream>>>(c->hd, a);
   c->dir_admits += 1;
   PYG_LAUNCHED(c);
-  k_l3_erase<<<(R + 7) / 8, 256, 0, c->stream>>>(c->hd, d_tok_off, d_hash_off, d_hashes, R,
-                                                 d_admitted, l3span, l3_out, l3_cap,
-                                                 cnt ? cnt + 1 : nullptr);
+  return PYG_OK;
+}
+
+__global__ void k_clamp_counts(int64_t* counts, int64_t l2_cap, int64_t l3_cap) {
+  if (counts[0] > l2_cap) counts[0] = l2_cap;
+  if (counts[1] > l3_cap) counts[1] = l3_cap;
+}
+
+// The ordered L3 promotion of the admissions k_admit just ran (same arguments): Jacobi
+// rounds, the in-order fixup if needed, the final erase (or, l3_out != null, the list of
+// erased chain hashes for the sharded step, whose L3 replicas apply every shard's list).
+static int l3_stage(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                    const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t R,
+                    const int32_t* d_placed_off, const int32_t* d_placed,
+                    const int32_t* d_admitted, int64_t* d_match3, uint64_t* l3_out,
+                    int64_t l3_cap, int64_t* d_counts) {
+  if (!c || R < 0) return PYG_EINVAL;
+  PYG_CUDA(cudaSetDevice(c->device));
+  if (R == 0 || c->n_rep == 0) return PYG_OK;
+  L3Rec* rec;
+  int32_t* ctl;
+  int rc = admit_scratch(c, R, &rec, &ctl);
+  if (rc) return rc;
+  // per-L3-block claims; stale epochs read as "no claim"
+  const int64_t l3cap = c->tiers[2 * c->n_rep].d.log_cap;
+  if (l3cap > c->claim_cap) {
+    if (c->d_claim) {
+      PYG_CUDA(cudaStreamSynchronize(c->stream));
+      PYG_CUDA(cudaFree(c->d_claim));
+      c->d_claim = nullptr;
+    }
+    PYG_CUDA(cudaMalloc(&c->d_claim, static_cast<size_t>(l3cap) * 8));
+    PYG_CUDA(cudaMemsetAsync(c->d_claim, 0xff, static_cast<size_t>(l3cap) * 8, c->stream));
+    c->claim_cap = l3cap;
+  }
+  PYG_CUDA(cudaMemsetAsync(ctl, 0, 64, c->stream));
+  PYG_CUDA(cudaMemsetAsync(ctl + 16, 0x7f, 64, c->stream));
+  L3Args la{d_tokens, d_tok_off, d_hash_off, d_hashes, d_placed_off, d_placed, d_admitted,
+            rec, static_cast<unsigned long long*>(c->d_claim), ctl, c->n_rep};
+  const unsigned g = static_cast<unsigned>(std::min<int64_t>((R + 7) / 8, 4 * 148));
+  for (int t = 0; t < kL3Rounds; ++t) {
+    const uint32_t ep = ++c->claim_epoch;
+    k_l3_claim<<<g, 256, 0, c->stream>>>(c->hd, la, ep, t);
+    PYG_LAUNCHED(c);
+    k_l3_walk<<<g, 256, 0, c->stream>>>(c->hd, la, ep, t);
+    PYG_LAUNCHED(c);
+  }
+  k_l3_fixup<<<1, 1024, 0, c->stream>>>(c->hd, la, ++c->claim_epoch);
+  PYG_LAUNCHED(c);
+  auto* cnt = reinterpret_cast<unsigned long long*>(d_counts);
+  k_l3_final<<<g, 256, 0, c->stream>>>(c->hd, la, d_match3, l3_out, l3_cap,
+                                       cnt ? cnt + 1 : nullptr);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -442,9 +702,12 @@ int pyg_admit_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_t
                         const int32_t* d_role, int32_t R, const int32_t* d_placed_off,
                         const int32_t* d_placed, double now, int32_t speculative,
                         int32_t* d_admitted, int64_t* d_match3) {
-  return admit_impl(c, d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, R, d_placed_off,
-                    d_placed, now, speculative, d_admitted, d_match3, nullptr, 0, nullptr, 0,
-                    nullptr);
+  int rc = admit_core(c, d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, R,
+                      d_placed_off, d_placed, now, speculative, d_admitted, d_match3, nullptr, 0,
+                      nullptr);
+  if (rc) return rc;
+  return l3_stage(c, d_tokens, d_tok_off, d_hash_off, d_hashes, R, d_placed_off, d_placed,
+                  d_admitted, d_match3, nullptr, 0, nullptr);
 }
 
 int pyg_admit_shard_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
@@ -452,12 +715,27 @@ int pyg_admit_shard_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_t
                         const int32_t* d_role, int32_t R, const int32_t* d_placed_off,
                         const int32_t* d_placed, double now, int32_t speculative,
                         int32_t* d_admitted, int64_t* d_match3, void* d_l2_erased,
-                        int64_t l2_cap, uint64_t* d_l3_hashes, int64_t l3_cap,
-                        int64_t* d_counts) {
-  if (!d_counts || (l2_cap && !d_l2_erased) || (l3_cap && !d_l3_hashes)) return PYG_EINVAL;
-  return admit_impl(c, d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, R, d_placed_off,
+                        int64_t l2_cap, int64_t* d_counts) {
+  if (!d_counts || (l2_cap && !d_l2_erased)) return PYG_EINVAL;
+  return admit_core(c, d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, R, d_placed_off,
                     d_placed, now, speculative, d_admitted, d_match3, d_l2_erased, l2_cap,
-                    d_l3_hashes, l3_cap, d_counts);
+                    d_counts);
+}
+
+int pyg_shard_l3_resolve_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
+                             const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t R,
+                             const int32_t* d_placed_off, const int32_t* d_placed,
+                             const int32_t* d_admitted, int64_t* d_match3,
+                             uint64_t* d_l3_hashes, int64_t l3_cap, int64_t l2_cap,
+                             int64_t* d_counts) {
+  if (!d_counts || (l3_cap && !d_l3_hashes)) return PYG_EINVAL;
+  int rc = l3_stage(c, d_tokens, d_tok_off, d_hash_off, d_hashes, R, d_placed_off, d_placed,
+                    d_admitted, d_match3, d_l3_hashes, l3_cap, d_counts);
+  if (rc) return rc;
+  // peers read these counts over NVLink: never past the lists (overflow is error 4)
+  k_clamp_counts<<<1, 1, 0, c->stream>>>(d_counts, l2_cap, l3_cap);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
 }
 
 int pyg_l3_erase_hashes_dev(pyg_ctx* c, const uint64_t* d_hashes, int64_t n,
@@ -487,6 +765,19 @@ int pyg_gather_csr_dev(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_src_o
   if (n_idx > 0x7fffffff) return PYG_EINVAL;
   k_gather_csr<<<static_cast<unsigned>(n_idx), 128, 0, c->stream>>>(d_src, d_src_off, d_idx, n_idx,
                                                                     d_dst_off, d_dst);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_nodes_compose_dev(pyg_ctx* c, int32_t n_rep, const int64_t* d_base_off,
+                          const pyg_reservation* d_base, const int32_t* d_placed_off,
+                          const int32_t* d_placed, const pyg_reservation* d_req,
+                          int64_t* d_out_off, pyg_reservation* d_out) {
+  if (!c || n_rep < 0 || (d_placed_off && (!d_placed || !d_req))) return PYG_EINVAL;
+  if (!n_rep) return PYG_OK;
+  PYG_CUDA(cudaSetDevice(c->device));
+  k_nodes_compose<<<n_rep, 128, 0, c->stream>>>(n_rep, d_base_off, d_base, d_placed_off,
+                                                d_placed, d_req, d_out_off, d_out);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

@@ -80,6 +80,7 @@ struct CtxDev {
   int32_t B;
   int32_t pad;
   int32_t* error;       // device error flag
+  unsigned long long* stats;  // [4] evicted blocks, evicted tokens, evictions run, unsatisfied
   // L2 directory (dir.cuh); main == nullptr until built
   uint64_t* dir_main;
   uint64_t* dir_rver;

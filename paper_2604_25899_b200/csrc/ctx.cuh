@@ -45,6 +45,10 @@ struct pyg_ctx {
   int32_t hash_ctas = 0;     // K1 persistent grid cap (0 = one CTA per SM)
   void* d_aux = nullptr;     // second on-demand buffer (fused assembly's chunk sources)
   size_t d_aux_size = 0;
+  // ordered L3 resolution of batched admission (batch.cu): per-L3-block claims
+  void* d_claim = nullptr;
+  int64_t claim_cap = 0;
+  uint32_t claim_epoch = 0;
 };
 
 namespace pyg_host {

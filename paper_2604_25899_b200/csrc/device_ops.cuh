@@ -251,8 +251,16 @@ __device__ __forceinline__ int64_t thread_walk(const TierDev& t, const uint64_t*
 // one idx probe of the running hash plus a span check.  Identical result up to
 // 64-bit hash collisions (the reference itself treats equal chain hashes as
 // equal prefixes, hierarchy.hpp:26-28).
+struct AllVisible {
+  __device__ __forceinline__ bool operator()(int64_t) const { return true; }
+};
+
+// vis(log index): whether a present block counts (the ordered L3 resolution of
+// batched admission hides blocks an earlier admission of the same call erases).
+template <class Vis = AllVisible>
 __device__ inline int64_t ragged_extend(const TierDev& t, const Block* log, const uint64_t* tokens,
-                                 int64_t L, const uint64_t* hashes, int64_t matched, int B) {
+                                 int64_t L, const uint64_t* hashes, int64_t matched, int B,
+                                 Vis vis = Vis()) {
   if (matched >= L || matched % B != 0) return matched;
   const uint64_t parent = matched == 0 ? kFnvOffset : hashes[matched / B - 1];
   uint64_t mask = ridx_get(t, parent) | ridx_get(t, orphan_key(matched));
@@ -267,7 +275,7 @@ __device__ inline int64_t ragged_extend(const TierDev& t, const Block* log, cons
         const int64_t e = matched + o;
         if (e % B != 0) {
           const int64_t li = idx_find(t, h);
-          if (li >= 0 && log[li].s == matched && log[li].e == e) best = e;
+          if (li >= 0 && log[li].s == matched && log[li].e == e && vis(li)) best = e;
         }
       }
       if ((mask >> o) <= 1ULL) break;  // no higher candidate
@@ -278,7 +286,7 @@ __device__ inline int64_t ragged_extend(const TierDev& t, const Block* log, cons
     for (int64_t k = 0; k < t.log_len; ++k) {
       const Block& b = log[k];
       if (!(b.flags & kAlive) || !(b.flags & kOrphan) || b.s != matched) continue;
-      if (b.e > L || b.e % B == 0 || b.e - b.s < 64 || b.e <= best) continue;
+      if (b.e > L || b.e % B == 0 || b.e - b.s < 64 || b.e <= best || !vis(k)) continue;
       uint64_t h = parent;
       for (int64_t x = matched; x < b.e; ++x) h = fnv_token(h, tokens[x]);
       if (h == b.hash) best = b.e;
@@ -439,6 +447,12 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
   if (threadIdx.x == 0) {
     tp->occupancy -= ftot;
     tp->n_alive -= cut;
+    if (c.stats) {
+      atomicAdd(c.stats, static_cast<unsigned long long>(cut));
+      atomicAdd(c.stats + 1, static_cast<unsigned long long>(ftot));
+      atomicAdd(c.stats + 2, 1ULL);
+      if (ftot < excess) atomicAdd(c.stats + 3, 1ULL);
+    }
   }
   __syncthreads();
   r.n_freed = cut;

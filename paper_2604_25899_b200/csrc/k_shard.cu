@@ -253,11 +253,12 @@ __global__ void k_local_placed(const int32_t* placed_off, const int32_t* placed,
   }
 }
 
-__global__ void k_apply_lists(CtxDev c, const pyg_peer* peers, int world, int me) {
+__global__ void k_apply_lists(CtxDev c, const pyg_peer* peers, int world, int me, int l3_lo,
+                              int l3_hi, int with_l2) {
   TierDev* tp = c.tiers + 2 * c.n_rep;
   for (int k = 0; k < world; ++k) {
     const pyg_peer& p = peers[k];
-    const int64_t n3 = p.list_counts[1];
+    const int64_t n3 = k >= l3_lo && k < l3_hi ? p.list_counts[1] : 0;
     int64_t freed = 0, cnt = 0;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n3;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -279,7 +280,7 @@ __global__ void k_apply_lists(CtxDev c, const pyg_peer* peers, int world, int me
       atomicAdd(reinterpret_cast<unsigned long long*>(&tp->n_alive),
                 static_cast<unsigned long long>(-cnt));
     }
-    if (k == me || !c.dir_main) continue;
+    if (k == me || !with_l2 || !c.dir_main) continue;
     const int64_t n2 = p.list_counts[0];
     const DirRecord* rec = static_cast<const DirRecord*>(p.l2_list);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n2;
@@ -502,7 +503,16 @@ int pyg_shard_local_placed_dev(pyg_ctx* c, const int32_t* d_placed_off, const in
 
 int pyg_shard_apply_lists_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world, int32_t me) {
   if (!c || world < 1) return PYG_EINVAL;
-  k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me);
+  k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, 0, world, 1);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_shard_apply_lists_range_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world,
+                                    int32_t me, int32_t l3_lo, int32_t l3_hi, int32_t with_l2) {
+  if (!c || world < 1 || l3_lo < 0 || l3_hi > world) return PYG_EINVAL;
+  if (l3_lo >= l3_hi && !with_l2) return PYG_OK;
+  k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, l3_lo, l3_hi, with_l2);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

@@ -299,6 +299,20 @@ __global__ void k_reg_set(CtxDev c, int32_t wf, uint8_t present, uint64_t mask) 
   c.reg_mask[wf] = mask;
 }
 
+// FutureRegistry::update for a batch of distinct workflows (a burst's issue-time updates,
+// engine.cpp:605-609, last write per workflow).  Out-of-range ids set the error flag.
+__global__ void k_reg_set_batch(CtxDev c, int32_t n, const int32_t* wf, const uint64_t* mask) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t w = wf[i];
+  if (w < 0 || w >= c.reg_cap) {
+    atomicExch(c.error, 6);
+    return;
+  }
+  c.reg_mask[w] = mask[i];
+  c.reg_present[w] = 1;
+}
+
 __global__ void k_dump(CtxDev c, int ti, pyg_block* out, int64_t cap, int64_t* count) {
   __shared__ int64_t sm[64];
   const TierDev t = c.tiers[ti];
@@ -643,6 +657,18 @@ int pyg_registry_update(pyg_ctx* c, int32_t wf, uint64_t mask) {
   int rc = reg_grow(c, wf);
   if (rc) return rc;
   k_reg_set<<<1, 1, 0, c->stream>>>(c->hd, wf, 1, mask);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_registry_update_batch_dev(pyg_ctx* c, int32_t n, const int32_t* d_wf,
+                                  const uint64_t* d_mask, int32_t max_wf) {
+  if (!c || n < 0 || max_wf < 0) return PYG_EINVAL;
+  if (!n) return PYG_OK;
+  PYG_CUDA(cudaSetDevice(c->device));
+  int rc = reg_grow(c, max_wf);
+  if (rc) return rc;
+  k_reg_set_batch<<<(n + 255) / 256, 256, 0, c->stream>>>(c->hd, n, d_wf, d_mask);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

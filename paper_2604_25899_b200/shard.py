@@ -19,11 +19,12 @@ the burst (global issue order = rank order, then index).  One step:
          hashes out of the origin GPU's HBM over NVLink (CUDA IPC peer mappings set up
          once; csrc/k_shard.cu) -- sizes bounded by capacity_holds, counts on device
   6. K4/K5 admission on the owner, per replica in global placement order
-         (engine.cpp:799-829); it exports the L2 blocks it erases and the L3 chain
-         hashes it promotes
-  7. a second flag barrier, then every rank reads every peer's lists in place:
-         clears the directory bits and erases the union from its replica of the
-         shared L3 (erasures commute)
+         (engine.cpp:799-829); it exports the L2 blocks it erases
+  7. the L3 promotions in engine order, chained over the ranks: rank g waits for
+         the L3 erase lists of ranks < g (their admissions come first), applies them
+         to its replica of the shared L3, resolves its own admissions' L3 matches in
+         order and publishes its list; then every rank applies the remaining lists
+         and clears the directory bits of every other rank's L2 erasures
   8. release (unpin) on the owner; each origin reads its requests' admission results
          from the owners (peer loads).  No host synchronisation inside the step.
 
@@ -332,16 +333,36 @@ class ShardedStep:
                                       _ptr(self.recv_role), self.cap_req, _ptr(self.p_off),
                                       _ptr(self.p_loc), now, int(bool(speculative)),
                                       _ptr(self.adm), _ptr(self.m3), _ptr(self.l2_list),
-                                      self.cap_hash, _ptr(self.l3_list), self.cap_hash,
-                                      _ptr(self.counts)))
+                                      self.cap_hash, _ptr(self.counts)))
         mark("admit")
-        # 7: every shard applies every shard's L3 erasures and L2-directory clears
+        # 7: the L3 promotions in engine order: rank g's admissions follow every lower rank's
+        # (global replica order), so it waits for their L3 erase lists, applies them to its
+        # replica of the shared L3, resolves its own in order and publishes its list; then
+        # every shard applies the remaining lists and every other shard's L2-directory clears
+        def resolve():
+            check(lib.pyg_shard_l3_resolve_dev(ctx.h, _ptr(self.r_tok), _ptr(self.recv_toff),
+                                               _ptr(self.recv_hoff), _ptr(self.r_hash),
+                                               self.cap_req, _ptr(self.p_off), _ptr(self.p_loc),
+                                               _ptr(self.adm), _ptr(self.m3), _ptr(self.l3_list),
+                                               self.cap_hash, self.cap_hash, _ptr(self.counts)))
+
+        me = plan.rank
         if self.p2p:
-            check(lib.pyg_shard_signal_dev(ctx.h, _ptr(self.flag_of[1]), W, plan.rank, self.seq))
+            if me > 0:
+                check(lib.pyg_shard_wait_dev(ctx.h, _ptr(self.flags[W:]), me, self.seq))
+                check(lib.pyg_shard_apply_lists_range_dev(ctx.h, _ptr(self.peers), W, me, 0, me,
+                                                          0))
+            resolve()
+            check(lib.pyg_shard_signal_dev(ctx.h, _ptr(self.flag_of[1]), W, me, self.seq))
             check(lib.pyg_shard_wait_dev(ctx.h, _ptr(self.flags[W:]), W, self.seq))
         else:
-            barrier_on_stream(self.dev)
-        check(lib.pyg_shard_apply_lists_dev(ctx.h, _ptr(self.peers), W, plan.rank))
+            for k in range(W):   # one stream barrier per rank's turn
+                if k == me:
+                    check(lib.pyg_shard_apply_lists_range_dev(ctx.h, _ptr(self.peers), W, me, 0,
+                                                              me, 0))
+                    resolve()
+                barrier_on_stream(self.dev)
+        check(lib.pyg_shard_apply_lists_range_dev(ctx.h, _ptr(self.peers), W, me, me, W, 1))
         mark("l2l3_lists")
         # 8: release on the owner; results of my requests from their owners
         if release:
