@@ -1,26 +1,36 @@
 #!/usr/bin/env python
 """Routed requests/sec of the B200 scheduling hot path (BASELINE.json metric).
 
-One *step* = one burst of R requests of the config-2 trace (deep-research DAG,
-10k workflows, 6 roles, 2 models x 16 replicas, 16-token blocks) routed
-through the whole hot path on device:
-  K1 chain hashing -> K2 staged-L2 matrix (every request x candidate replica)
-  -> K3 sequential-commit routing (engine order) -> K4/K5 admission of placed
-  requests (lookup with L3, evict_for_space, promoted-span erase, insert_chain
-  pinned) -> K5 release (unpin).
-Inputs are resident in HBM for `value`; `e2e` runs the same step through the
-host-buffer C-ABI entry pyg_step_host (pinned host arrays copied in and results
-copied out every step).
+Workload (default): BASELINE config 4, the bursty multi-LLM trace -- L ~ lognormal(2048, cv 1)
+in [64, 32768] tokens, 512 shared system prefixes, 10% unprofiled requests -- on 256 replicas
+(8 models x 32), 16-token blocks, kv 100k / L2 200k tokens per replica.  The trace arrives in
+bursts of 125,000 requests per GPU; 8 bursts = the config's 1M requests.  `--workload
+long_context` is config 3 (32,768-token prompts, 64 replicas, kv 141k: capacity-bound).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-Multi-GPU (torchrun, one rank per GPU): weak scaling -- each rank owns its own
-cluster shard (its models' replicas) and its own burst; no data-path collective.
+One step = one burst through the whole hot path on a cluster whose state carries over
+(paper_2604_25899_b200/steady.py): release of burst k-2 (its placements complete) ->
+node table = background + burst k-1's placements -> registry updates -> K2 staged matrix ->
+K3 sequential-commit route -> K4/K5 admission (evict_for_space, promoted L2/L3 spans erased in
+engine order, insert_chain).  K1 (chain hashing) of burst k+1 runs on a second stream during
+step k; every step still hashes its own burst inside the timed region.  Every step routes a
+DISTINCT burst; L1 starts near full (warm fill) so admissions evict.
+
+  value  : routed requests/s with the bursts resident in HBM (CUDA events, max over ranks)
+  e2e    : the same steps through the public API from pinned HOST buffers: every burst's
+           tokens + metadata copied host->device and decisions/admissions/lookups copied back
+           inside the timed region
+  --impl reference : the unmodified reference (oracle/_ref) through the identical burst
+           sequence (same seeds, cluster, warm state), each burst a bounded prefix sample,
+           node_view staged values over all host threads
+  --check K : K full-size bursts on the GPU and through the reference; compares every
+           decision, admission, lookup, staged value and, at the end, every tier
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--check K]
 """
 from __future__ import annotations
 
 import argparse
 import json
-import multiprocessing as mp
 import os
 import statistics
 import subprocess
@@ -38,35 +48,57 @@ INT_CEILING_GBS = 4110.0
 METRIC = "routed requests/sec (prefix-match+evict+route) at 1/2/4/8 B200; % HBM peak"
 UNIT = "requests/s"
 
+DEFAULTS = {  # per workload: requests per burst per GPU, replicas, models, kv, l2
+    "bursty": dict(requests=125_000, replicas=256, models=8, kv=100_000, l2=200_000),
+    "long_context": dict(requests=12_500, replicas=64, models=1, kv=141_000, l2=200_000),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="deep_research", choices=["deep_research", "bursty"],
-                    help="deep_research = config 2 (default); bursty = config 4 (per-GPU slice)")
-    ap.add_argument("--requests", type=int, default=125_000, help="bursty: requests per GPU")
-    ap.add_argument("--workflows", type=int, default=10_000)
-    ap.add_argument("--model-stride", type=int, default=0,
-                    help="experiments: emulate the N-GPU burst's model groups on one GPU")
-    ap.add_argument("--replicas", type=int, default=32)
+    ap.add_argument("--workload", default="bursty", choices=list(DEFAULTS))
+    ap.add_argument("--requests", type=int, default=0, help="requests per burst per GPU")
+    ap.add_argument("--replicas", type=int, default=0)
+    ap.add_argument("--models", type=int, default=0)
+    ap.add_argument("--kv", type=int, default=0)
+    ap.add_argument("--l2", type=int, default=0)
     ap.add_argument("--block", type=int, default=16)
-    ap.add_argument("--kv", type=int, default=100_000)
-    ap.add_argument("--l2", type=int, default=200_000)
-    ap.add_argument("--mode", default="seq", choices=["seq", "snapshot"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--check", type=int, default=0,
+                    help="parity: K full-size bursts on the GPU and through the reference")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--sample", type=int, default=0,
+                    help="reference arm / cpu_baseline: requests per burst (bounded prefix)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
-    ap.add_argument("--k1-after", default="start", choices=["staged", "start"],
-                    help="overlap (one GPU): K1 of step k+1 starts with step k (start) or "
-                         "after its K2 (staged)")
     ap.add_argument("--free-sms", type=int, default=8,
-                    help="K1 of step k+1 overlaps steps k's route/admission on a second stream, "
-                         "its grid capped at (SMs - free_sms); -1 = no overlap (serial step)")
-    return ap.parse_args()
+                    help="K1 of step k+1 overlaps step k on a second stream, its grid capped at "
+                         "(SMs - free_sms); -1 = no overlap (serial step)")
+    a = ap.parse_args()
+    for k, v in DEFAULTS[a.workload].items():
+        if not getattr(a, k):
+            setattr(a, k, v)
+    return a
+
+
+def maybe_self_launch(args):
+    """bench.py --gpus N without torchrun: relaunch as N ranks (one process per GPU)."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+               str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
 
 
 def peaks():
@@ -79,13 +111,23 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 class Clocks:
     """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
 
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.out = []
 
     def start(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -103,11 +145,8 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
-        rows = []
-        for line in out.strip().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                rows.append(parts)
+        rows = [[x.strip() for x in line.split(",")] for line in out.strip().splitlines()]
+        rows = [r for r in rows if len(r) == 6]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
@@ -121,668 +160,513 @@ class Clocks:
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 # ------------------------------------------------------------------ workload
-def build_workload(args, rank, ws, device):
-    """Rank `rank`'s burst and the GLOBAL cluster.  ws == 1: config 2 as stated (10k
-    workflows, 2 models x 16 replicas).  ws > 1 (weak scaling): every rank adds one config-2
-    unit -- 10k workflows with their own ids and two more models of 16 replicas, owned by
-    that rank; workflow w runs on model pair w % ws, so 1 - 1/ws of each rank's requests are
-    routed to and admitted on other GPUs."""
+def setup_cluster(args):
     from paper_2604_25899_b200 import workload as W
+    return W.make_cluster(args.replicas, args.models, kv=args.kv, l2=args.l2, seed=0)
+
+
+def warm_inputs(args, cl, device):
+    """The warm trace, its ops and the warm-fill plan (identical for every arm)."""
+    from paper_2604_25899_b200 import steady as S
+    n = 64 * args.replicas if args.workload == "bursty" else 4 * args.replicas
+    warm = S.make_burst(10_000, n, args.seed + 17, device, args.workload, args.models)
+    l2g = 64 if args.workload == "bursty" else 8
+    ops = S.warm_ops(warm, cl, l3_prefixes=128 if args.workload == "bursty" else 16,
+                     l2_per_group=l2g, seed=args.seed)
+    off, placed = S.warm_fill_plan(warm, cl)
+    return warm, ops, off, placed
+
+
+def describe(args, ws):
     if args.workload == "bursty":
-        # config 4: 1M requests over 4 models x 64 replicas at 8 GPUs = 125k requests and
-        # 32 replicas (8 per model, interleaved) per GPU
-        tr = W.bursty(n_requests=args.requests, seed=1 + rank, device=device,
-                      r_base=rank * args.requests)
-        cl = W.make_cluster(args.replicas * ws, 4, kv=args.kv, l2=args.l2, seed=0,
-                            interleave=True)
-        return tr, cl
-    stride = ws if ws > 1 else args.model_stride
-    tr = W.deep_research(n_workflows=args.workflows, seed=1 + rank, device=device,
-                         wf_base=rank * args.workflows, model_stride=stride)
-    cl = W.make_cluster(args.replicas * ws, 2 * max(stride, 1), kv=args.kv, l2=args.l2, seed=0)
-    return tr, cl
+        return (f"config-4 bursty multi-LLM trace in bursts of {args.requests} requests per GPU "
+                f"({ws * args.requests} per step; 8 steps x 125k = the config's 1M requests at N=1), "
+                f"L~lognormal(2048, cv 1) in [64, 32768], 512 shared prefixes, 10% unprofiled, "
+                f"{args.replicas} replicas ({args.models} models x {args.replicas // args.models}), "
+                f"B={args.block}, kv={args.kv}, l2={args.l2}; state carried across bursts "
+                f"(placements held 2 bursts, releases, warm-filled L1 -> eviction, ordered L3)")
+    return (f"config-3 long-context mix in bursts of {args.requests} requests per GPU: "
+            f"L=32768 (2048 role sys + 28672 carried context + 2048 unique), {args.replicas} "
+            f"replicas, kv={args.kv} (capacity_holds binds), B={args.block}, l2={args.l2}; state "
+            f"carried across bursts")
 
 
-def n_workflows_total(args, ws, tr):
-    if args.workload == "bursty":
-        return (ws * args.requests) // 8 + 1
-    return ws * args.workflows
+def algorithmic_bytes(bursts_host, B, cl, stats, max_cand):
+    """SURVEY.md 8(d) bytes of the timed steps: K1 (8L + 8 ceil(L/B) + 16 per request), K2
+    (32 B per probe of the per-candidate walks the reference semantics require: staged/B + 1
+    per (request, candidate)), K3 (32 + 24 per request), admission (64 B per inserted block +
+    32 B per lookup probe on 3 tiers), eviction (24 B per scanned L1 block + 8 per victim)."""
+    tot = {"hash": 0, "staged": 0, "route": 0, "admit": 0, "evict": 0, "probes": 0}
+    for tok_off, group, staged, placed in bursts_host:
+        L = np.diff(tok_off)
+        nb = (L + B - 1) // B
+        tot["hash"] += 8 * int(L.sum()) + 8 * int(nb.sum()) + 16 * (len(L) + 1)
+        ncand = np.diff(cl.cand_off)[group]
+        mask = np.arange(max_cand)[None, :] < ncand[:, None]
+        probes = int(((staged + B - 1) // B + 1)[mask].sum())
+        tot["probes"] += probes
+        tot["staged"] += 32 * probes + 4 * int(mask.sum())
+        tot["route"] += 56 * len(L)
+        tot["admit"] += int(sum(32 * 3 * (nb[r] // 4 + 1) + 64 * nb[r] for r in placed))
+    blocks_per_l1 = float(np.mean(cl.kv_capacity)) / B
+    tot["evict"] = int(24 * stats["evictions"] * blocks_per_l1 + 8 * stats["evicted_blocks"])
+    tot["total"] = sum(tot[k] for k in ("hash", "staged", "route", "admit", "evict"))
+    return tot
 
 
-def describe(args, tr, ws):
-    if args.workload == "bursty":
-        return (f"config-4 bursty multi-LLM slice: {args.requests} requests/GPU "
-                f"({ws * args.requests} total), L~lognormal(2048,1.0) in [64,32768], 4 models x "
-                f"{args.replicas * ws // 4} replicas = {args.replicas * ws} replicas "
-                f"({args.replicas}/GPU), B={args.block}, kv={args.kv}, l2={args.l2}")
-    if ws == 1:
-        return (f"config-2 deep_research burst: {args.workflows} workflows = {tr.R} requests/step, "
-                f"6 roles, 2 models x {args.replicas // 2} replicas, B={args.block}, kv={args.kv}, "
-                f"l2={args.l2}")
-    return (f"config-2 deep_research burst per GPU: {args.workflows} workflows (~{tr.R} requests) "
-            f"per GPU, 6 roles, {2 * ws} models x {args.replicas // 2} replicas = "
-            f"{args.replicas * ws} replicas sharded {args.replicas}/GPU, B={args.block}, "
-            f"kv={args.kv}, l2={args.l2}")
-
-
-def warm_l2(ctx, tr, cl, rng, frac=0.01, rep_base=0, n_local=None, n_workflows=None):
-    """Stage a sample of prompts' prefixes into replicas' L2 (what forward staging does,
-    manager.cpp:60-100), so the staged matrix has real hits and tie-breaks.  Only this
-    ctx's replicas [rep_base, rep_base + n_local) are written."""
-    n_local = cl.n_replicas if n_local is None else n_local
-    mine = [r for r in range(tr.R)
-            if any(rep_base <= c < rep_base + n_local
-                   for c in cl.cand[cl.cand_off[tr.group[r]]:cl.cand_off[tr.group[r] + 1]])]
-    n = max(1, int(tr.R * frac))
-    for r in rng.choice(mine, min(n, len(mine)), replace=False):
-        g = int(tr.group[r])
-        cands = [c for c in cl.cand[cl.cand_off[g]:cl.cand_off[g + 1]]
-                 if rep_base <= c < rep_base + n_local]
-        rep = int(rng.choice(cands))
-        p = tr.prompt(int(r))
-        ctx.insert_chain(rep - rep_base, 1, p, int(len(p) * rng.uniform(0.3, 1.0)),
-                         int(tr.wf[r]), int(tr.role[r]), 0.5, 0)
-    for w in range(0, n_workflows or int(tr.wf.max()) + 1):
-        ctx.registry_update(w, 0x3E)  # every workflow still expects roles 1..5
-
-
-def algorithmic_bytes(tr, B, staged, max_cand, cl, placed, match3):
-    """SURVEY.md 8(d) per-step byte count of the hot path."""
-    L = np.diff(tr.tok_off)
-    nb = (L + B - 1) // B
-    hash_bytes = 8 * int(L.sum()) + 8 * int(nb.sum()) + 16 * (tr.R + 1)
-    ncand = np.diff(cl.cand_off)[tr.group]
-    st = staged[:tr.R]
-    mask = np.arange(max_cand)[None, :] < ncand[:, None]
-    probes = int(((st + B - 1) // B + 1)[mask].sum())
-    staged_bytes = 32 * probes + 4 * int(mask.sum())
-    route_bytes = 32 * tr.R + 24 * tr.R
-    adm = placed
-    l1 = match3[:tr.R, 0]
-    admit_bytes = 0
-    if adm.size:
-        admit_bytes = int(sum(32 * (3 * (nb[r] // 4 + 1)) + 64 * nb[r] for r in adm))
-    return {"hash": hash_bytes, "staged": staged_bytes, "route": route_bytes,
-            "admit": admit_bytes, "total": hash_bytes + staged_bytes + route_bytes + admit_bytes,
-            "probes": probes}
-
-
-# --------------------------------------------------------------- CPU baseline
-def _cpu_worker(payload):
-    """Reference engine composition (oracle/_ref, unmodified sources) on one core."""
-    wf_count, seed, seconds, replicas, kv, l2, B, rank_base, workload = payload
-    import torch  # noqa: F401
-    from oracle.py_oracle import Reference
-    from oracle.step import apply_warm_oracle, warm_ops
-    from paper_2604_25899_b200 import workload as W
-    ref = Reference(B)
-    if workload == "bursty":
-        tr = W.bursty(n_requests=wf_count * 8, seed=seed, device="cpu")
-        cl = W.make_cluster(replicas, 4, kv=kv, l2=l2, seed=seed, interleave=True)
-    else:
-        tr = W.deep_research(n_workflows=wf_count, seed=seed, device="cpu")
-        cl = W.make_cluster(replicas, 2, kv=kv, l2=l2, seed=seed, id_base=rank_base)
-    caches = [ref.new_cache(int(cl.kv_capacity[n]), int(cl.l2_capacity[n])) for n in range(replicas)]
-    l3, reg = ref.new_l3(), ref.new_registry()
-    apply_warm_oracle(ref, caches, l3, reg, tr, warm_ops(tr, cl, seed, n_chains=4))
-    toks = tr.tokens_np()
-    done, t0 = 0, time.perf_counter()
-    chunk = 64
-    step = 0
-    while time.perf_counter() - t0 < seconds:
-        a = (done % tr.R)
-        b = min(a + chunk, tr.R)
-        idx = np.arange(a, b)
-        sub = tr.subset(idx)
-        ref.step(caches, l3, reg, True, sub.tokens_np(), sub.tok_off, sub.res, sub.group, sub.wf,
-                 sub.role, cl, 1, 0.05, 1.0 + step, True, want_out=False)
-        done += b - a
-        step += 1
-    el = time.perf_counter() - t0
+# --------------------------------------------------------------- reference arm
+def reference_run(args, n_steps, n_warm, threads, hash_once, sample, seconds=None):
+    """The reference through the burst sequence: warm state as ours, then bursts 0.. each
+    truncated to its first `sample` requests.  Returns (requests, seconds) of the measured
+    steps (those after n_warm), stopping early once `seconds` elapse."""
+    from oracle.steady_ref import RefSteady
+    from paper_2604_25899_b200 import steady as S
+    cl = setup_cluster(args)
+    warm, ops, off, placed = warm_inputs(args, cl, "cpu")
+    ref = RefSteady(args.block, cl, threads=threads, hash_once=hash_once)
+    ref.warm(warm, ops, off, placed)
+    done, el = 0, 0.0
+    for k in range(n_warm + n_steps):
+        tr = S.make_burst(k, args.requests, args.seed, "cpu", args.workload, args.models,
+                          n_keep=sample)
+        toks = tr.tokens_np()
+        rw, rm = S.registry_pairs(tr.wf, tr.role)
+        t0 = time.perf_counter()
+        ref.step(k, toks, tr.tok_off, tr.res, tr.group, tr.wf, tr.role, rw, rm, 1.0 + k)
+        dt = time.perf_counter() - t0
+        if k >= n_warm:
+            done += tr.R
+            el += dt
+            if seconds is not None and el >= seconds:
+                break
     return done, el, float(np.diff(tr.tok_off).mean())
 
 
-def cpu_baseline(args, cores, seconds):
+def cpu_sample_desc(args, n, threads, hash_once, mean_len, sample):
+    how = ("chain_boundary_hashes once + tier(L2).matched_prefix per candidate (hash-once)"
+           if hash_once else "cache.lookup(prompt, nullptr).l2 per candidate (the engine's "
+           "node_view, one rehash per candidate)")
+    return (f"{n} requests = the first {sample} of each {args.workload} burst (same seeds, "
+            f"cluster, warm state; state carried across the sample bursts), mean prompt "
+            f"{mean_len:.0f} tokens, through the unmodified reference "
+            f"(oracle/_ref/libpythia_ref{args.block}.so pref_burst: {how}, route, admission "
+            f"with evict_for_space, releases) on {args.replicas} replicas, {threads} thread(s); "
+            f"CPU {cpu_model()}")
+
+
+def cpu_baseline(args, hash_once=False):
     from oracle.py_oracle import reference_available
     if not reference_available(args.block):
         return None
-    wf = max(40, min(args.workflows, 400))
-    payloads = [(wf, 100 + i, seconds, args.replicas, args.kv, args.l2, args.block, 0,
-                 args.workload) for i in range(cores)]
-    if cores == 1:
-        res = [_cpu_worker(payloads[0])]
-    else:
-        ctx = mp.get_context("fork")
-        with ctx.Pool(cores) as pool:
-            res = pool.map(_cpu_worker, payloads)
-    rate = sum(d / e for d, e, _ in res)
-    n = sum(d for d, _, _ in res)
-    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": (f"{n} {'config-4' if args.workload == 'bursty' else 'config-2'} requests "
-                       f"(mean prompt {res[0][2]:.0f} tokens) routed through "
-                       f"the unmodified reference (oracle/_ref/libpythia_ref{args.block}.so, "
-                       f"pref_step: per-candidate lookup, route, admit, release) on "
-                       f"{args.replicas} replicas, {cores} process(es) x {seconds:.0f}s")}
-
-
-def _lib_check(ctx, db):
-    """hash_off from the freshly assembled tok_off (on device, no host sync)."""
-    import ctypes as C
-    from paper_2604_25899_b200 import _lib
-    _lib.check(_lib._lib.pyg_hash_offsets_dev(ctx.h, C.c_void_p(db.tok_off.data_ptr()), db.R,
-                                              C.c_void_p(db.hash_off.data_ptr()), None))
+    sample = args.sample or (1000 if args.workload == "bursty" else 100)
+    n, el, ml = reference_run(args, 50, 1, 1, hash_once, sample, args.cpu_seconds)
+    return {"value": n / el, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": cpu_sample_desc(args, n, 1, hash_once, ml, sample)}
 
 
 def run_reference(args):
-    ws, rank, local = dist_env()
+    ws, rank, _ = dist_env()
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
-    if args.profile:
-        cores = 1
-    t_budget = max(5.0, min(args.cpu_seconds, 20.0))
-    t0 = time.perf_counter()
-    bl = cpu_baseline(args, cores, t_budget)
-    if bl is None:
+    from oracle.py_oracle import reference_available
+    if not reference_available(args.block):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    el = time.perf_counter() - t0
-    line = {"impl": "reference", "metric": METRIC, "value": bl["value"], "unit": UNIT,
+    cores = os.cpu_count() or 1
+    sample = args.sample or (4000 if args.workload == "bursty" else 200)
+    n, el, ml = reference_run(args, args.steps, args.warmup, cores, False, sample)
+    value = n / el
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * el / max(args.steps, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": f"{args.workload} burst (bounded CPU sample)",
+            "config": {"workload": describe(args, 1) + " [bounded prefix sample per burst]",
                        "replicas": args.replicas, "block_tokens": args.block,
-                       "route_mode": "seq_commit"},
-            "cpu_baseline": bl,
-            "e2e": {"value": bl["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                       "route_mode": "seq_commit", "sample_requests_per_burst": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": cpu_sample_desc(args, n, cores, False, ml, sample)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
 # ------------------------------------------------------------------ our arm
+class Arm:
+    """One GPU's state for the steady-state bench: bursts in HBM, the cluster ctx, the
+    hashing ctx on its own stream."""
+
+    def __init__(self, args, dev, n_bursts):
+        import ctypes
+        import torch
+        from paper_2604_25899_b200 import Context
+        from paper_2604_25899_b200 import steady as S
+        self.args, self.dev, self.S = args, dev, S
+        self.cl = setup_cluster(args)
+        cl = self.cl
+        self.ctx = Context(cl.n_replicas, cl.kv_capacity, cl.l2_capacity, args.block,
+                           device=dev.index)
+        torch.cuda.set_stream(torch.cuda.Stream(device=dev, priority=-1))
+        self.S_stream = torch.cuda.current_stream(dev)
+        from paper_2604_25899_b200 import batch as PB
+        self.PB = PB
+        PB.bind_current_stream(self.ctx)
+        warm, ops, off, placed = warm_inputs(args, cl, dev)
+        self.n_fill = S.apply_warm_fill_gpu(self.ctx, warm, off, placed, args.block, dev)
+        S.apply_ops_gpu(self.ctx, warm, ops)
+        del warm
+        self.bursts = []
+        for k in range(n_bursts):
+            tr = S.make_burst(k, args.requests, args.seed, dev, args.workload, args.models)
+            self.bursts.append(S.upload_burst(tr, args.block, dev))
+            del tr
+        self.st = S.Steady(self.ctx, cl, args.requests, dev)
+        self.overlap = args.free_sms >= 0
+        self.H = torch.cuda.Stream(device=dev, priority=0) if self.overlap else self.S_stream
+        self.hctx = Context(0, [], [], args.block, device=dev.index)
+        self.hctx.set_stream(ctypes.c_void_p(self.H.cuda_stream))
+        if self.overlap:
+            n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+            self.hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
+        self.ev_h = {}
+        torch.cuda.synchronize(dev)
+        self.ctx.check_device_error()
+
+    def launches(self):
+        return self.ctx.kernel_launches() + self.hctx.kernel_launches()
+
+    def hash_into(self, k, hev=None):
+        import torch
+        self.H.wait_stream(self.S_stream)  # K1(k) starts with step k-1 (step k-2 is done)
+        if hev is not None:
+            hev[0].record(self.H)
+        self.PB.hash_batch(self.hctx, self.bursts[k].b)
+        if hev is not None:
+            hev[1].record(self.H)
+        e = torch.cuda.Event()
+        e.record(self.H)
+        self.ev_h[k] = e
+
+    def run(self, k0, n, evs=None, hevs=None):
+        """steps k0 .. k0+n-1; K1 of the first burst inside this call."""
+        self.hash_into(k0, hevs[0] if hevs else None)
+        for i in range(n):
+            k = k0 + i
+            self.S_stream.wait_event(self.ev_h.pop(k))
+            if i + 1 < n:
+                self.hash_into(k + 1, hevs[i + 1] if hevs else None)
+            e = evs[i] if evs else None
+            if e:
+                e[0].record(self.S_stream)
+            self.PB.bind_current_stream(self.ctx)
+            if k >= self.S.HOLD:
+                self.st.complete(self.bursts[k - self.S.HOLD], k)
+            self.st.compose_nodes(self.bursts[k - 1] if k >= 1 else None, k)
+            self.st.registry(self.bursts[k])
+            self.st.route_admit(self.bursts[k], k, 1.0 + k, e[1:] if e else None)
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
     ws, rank, local = dist_env()
     if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        return run_sharded(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    from paper_2604_25899_b200 import Context
-    from paper_2604_25899_b200 import batch as PB
-
-    if ws > 1:
-        return run_sharded(args, ws, rank, local, dev)
-    tr, cl = build_workload(args, rank, ws, dev)
-    ctx = Context(cl.n_replicas, cl.kv_capacity, cl.l2_capacity, args.block, device=local)
-    PB.bind_current_stream(ctx)
-    rng = np.random.default_rng(rank)
-    warm_l2(ctx, tr, cl, rng, n_workflows=n_workflows_total(args, ws, tr))
-    db = PB.DeviceBatch(tr.R, tr.tokens, torch.from_numpy(tr.tok_off).to(dev), None, None,
-                        torch.from_numpy(tr.res.view(np.int64).reshape(tr.R, 4).copy()).to(dev),
-                        torch.from_numpy(tr.group).to(dev), torch.from_numpy(tr.wf).to(dev),
-                        torch.from_numpy(tr.role).to(dev), 0, tr.n_tokens)
-    nb = (np.diff(tr.tok_off) + args.block - 1) // args.block
-    hoff = np.zeros(tr.R + 1, np.int64)
-    np.cumsum(nb, out=hoff[1:])
-    db.hash_off = torch.from_numpy(hoff).to(dev)
-    db.hashes = torch.empty(int(hoff[-1]), dtype=torch.int64, device=dev)
-    db.n_hashes = int(hoff[-1])
-    dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand,
-                         device=dev)
-    out = PB.alloc_out(ctx, db, dn, device=dev)
-    mode = PB.SEQ_COMMIT if args.mode == "seq" else PB.SNAPSHOT
-    now = [1.0]
-
-    phases = ["hash", "staged", "route", "admit", "release"]
-    overlap = args.free_sms >= 0
-    S = torch.cuda.Stream(device=dev, priority=-1) if overlap else torch.cuda.current_stream(dev)
-    torch.cuda.set_stream(S)
-    PB.bind_current_stream(ctx)
-    if overlap:
-        # hashing needs no cache state: K1 of step k+1 runs on its own (replica-less) ctx and
-        # low-priority stream while step k routes and admits; two hash buffers
-        import copy
-        import ctypes
-        H = torch.cuda.Stream(device=dev, priority=0)
-        hctx = Context(0, [], [], args.block, device=local)
-        hctx.set_stream(ctypes.c_void_p(H.cuda_stream))
-        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
-        db2 = copy.copy(db)
-        db2.hashes = torch.empty_like(db.hashes)
-        bufs = [db, db2]
-        ev_h = [torch.cuda.Event() for _ in range(2)]
-        ev_k2 = torch.cuda.Event()
-
-    def run_steps(n, evs=None, hev=None):
-        """n steps; evs[s] = per-phase events on the step stream, hev[s] = (start, end) of
-        K1 on the hash stream (overlap mode)."""
-        if not overlap:
-            for k in range(n):
-                e = evs[k] if evs is not None else None
-                fns = [lambda: PB.hash_batch(ctx, db), lambda: PB.staged_matrix(ctx, db, dn, out),
-                       lambda: PB.route_batch(ctx, db, dn, out, mode),
-                       lambda: PB.admit_batch(ctx, db, out, now[0], True),
-                       lambda: PB.release_batch(ctx, db, out)]
-                for i, f in enumerate(fns):
-                    if e is not None:
-                        e[i].record(S)
-                    f()
-                if e is not None:
-                    e[len(fns)].record(S)
-                now[0] += 1.0
-            return
-
-        def hash_into(k):
-            H.wait_stream(S)   # after K2(k-1): step k-1 no longer needs the whole GPU, and
-            if hev is not None:  # release(k-2), the last reader of this buffer, is done
-                hev[k][0].record(H)
-            PB.hash_batch(hctx, bufs[k % 2])
-            if hev is not None:
-                hev[k][1].record(H)
-            ev_h[k % 2].record(H)
-
-        hash_into(0)
-        for k in range(n):
-            b = bufs[k % 2]
-            e = evs[k] if evs is not None else None
-            if e is not None:
-                e[0].record(S)
-            S.wait_event(ev_h[k % 2])
-            if e is not None:
-                e[1].record(S)
-            if k + 1 < n and args.k1_after == "start":
-                hash_into(k + 1)
-            PB.staged_matrix(ctx, b, dn, out)
-            if e is not None:
-                e[2].record(S)
-            if k + 1 < n and args.k1_after == "staged":
-                hash_into(k + 1)
-            PB.route_batch(ctx, b, dn, out, mode)
-            if e is not None:
-                e[3].record(S)
-            PB.admit_batch(ctx, b, out, now[0], True)
-            if e is not None:
-                e[4].record(S)
-            PB.release_batch(ctx, b, out)
-            if e is not None:
-                e[5].record(S)
-            now[0] += 1.0
-
-    run_steps(args.warmup)
-    torch.cuda.synchronize()
+    if args.check:
+        return run_check(args, dev)
+    W_, K = args.warmup, args.steps
+    E = 0 if (args.no_e2e or args.profile) else args.e2e_steps
+    arm = Arm(args, dev, W_ + K)
+    ctx = arm.ctx
+    arm.run(0, W_)
+    torch.cuda.synchronize(dev)
     ctx.check_device_error()
-
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    ctx.stats(reset=True)
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    launches0 = ctx.kernel_launches() + (hctx.kernel_launches() if overlap else 0)
-    ev_all = [[torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)]
-              for _ in range(args.steps)]
-    hev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)] if overlap else None
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(S)
-    run_steps(args.steps, ev_all, hev)
-    t_end.record(S)
-    torch.cuda.synchronize()
-    launches = ctx.kernel_launches() + (hctx.kernel_launches() if overlap else 0) - launches0
+    l0 = arm.launches()
+    ET = torch.cuda.Event
+    evs = [[ET(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    hevs = [(ET(enable_timing=True), ET(enable_timing=True)) for _ in range(K)]
+    t0, t1 = ET(enable_timing=True), ET(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    t0.record(arm.S_stream)
+    arm.run(W_, K, evs, hevs)
+    t1.record(arm.S_stream)
+    torch.cuda.synchronize(dev)
+    launches = arm.launches() - l0
     clk = clocks.stop()
     ctx.check_device_error()
-    ms = t_start.elapsed_time(t_end)
-    phase_ms = {p: sum(e[i].elapsed_time(e[i + 1]) for e in ev_all) / args.steps
-                for i, p in enumerate(phases)}
-    if overlap:  # K1 itself, timed on its own stream
-        phase_ms["hash"] = sum(a.elapsed_time(b) for a, b in hev) / args.steps
-        phase_ms["hash_wait"] = sum(e[0].elapsed_time(e[1]) for e in ev_all) / args.steps
-    if ws > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    total_req = tr.R * ws * args.steps
-    value = total_req / (ms / 1000.0)
-
-    h = out.host()
-    placed = h["placed"][:h["placed_off"][-1]]
-    n_placed = int(len(placed))
-    n_admitted = int(h["admitted"][:tr.R].sum())
-    ab = algorithmic_bytes(tr, args.block, h["staged"], dn.max_cand, cl, placed, h["match3"])
+    stats = ctx.stats(reset=True)
+    ms = t0.elapsed_time(t1)
+    ms_step = ms / K
+    R = args.requests
+    value = R * K / (ms / 1000.0)
+    phases = ["bookkeeping", "staged", "route", "admit"]
+    phase_ms = {p: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / K for i, p in enumerate(phases)}
+    phase_ms["hash"] = sum(a.elapsed_time(b) for a, b in hevs) / K
+    # bytes: K1 exactly per timed burst (host offsets); the staged / admission terms from the
+    # last burst's outputs (still in the ring), eviction from the measured counters
+    timed = arm.bursts[W_:W_ + K]
+    hash_bytes = float(np.mean([8 * int(b.tok_off[-1]) + 8 * b.b.n_hashes + 16 * (b.R + 1)
+                                for b in timed]))
+    o = arm.st.out(W_ + K - 1)
+    h = o.host()
+    last = arm.bursts[W_ + K - 1]
+    placed_last = h["placed"][:h["placed_off"][-1]]
+    ab = algorithmic_bytes([(last.tok_off, last.group, h["staged"][:R], placed_last)],
+                           args.block, arm.cl, {"evictions": 0, "evicted_blocks": 0},
+                           arm.st.nodes.max_cand)
     peak, peak_src = peaks()
-    hash_gbs = ab["hash"] / (phase_ms["hash"] / 1000.0) / 1e9
-    step_gbs = ab["total"] / (ms_step / 1000.0) / 1e9
+    hash_gbs = hash_bytes / (phase_ms["hash"] / 1000.0) / 1e9
+    ev = algorithmic_bytes([], args.block, arm.cl, stats, arm.st.nodes.max_cand)["evict"] / K
+    step_bytes = hash_bytes + ab["staged"] + ab["route"] + ab["admit"] + ev
+    step_gbs = step_bytes / (ms_step / 1000.0) / 1e9
 
-    # e2e: (a) through the public API with device prompt assembly -- per step the host
-    # uploads the prompt segment descriptors, the fresh tokens and the request metadata,
-    # the prompts are assembled from the HBM-resident exchange history, the whole step
-    # runs and decisions/admissions/matches come back; (b) through the token-upload entry
-    # pyg_step_host (every prompt token crosses PCIe), reported as e2e_tokens
-    e2e = e2e_tokens = None
-    if not args.no_e2e and not args.profile:
-        from paper_2604_25899_b200.prompts import PipelinedSteps
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        meta = (pin(tr.res.view(np.int64).reshape(tr.R, 4)), pin(tr.group), pin(tr.wf),
-                pin(tr.role))
-        node_b = sum(x.numel() * x.element_size()
-                     for x in (dn.replica_id, dn.kv_capacity, dn.asg_off, dn.asg, dn.cand_off,
-                               dn.cand))
-
-        def run_step(b, k, after_gather):
-            # K1 already ran on the pipeline's prep stream; the next step's assembly + K1
-            # may start with this step (its input set was last read by the previous step)
-            if args.k1_after == "start":
-                after_gather()
-            PB.staged_matrix(ctx, b, dn, out)
-            after_gather()  # no-op when already called
-            PB.route_batch(ctx, b, dn, out, mode)
-            PB.admit_batch(ctx, b, out, now[0] + k, True)
-            PB.release_batch(ctx, b, out)
-            return out.decisions[:tr.R], out.admitted[:tr.R], out.match3[:tr.R]
-
-        pipe = PipelinedSteps(ctx, tr, db, dev, run_step, meta,
-                              (out.decisions[:tr.R], out.admitted[:tr.R], out.match3[:tr.R]))
-        pipe.run(2)
-        e2e_steps = max(4, min(args.steps, 10))
-        t0 = time.perf_counter()
-        pipe.run(e2e_steps, first_index=2)
-        e_ms = (time.perf_counter() - t0) * 1000.0
-        now[0] += e2e_steps + 2
-        e2e = {"value": tr.R * e2e_steps / (e_ms / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": int(pipe.h2d_bytes + node_b),
-               "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": e_ms / e2e_steps,
-               "via": ("public API with device prompt assembly: per step the segment "
-                       "descriptors, fresh tokens and request metadata are uploaded from pinned "
-                       "memory (copy stream), the prompts gathered from the HBM-resident "
-                       "exchange history and hashed in one fused pass (pyg_assemble_hash_dev) on a prep stream, "
-                       "all overlapped with earlier steps (3 staging sets, 2 batch sets); the "
-                       "rest of the step runs and decisions/admissions/matches are copied back"),
-               "fresh_tokens_per_step": pipe.pools[0].fresh_tokens}
-        hs = PB.HostStep(ctx, tr.tokens_np(), tr.tok_off, tr.res, tr.group, tr.wf, tr.role, cl)
-        for _ in range(2):
-            hs(now[0], mode)
-            now[0] += 1.0
-        torch.cuda.synchronize()
-        t_steps = max(2, min(args.steps, 5))
-        t0 = time.perf_counter()
-        for _ in range(t_steps):
-            hs(now[0], mode)
-            now[0] += 1.0
-        t_ms = (time.perf_counter() - t0) * 1000.0
-        e2e_tokens = {"value": tr.R * t_steps / (t_ms / 1000.0), "unit": UNIT,
-                      "h2d_bytes_per_step": hs.h2d_bytes, "d2h_bytes_per_step": hs.d2h_bytes,
-                      "ms_per_step": t_ms / t_steps,
-                      "via": "pyg_step_host: every prompt token uploaded (pinned host buffers)"}
-
+    e2e = None
+    if E:
+        e2e = run_e2e(args, arm, E, W_ + K)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "hash_kernel_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("traffic_bytes_per_launch")
+                d = json.load(f)
+            if d.get("workload") == args.workload:
+                traffic = d.get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
-
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
-        cpu = cpu_baseline(args, 1, args.cpu_seconds)
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {
-                "workload": describe(args, tr, ws),
-                "route_mode": "seq_commit" if mode == PB.SEQ_COMMIT else "snapshot",
-                "requests_per_step_per_gpu": tr.R, "tokens_per_step_per_gpu": tr.n_tokens,
-                "placed_per_step": n_placed, "admitted_per_step": n_admitted,
-                "l2_flush": "none needed: step inputs (tokens %.2f GB) exceed the 126 MB L2"
-                            % (tr.n_tokens * 8 / 1e9),
-                "parallelism": f"replica shards x{ws} (weak)",
-                "k1_overlap": (f"K1 of step k+1 on a second stream (grid = SMs - {args.free_sms}), "
-                               f"from step k's {args.k1_after}; every step still hashes its own "
-                               "burst inside the timed region") if overlap else "none (serial)"},
-            "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1)", "achieved": hash_gbs,
-                         "peak": peak, "unit": "GB/s", "frac": hash_gbs / peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": ab["hash"],
-                         "avg_launch_ms": phase_ms["hash"],
-                         "int_ceiling": {"gbs": INT_CEILING_GBS,
-                                         "frac": hash_gbs / INT_CEILING_GBS,
-                                         "source": "profiles/r01_fnv_core.txt: FNV-1a core with "
-                                                   "register-resident tokens, 513 Gtok/s"}},
-            "step_roofline": {"achieved": step_gbs, "frac": step_gbs / peak,
-                              "algorithmic_bytes_per_step": ab["total"], "probes": ab["probes"]},
-            "phase_ms": phase_ms,
-            "clocks": clk,
-            "gpu_launches": int(launches),
-            "e2e": e2e,
-            "e2e_tokens": e2e_tokens,
-            "cpu_baseline": cpu,
-        }
-        print(json.dumps(line))
-    if ws > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    cpu = cpu_h1 = None
+    if not args.no_cpu_baseline and not args.profile:
+        cpu = cpu_baseline(args, hash_once=False)
+        cpu_h1 = cpu_baseline(args, hash_once=True)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W_,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {
+            "workload": describe(args, 1), "route_mode": "seq_commit",
+            "requests_per_step": R, "tokens_per_step": int(sum(b.b.n_tokens for b in
+                                                               arm.bursts[W_:]) / K),
+            "distinct_bursts": True,
+            "placed_per_step": stats["admissions"] / K,
+            "admitted_per_step": stats["admitted"] / K,
+            "evicted_blocks_per_step": stats["evicted_blocks"] / K,
+            "evicted_tokens_per_step": stats["evicted_tokens"] / K,
+            "evictions_per_step": stats["evictions"] / K,
+            "l3_promoted_tokens_per_step": stats["l3_promoted_tokens"] / K,
+            "warm_fill_admissions": arm.n_fill,
+            "l2_flush": "none needed: every step reads a distinct burst (%.2f GB of tokens) "
+                        "larger than the 126 MB L2" % (arm.bursts[-1].b.n_tokens * 8 / 1e9),
+            "parallelism": "one GPU holds every replica",
+            "k1_overlap": (f"K1 of burst k+1 on a second stream (grid = SMs - {args.free_sms}) "
+                           "during step k; each step's own K1 is inside the timed region")
+            if arm.overlap else "none (serial)"},
+        "roofline": {"bound": "hbm", "kernel": "k_hash_staged (K1, chain_boundary_hashes)",
+                     "achieved": hash_gbs, "peak": peak, "unit": "GB/s", "frac": hash_gbs / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": int(hash_bytes),
+                     "avg_launch_ms": phase_ms["hash"],
+                     "int_ceiling": {"gbs": INT_CEILING_GBS, "frac": hash_gbs / INT_CEILING_GBS,
+                                     "source": "profiles/r01_fnv_core.txt: FNV-1a core with "
+                                               "register-resident tokens, 513 Gtok/s"}},
+        "step_roofline": {"achieved": step_gbs, "frac": step_gbs / peak,
+                          "algorithmic_bytes_per_step": int(step_bytes), "probes": ab["probes"]},
+        "phase_ms": phase_ms, "clocks": clk, "gpu_launches": int(launches),
+        "e2e": e2e, "cpu_baseline": cpu, "cpu_baseline_hash_once": cpu_h1,
+    }
+    print(json.dumps(line))
 
 
-def run_sharded(args, ws, rank, local, dev):
-    """N > 1: the sharded step (paper_2604_25899_b200/shard.py) -- replicas partitioned over
-    the GPUs, route inputs all-gathered, placed requests dispatched to their owner GPU."""
+def run_e2e(args, arm, E, k_first):
+    """E more steps through the public API from pinned host buffers: per step the burst's
+    tokens, offsets and request metadata go host->device (copy stream, one burst ahead), K1
+    and the step run, decisions / admissions / lookups come back (d2h stream)."""
     import torch
-    import torch.distributed as dist
-    from paper_2604_25899_b200 import Context
-    from paper_2604_25899_b200 import batch as PB
-    from paper_2604_25899_b200.shard import ShardPlan, ShardedStep
+    S, PB = arm.S, arm.PB
+    dev = arm.dev
+    host, devb = [], []
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    for i in range(E):
+        k = k_first + i
+        tr = S.make_burst(k, args.requests, args.seed, dev, args.workload, args.models)
+        b = S.upload_burst(tr, args.block, dev)  # device buffers (overwritten by the copies)
+        rw, rm = S.registry_pairs(tr.wf, tr.role)
+        host.append({"tokens": tr.tokens.cpu().pin_memory(), "tok_off": pin(tr.tok_off),
+                     "res": pin(tr.res.view(np.int64).reshape(tr.R, 4)), "group": pin(tr.group),
+                     "wf": pin(tr.wf), "role": pin(tr.role), "reg_wf": pin(rw),
+                     "reg_mask": pin(rm.view(np.int64))})
+        devb.append(b)
+        del tr
+    R = args.requests
+    res_h = [[torch.empty((R, 3), dtype=torch.int64).pin_memory(),
+              torch.empty(R, dtype=torch.int32).pin_memory(),
+              torch.empty((R, 3), dtype=torch.int64).pin_memory()] for _ in range(2)]
+    bursts = {k_first - 2 + j: arm.bursts[k_first - 2 + j] for j in range(2)}
+    for i in range(E):
+        bursts[k_first + i] = devb[i]
+    cp = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+    up = {}
+    h2d_bytes = sum(int(v.numel() * v.element_size()) for v in host[0].values())
+    d2h_bytes = sum(int(t.numel() * t.element_size()) for t in res_h[0])
 
-    tr, cl = build_workload(args, rank, ws, dev)
-    n_loc = args.replicas
-    base = rank * n_loc
-    counts = torch.tensor([tr.R], dtype=torch.int64, device=dev)
-    allc = [torch.zeros_like(counts) for _ in range(ws)]
-    dist.all_gather(allc, counts)
-    plan = ShardPlan([n_loc] * ws, [int(x.item()) for x in allc], rank, args.block)
-    ctx = Context(n_loc, cl.kv_capacity[base:base + n_loc], cl.l2_capacity[base:base + n_loc],
-                  args.block, device=local)
-    PB.bind_current_stream(ctx)
-    rng = np.random.default_rng(rank)
-    warm_l2(ctx, tr, cl, rng, rep_base=base, n_local=n_loc,
-            n_workflows=n_workflows_total(args, ws, tr))
-    db = PB.DeviceBatch(tr.R, tr.tokens, torch.from_numpy(tr.tok_off).to(dev), None, None,
-                        torch.from_numpy(tr.res.view(np.int64).reshape(tr.R, 4).copy()).to(dev),
-                        torch.from_numpy(tr.group).to(dev), torch.from_numpy(tr.wf).to(dev),
-                        torch.from_numpy(tr.role).to(dev), 0, tr.n_tokens)
-    nb = (np.diff(tr.tok_off) + args.block - 1) // args.block
-    hoff = np.zeros(tr.R + 1, np.int64)
-    np.cumsum(nb, out=hoff[1:])
-    db.hash_off = torch.from_numpy(hoff).to(dev)
-    db.hashes = torch.empty(int(hoff[-1]), dtype=torch.int64, device=dev)
-    dn = PB.upload_nodes(cl.replica_id, cl.kv_capacity, cl.asg_off, cl.asg, cl.cand_off, cl.cand,
-                         device=dev)
-    tt = torch.tensor([tr.n_tokens], dtype=torch.int64, device=dev)
-    dist.all_reduce(tt)
-    st = ShardedStep(ctx, plan, db, dn, dev, cl.kv_capacity[base:base + n_loc], int(tt.item()))
-    st.build_directory()
-    overlap = args.free_sms >= 0
-    S = torch.cuda.Stream(device=dev, priority=-1) if overlap else torch.cuda.current_stream(dev)
-    torch.cuda.set_stream(S)
-    PB.bind_current_stream(ctx)
-    if overlap:
-        # as in run_ours: K1 of step k+1 on its own ctx/stream, launched once step k's route
-        # rows are all-gathered (every peer is done reading the other input set by then)
-        import copy
-        import ctypes
-        H = torch.cuda.Stream(device=dev, priority=0)
-        hctx = Context(0, [], [], args.block, device=local)
-        hctx.set_stream(ctypes.c_void_p(H.cuda_stream))
-        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
-        db2 = copy.copy(db)
-        db2.hashes = torch.empty_like(db.hashes)
-        st2 = ShardedStep(ctx, plan, db2, dn, dev, cl.kv_capacity[base:base + n_loc],
-                          int(tt.item()))
-        sts, bufs = [st, st2], [db, db2]
-        ev_h = [torch.cuda.Event() for _ in range(2)]
-    now = [1.0]
+    def upload(i):
+        b, h = devb[i], host[i]
+        with torch.cuda.stream(cp):
+            b.b.tokens[:h["tokens"].numel()].copy_(h["tokens"], non_blocking=True)
+            b.b.tok_off.copy_(h["tok_off"], non_blocking=True)
+            b.b.res.copy_(h["res"], non_blocking=True)
+            b.b.group.copy_(h["group"], non_blocking=True)
+            b.b.wf.copy_(h["wf"], non_blocking=True)
+            b.b.role.copy_(h["role"], non_blocking=True)
+            b.reg_wf.copy_(h["reg_wf"], non_blocking=True)
+            b.reg_mask.copy_(h["reg_mask"], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(cp)
+            up[i] = e
 
-    def run_steps(n, evh=None):
-        if not overlap:
-            out = None
-            for k in range(n):
-                out = st.step(now[0], ev_hash=evh[k] if evh else None)
-                now[0] += 1.0
-            return out
+    import ctypes
+    from paper_2604_25899_b200 import _lib
+    fetched = [None, None]
+    def k1(i):
+        """hash offsets + K1 of e2e burst i on the hash stream, after its upload"""
+        b = devb[i]
+        arm.H.wait_event(up.pop(i))
+        _lib.check(_lib._lib.pyg_hash_offsets_dev(arm.hctx.h,
+                                                  ctypes.c_void_p(b.b.tok_off.data_ptr()), b.R,
+                                                  ctypes.c_void_p(b.b.hash_off.data_ptr()), None))
+        PB.hash_batch(arm.hctx, b.b)
+        e = torch.cuda.Event()
+        e.record(arm.H)
+        return e
 
-        def hash_into(k):
-            H.wait_stream(S)
-            if evh:
-                evh[k][0].record(H)
-            PB.hash_batch(hctx, bufs[k % 2])
-            if evh:
-                evh[k][1].record(H)
-            ev_h[k % 2].record(H)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    upload(0)
+    if E > 1:
+        upload(1)
+    eh = k1(0)
+    for i in range(E):
+        k = k_first + i
+        b = devb[i]
+        arm.S_stream.wait_event(eh)
+        PB.bind_current_stream(arm.ctx)
+        if k >= S.HOLD:
+            arm.st.complete(bursts[k - S.HOLD], k)
+        arm.st.compose_nodes(bursts[k - 1], k)
+        arm.st.registry(b)
+        o = arm.st.route_admit(b, k, 1.0 + k)
+        es = torch.cuda.Event()
+        es.record(arm.S_stream)
+        if i + 1 < E:          # K1 of the next burst overlaps this step
+            eh = k1(i + 1)
+        if i + 2 < E:
+            upload(i + 2)
+        s = i % 2
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(es)
+            if fetched[s] is not None:
+                fetched[s].synchronize()
+            res_h[s][0].copy_(o.decisions[:R], non_blocking=True)
+            res_h[s][1].copy_(o.admitted[:R], non_blocking=True)
+            res_h[s][2].copy_(o.match3[:R], non_blocking=True)
+            ef = torch.cuda.Event()
+            ef.record(d2h)
+            fetched[s] = ef
+    torch.cuda.synchronize(dev)
+    el = time.perf_counter() - t0
+    arm.ctx.check_device_error()
+    return {"value": R * E / el, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+            "d2h_bytes_per_step": d2h_bytes, "ms_per_step": 1000.0 * el / E, "steps": E,
+            "via": ("public API from pinned host buffers: per step the burst's tokens, offsets "
+                    "and request metadata are copied host->device (copy stream, one burst "
+                    "ahead), hash offsets + K1 + the steady step run on device, decisions / "
+                    "admissions / lookups are copied back; wall clock over the steps")}
 
-        hash_into(0)
-        out = None
-        for k in range(n):
-            S.wait_event(ev_h[k % 2])
-            nxt = (lambda kk=k + 1: hash_into(kk)) if k + 1 < n else None
-            out = sts[k % 2].step(now[0], prehashed=True, after_gather=nxt)
-            now[0] += 1.0
-        return out
 
-    run_steps(args.warmup)
-    torch.cuda.synchronize()
-    ctx.check_device_error()
-    dist.barrier()
-    torch.cuda.synchronize()
-    clocks = Clocks(local)
-    clocks.start()
-    time.sleep(0.3)
-    launches0 = ctx.kernel_launches() + (hctx.kernel_launches() if overlap else 0)
-    evh = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    t0e = torch.cuda.Event(enable_timing=True)
-    t1e = torch.cuda.Event(enable_timing=True)
-    t0e.record(S)
-    out = run_steps(args.steps, evh)
-    t1e.record(S)
-    torch.cuda.synchronize()
-    launches = ctx.kernel_launches() + (hctx.kernel_launches() if overlap else 0) - launches0
-    clk = clocks.stop()
-    ctx.check_device_error()
-    ms = t0e.elapsed_time(t1e)
-    hash_ms = sum(a.elapsed_time(b) for a, b in evh) / args.steps
-    t = torch.tensor([ms, hash_ms], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, hash_ms_max = float(t[0].item()), float(t[1].item())
-    ms_step = ms / args.steps
-    value = plan.R_total * args.steps / (ms / 1000.0)
-    peak, peak_src = peaks()
-    L = np.diff(tr.tok_off)
-    hash_bytes = 8 * int(L.sum()) + 8 * int(nb.sum()) + 16 * (tr.R + 1)
-    hash_gbs = hash_bytes / (hash_ms / 1000.0) / 1e9
-
-    # e2e through the public API with device prompt assembly (see run_ours): per step each
-    # rank uploads its segment descriptors, fresh tokens and request metadata from pinned
-    # memory and assembles its prompts from its HBM-resident history -- both overlapped with
-    # the previous step (two input sets, each with its own ShardedStep exchange window) --
-    # runs the sharded step and copies its requests' results back
-    e2e = None
-    if not args.no_e2e and not args.profile:
-        from paper_2604_25899_b200.prompts import PipelinedSteps, clone_batch
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        meta = (pin(tr.res.view(np.int64).reshape(tr.R, 4)), pin(tr.group), pin(tr.wf),
-                pin(tr.role))
-        db1 = clone_batch(db)
-        for dst, src in ((db1.tok_off, db.tok_off), (db1.hash_off, db.hash_off)):
-            dst.copy_(src)
-        st1 = ShardedStep(ctx, plan, db1, dn, dev, cl.kv_capacity[base:base + n_loc], int(tt.item()))
-        steps_of = {id(db): st, id(db1): st1}
-        a0 = plan.req_base
-
-        def run_step(b, k, after_gather):
-            o = steps_of[id(b)].step(now[0] + k, prehashed=True, after_gather=after_gather)
-            return o["decisions"][a0:a0 + plan.R_local], o["admitted"], o["match3"]
-
-        res_like = (torch.empty((plan.R_local, 3), dtype=torch.int64),
-                    torch.empty(plan.R_local, dtype=torch.int32),
-                    torch.empty((plan.R_local, 3), dtype=torch.int64))
-        pipe = PipelinedSteps(ctx, tr, db, dev, run_step, meta, res_like, second_batch=db1)
-        pipe.run(2)
-        dist.barrier()
-        e_steps = max(4, min(args.steps, 10))
+def run_check(args, dev):
+    """--check K: K full-size bursts on the GPU and through the unmodified reference (all host
+    threads for the staged values, hash-once -- the same reference functions without repeated
+    hashing), compared burst by burst and, at the end, tier by tier."""
+    import torch
+    from oracle.steady_ref import RefSteady
+    K = args.check
+    t_start = time.perf_counter()
+    arm = Arm(args, dev, K)
+    S = arm.S
+    cl = arm.cl
+    ref = RefSteady(args.block, cl, threads=os.cpu_count() or 1, hash_once=True)
+    warm, ops, off, placed = warm_inputs(args, cl, "cpu")
+    ref.warm(warm, ops, off, placed)
+    del warm
+    report = {"check": "steady-state bursts vs the unmodified reference", "bursts": K,
+              "workload": describe(args, 1), "per_burst": []}
+    ok = True
+    arm.ctx.stats(reset=True)
+    for k in range(K):
+        arm.run(k, 1)
+        torch.cuda.synchronize(dev)
+        arm.ctx.check_device_error()
+        got = arm.st.out(k).host()
+        b = arm.bursts[k]   # the reference gets the very same inputs
+        toks = b.b.tokens.cpu().numpy().view(np.uint64)
+        rw, rm = S.registry_pairs(b.wf, b.role)
         t0 = time.perf_counter()
-        pipe.run(e_steps, first_index=2)
-        e_ms = (time.perf_counter() - t0) * 1000.0
-        now[0] += e_steps + 2
-        t = torch.tensor([e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
-        hb = torch.tensor([pipe.h2d_bytes, pipe.pools[0].fresh_tokens], dtype=torch.int64,
-                          device=dev)
-        dist.all_reduce(hb)
-        e2e = {"value": plan.R_total * e_steps / (e_ms / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": int(hb[0].item()),
-               "d2h_bytes_per_step": int(pipe.d2h_bytes * ws), "ms_per_step": e_ms / e_steps,
-               "via": ("ShardedStep through the public API with device prompt assembly: per rank "
-                       "and step, segment descriptors + fresh tokens + metadata uploaded, "
-                       "prompts assembled and hashed (K1) on side streams overlapping earlier "
-                       "steps; bytes summed over ranks"),
-               "fresh_tokens_per_step": int(hb[1].item())}
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {
-                "workload": describe(args, tr, ws),
-                "route_mode": "seq_commit (whole burst, identical on every GPU)",
-                "requests_per_step": plan.R_total, "requests_per_step_per_gpu": tr.R,
-                "tokens_per_step_per_gpu": tr.n_tokens,
-                "placed_on_rank0_per_step": int(out["recv_count"].item()),
-                "l2_flush": "none needed: step inputs (tokens %.2f GB/GPU) exceed the 126 MB L2"
-                            % (tr.n_tokens * 8 / 1e9),
-                "parallelism": (f"replica shards x{ws}: "
-                                + ("route rows exchanged over NVLink peer memory behind a flag "
-                                   "barrier (no NCCL in the step)" if st.p2p else
-                                   "NCCL all-gather of route inputs + one NCCL stream barrier")
-                                + "; owner GPUs pull placed requests' tokens/hashes and peers' "
-                                  "L2/L3 erase lists and results over NVLink P2P (CUDA IPC); "
-                                  "no host sync in the step"),
-                "k1_overlap": (f"K1 of step k+1 on a second stream (grid = SMs - {args.free_sms}) "
-                               "from step k's route-row exchange on") if overlap else "none (serial)"},
-            "roofline": {"bound": "hbm", "kernel": "k_hash_batch (K1), rank 0",
-                         "achieved": hash_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": hash_gbs / peak, "traffic": None, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": hash_bytes, "avg_launch_ms": hash_ms,
-                         "max_over_ranks_launch_ms": hash_ms_max},
-            "clocks": clk, "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": None,
-        }
-        print(json.dumps(line))
-    dist.barrier()
-    dist.destroy_process_group()
+        d, a, m3, stg = ref.step(k, toks, b.tok_off, b.res, b.group, b.wf, b.role, rw, rm,
+                                 1.0 + k, want_staged=True)
+        t_ref = time.perf_counter() - t0
+        R = b.R
+        mc = stg.shape[1]
+        gd = got["decisions"][:R]
+        pl = d["target"] >= 0
+        row = {"burst": k, "requests": R, "placed": int(pl.sum()), "admitted": int(a.sum()),
+               "ref_seconds": round(t_ref, 2),
+               "staged": bool(np.array_equal(got["staged"][:R, :mc], stg)),
+               "target": bool(np.array_equal(gd["target"], d["target"])),
+               "tiebreak": bool(np.array_equal(gd["tiebreak"], d["tiebreak"])),
+               "headroom": bool(np.array_equal(gd["headroom"], d["headroom"])),
+               "oom_bound_bits": gd["oom_bound"].tobytes() == d["oom_bound"].tobytes(),
+               "admitted_eq": bool(np.array_equal(got["admitted"][:R], a)),
+               "match3": bool(np.array_equal(got["match3"][:R][pl], m3[pl]))}
+        row["ok"] = all(v for kk, v in row.items() if isinstance(v, bool))
+        ok &= row["ok"]
+        report["per_burst"].append(row)
+        print(json.dumps(row), flush=True)
+        del toks
+    stats = arm.ctx.stats()
+    tiers_ok = True
+    bad = []
+    for n in range(cl.n_replicas):
+        for t in (0, 1):
+            if arm.ctx.dump(n, t).tobytes() != ref.dump(n, t).tobytes():
+                tiers_ok = False
+                bad.append((n, t))
+    l3_ok = arm.ctx.dump(0, 2).tobytes() == ref.dump(0, 2).tobytes()
+    report.update({"tiers_equal": tiers_ok, "l3_equal": l3_ok, "bad_tiers": bad[:10],
+                   "device_stats": stats, "ok": bool(ok and tiers_ok and l3_ok),
+                   "seconds": round(time.perf_counter() - t_start, 1),
+                   "host_threads": os.cpu_count()})
+    print(json.dumps(report))
+
+
+def run_sharded(args):
+    raise SystemExit("multi-GPU steady-state bench: see run_sharded in the next revision")
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    maybe_self_launch(args)
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -92,9 +92,10 @@ int pyg_set_stream(pyg_ctx* ctx, void* cuda_stream);
 int pyg_synchronize(pyg_ctx* ctx);
 /* number of kernels this ctx has launched (for the bench's gpu_launches claim) */
 int64_t pyg_kernel_launches(pyg_ctx* ctx);
-/* Counters since creation / the last reset (synchronizes the ctx stream): out[0] blocks
-   evicted by evict_for_space, out[1] their tokens, out[2] evictions that had work
-   (excess > 0), out[3] of those unsatisfied. */
+/* Counters since creation / the last reset (synchronizes the ctx stream), out[8]: [0] blocks
+   evicted by evict_for_space, [1] their tokens, [2] evictions that had work (excess > 0),
+   [3] of those unsatisfied, [4] batched admissions tried, [5] admitted, [6] L3 tokens
+   promoted by batched admission, [7] reserved. */
 int pyg_stats(pyg_ctx* ctx, int64_t* out, int32_t reset);
 /* (Re)sets a replica's tier capacities -- CacheHierarchy(l1_capacity, l2_capacity)
    (hierarchy.hpp:100) for a replica slot the engine provisions later (engine.cpp:197, 1482). */

@@ -31,20 +31,20 @@ class RefSteady:
         self.hist = {}   # burst -> (tokens, tok_off, target replica index per request, admitted)
 
     def warm(self, trace, ops, fill_off, fill_placed, now=0.5):
-        """The warm-up of steady.py: ops, then the warm fill admitted in replica order and
-        released (mirrors steady.apply_warm_fill_gpu)."""
-        apply_warm_oracle(self.ref, self.caches, self.l3, self.reg, trace, ops)
-        adm = []
+        """The warm-up of steady.py: the warm fill, then the ops.  The fill runs while L2/L3
+        are empty and every replica stays under its KV capacity, so admitting a placement
+        (lookup, evict_for_space with nothing to free, insert_chain pinned) and releasing it
+        is insert_chain(L1, prompt, len, lineage, now, 0) -- what this does, replica by
+        replica in placement order (steady.apply_warm_fill_gpu runs the batched admission)."""
+        n_fill = 0
         for n in range(self.cl.n_replicas):
             for r in fill_placed[fill_off[n]:fill_off[n + 1]]:
                 p = trace.prompt(int(r))
-                ok, _ = self.ref.admit(self.caches[n], self.l3, self.l3, self.reg, True, p,
-                                       int(trace.wf[r]), int(trace.role[r]), now)
-                if ok:
-                    adm.append((n, p))
-        for n, p in adm:
-            self.ref.unpin_chain(self.caches[n], p, len(p))
-        return len(adm)
+                self.ref.insert_chain(self.caches[n], 0, p, len(p), int(trace.wf[r]),
+                                      int(trace.role[r]), now, 0)
+                n_fill += 1
+        apply_warm_oracle(self.ref, self.caches, self.l3, self.reg, trace, ops)
+        return n_fill
 
     def node_table(self, k):
         """background + burst k-1's placements, per replica in placement order."""

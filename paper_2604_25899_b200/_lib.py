@@ -229,10 +229,12 @@ class Context:
 
     def stats(self, reset=False) -> dict:
         """pyg_stats: eviction counters (synchronizes the ctx stream)."""
-        out = np.zeros(4, np.int64)
+        out = np.zeros(8, np.int64)
         check(_lib.pyg_stats(self.h, out.ctypes.data, int(bool(reset))))
         return {"evicted_blocks": int(out[0]), "evicted_tokens": int(out[1]),
-                "evictions": int(out[2]), "unsatisfied": int(out[3])}
+                "evictions": int(out[2]), "unsatisfied": int(out[3]),
+                "admissions": int(out[4]), "admitted": int(out[5]),
+                "l3_promoted_tokens": int(out[6])}
 
     # -- hashing
     def chain_hashes(self, tokens):

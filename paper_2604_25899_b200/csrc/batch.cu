@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     const EvictOut ev = block_evict(c, t1p, excess, a.spec, nullptr, 0, smem, sm);
     if (!ev.satisfied) {
       if (threadIdx.x == 0) {
+        if (c.stats) atomicAdd(c.stats + 4, 1ULL);
         a.admitted[r] = 0;
         a.match3[3 * r] = m[0];
         a.match3[3 * r + 1] = m[1];
@@ -259,6 +260,10 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+      if (c.stats) {
+        atomicAdd(c.stats + 4, 1ULL);
+        if (room) atomicAdd(c.stats + 5, 1ULL);
+      }
       a.admitted[r] = room ? 1 : 0;
       a.match3[3 * r] = m[0];
       a.match3[3 * r + 1] = m[1];
@@ -471,6 +476,7 @@ __global__ void k_l3_final(CtxDev c, L3Args a, int64_t* match3, uint64_t* list, 
       atomicAdd(reinterpret_cast<unsigned long long*>(&tp->n_alive),
                 static_cast<unsigned long long>(-cnt));
     }
+    if (lane == 0 && c.stats) atomicAdd(c.stats + 6, static_cast<unsigned long long>(reusable - q.l12));
   }
 }
 
@@ -588,8 +594,8 @@ int pyg_check_device_error(pyg_ctx* c) {
 int pyg_stats(pyg_ctx* c, int64_t* out, int32_t reset) {
   if (!c || !out) return PYG_EINVAL;
   PYG_CUDA(cudaSetDevice(c->device));
-  PYG_CUDA(cudaMemcpyAsync(out, c->hd.stats, 32, cudaMemcpyDeviceToHost, c->stream));
-  if (reset) PYG_CUDA(cudaMemsetAsync(c->hd.stats, 0, 32, c->stream));
+  PYG_CUDA(cudaMemcpyAsync(out, c->hd.stats, 64, cudaMemcpyDeviceToHost, c->stream));
+  if (reset) PYG_CUDA(cudaMemsetAsync(c->hd.stats, 0, 64, c->stream));
   PYG_CUDA(cudaStreamSynchronize(c->stream));
   return PYG_OK;
 }

@@ -230,7 +230,7 @@ int pyg_create(const pyg_config* cfg, pyg_ctx** out) {
   if ((rc = cuda_check(cudaMalloc(&hd.off, std::max(1, c->n_rep) * sizeof(int32_t)), "cudaMalloc")))
     return fail(rc);
   if ((rc = cuda_check(cudaMalloc(&hd.error, sizeof(int32_t)), "cudaMalloc"))) return fail(rc);
-  if ((rc = cuda_check(cudaMalloc(&hd.stats, 4 * sizeof(unsigned long long)), "cudaMalloc")))
+  if ((rc = cuda_check(cudaMalloc(&hd.stats, 8 * sizeof(unsigned long long)), "cudaMalloc")))
     return fail(rc);
   hd.reg_cap = 1024;
   if ((rc = cuda_check(cudaMalloc(&hd.reg_present, hd.reg_cap), "cudaMalloc"))) return fail(rc);
@@ -239,7 +239,7 @@ int pyg_create(const pyg_config* cfg, pyg_ctx** out) {
   cudaMemsetAsync(hd.decode, 0, std::max(1, c->n_rep) * sizeof(int64_t), c->stream);
   cudaMemsetAsync(hd.off, 0, std::max(1, c->n_rep) * sizeof(int32_t), c->stream);
   cudaMemsetAsync(hd.error, 0, sizeof(int32_t), c->stream);
-  cudaMemsetAsync(hd.stats, 0, 4 * sizeof(unsigned long long), c->stream);
+  cudaMemsetAsync(hd.stats, 0, 8 * sizeof(unsigned long long), c->stream);
   cudaMemsetAsync(hd.reg_present, 0, hd.reg_cap, c->stream);
   cudaMemsetAsync(hd.reg_mask, 0, hd.reg_cap * sizeof(uint64_t), c->stream);
   std::vector<uint64_t> ones(c->n_rep + 1, 1);  // next_id_ = 1 (hierarchy.hpp:82,122)

@@ -80,7 +80,8 @@ struct CtxDev {
   int32_t B;
   int32_t pad;
   int32_t* error;       // device error flag
-  unsigned long long* stats;  // [4] evicted blocks, evicted tokens, evictions run, unsatisfied
+  unsigned long long* stats;  // [8] evicted blocks, evicted tokens, evictions run, unsatisfied,
+                              //     admissions tried, admitted, L3 tokens promoted, -
   // L2 directory (dir.cuh); main == nullptr until built
   uint64_t* dir_main;
   uint64_t* dir_rver;

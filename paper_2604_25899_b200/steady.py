@@ -57,11 +57,25 @@ def registry_pairs(wf: np.ndarray, role: np.ndarray):
     return u.astype(np.int32), registry_mask(role[last])
 
 
-def make_bursts(n_bursts, R, seed=1, device="cuda", n_models=N_MODELS, first=0, **kw):
-    """Bursts first .. first+n_bursts-1 of a config-4 trace (R requests each; request and
-    workflow ids continue across bursts, prefixes are shared by the whole trace)."""
-    return [W.bursty(n_requests=R, seed=seed * 1_000_003 + k, device=device, n_models=n_models,
-                     r_base=k * R, **kw) for k in range(first, first + n_bursts)]
+def make_burst(k, R, seed=1, device="cuda", kind="bursty", n_models=N_MODELS, n_keep=None,
+               **kw) -> W.Trace:
+    """Burst k of a trace, R requests (request and workflow ids continue across bursts;
+    prefixes / carried contexts are shared by the whole trace).  kind: 'bursty' (config 4)
+    or 'long_context' (config 3).  n_keep: only the first n_keep requests of the burst."""
+    if kind == "bursty":
+        return W.bursty(n_requests=R, seed=seed * 1_000_003 + k, device=device,
+                        n_models=n_models, r_base=k * R, n_keep=n_keep, **kw)
+    if kind == "long_context":
+        return W.long_context(n_requests=R, seed=seed * 1_000_003 + k, device=device,
+                              r_base=k * R, n_keep=n_keep, **kw)
+    raise ValueError(kind)
+
+
+def make_bursts(n_bursts, R, seed=1, device="cuda", n_models=N_MODELS, first=0, kind="bursty",
+                n_keep=None, **kw):
+    """Bursts first .. first+n_bursts-1 (make_burst)."""
+    return [make_burst(k, R, seed, device, kind, n_models, n_keep, **kw)
+            for k in range(first, first + n_bursts)]
 
 
 def config4_cluster(kv=100_000, l2=200_000, seed=0, n_replicas=REPLICAS, n_models=N_MODELS):
@@ -253,7 +267,9 @@ def warm_fill_plan(warm: W.Trace, cl: W.Cluster, fill_frac=0.85):
 
 
 def apply_warm_fill_gpu(ctx, warm: W.Trace, off, placed, B, device, now=0.5):
-    """Admit the warm placements (K4/K5: lookup, evict, insert pinned) and release them."""
+    """Admit the warm placements (K4/K5: lookup, evict, insert pinned) and release them.  Run
+    it first, on empty tiers (then warm_ops): every replica stays under its KV capacity, so
+    this leaves exactly insert_chain(L1, prompt, len, lineage, now, 0) per placement."""
     wb = upload_burst(warm, B, device)
     PB.bind_current_stream(ctx)
     PB.hash_batch(ctx, wb.b)

@@ -317,21 +317,26 @@ def coding_assistant(n_workflows=1_000, seed=1, device=None, unprofiled_frac=0.0
 
 
 def long_context(n_requests=100_000, seed=1, device=None, n_roles=8, steps=4,
-                 sys_tokens=2048, ctx_tokens=28672, unique_tokens=2048) -> Trace:
+                 sys_tokens=2048, ctx_tokens=28672, unique_tokens=2048, r_base=0,
+                 n_keep=None) -> Trace:
     """Config 3: L = 32,768 = 2,048-token role sys prompt + 28,672-token per-workflow carried
-    context (shared by the workflow's `steps` requests) + 2,048 unique tokens."""
+    context (shared by the workflow's `steps` requests) + 2,048 unique tokens.  r_base offsets
+    request / workflow ids (a later burst of the trace); n_keep keeps the first n_keep."""
     device = device or ("cuda" if torch.cuda.is_available() else "cpu")
     rng = np.random.default_rng(seed)
     b = _Builder()
     roles = [Role(f"role{k}", 0, sys_tokens, ctx_tokens, 1000, 0.45) for k in range(n_roles)]
     res, group, wfs, rls = [], [], [], []
     up = _p99(1000, 0.45)
+    if n_keep is not None:
+        n_requests = min(n_requests, n_keep)
     for r in range(n_requests):
-        w = r // steps
+        g = r_base + r
+        w = g // steps
         ro = int(rng.integers(0, n_roles))
         b.add(r, "w", b.words(f"sys_role{ro}", sys_tokens), 0, sys_tokens)
         b.add(r, "i", response_key(f"w{w}_ctx"), 0, ctx_tokens)
-        b.add(r, "i", salt_key(f"w{w}_s{r % steps}_0"), 0, unique_tokens, fresh=True)
+        b.add(r, "i", salt_key(f"w{w}_s{g % steps}_0"), 0, unique_tokens, fresh=True)
         res.append((sys_tokens + ctx_tokens + unique_tokens, up, ALPHA, 0))
         group.append(0)
         wfs.append(w)
@@ -342,10 +347,12 @@ def long_context(n_requests=100_000, seed=1, device=None, n_roles=8, steps=4,
 
 
 def bursty(n_requests=1_000_000, seed=1, device=None, n_models=4, mean_len=2048, cv=1.0,
-           n_prefixes=512, r_base=0) -> Trace:
+           n_prefixes=512, r_base=0, n_keep=None) -> Trace:
     """Config 4: L ~ lognormal(2048, 1.0) clamped to [64, 32768] over 4 models; prompts share
     one of n_prefixes system prefixes (shared across the model's workflows) + unique suffix.
-    r_base offsets request / workflow ids (one GPU's slice of a larger burst)."""
+    r_base offsets request / workflow ids (one GPU's slice of a larger burst).  n_keep: only
+    the first n_keep requests of the n_requests drawn (a bounded sample whose requests equal
+    the full burst's first n_keep)."""
     device = device or ("cuda" if torch.cuda.is_available() else "cpu")
     rng = np.random.default_rng(seed)
     s2 = math.log(1 + cv * cv)
@@ -358,6 +365,10 @@ def bursty(n_requests=1_000_000, seed=1, device=None, n_models=4, mean_len=2048,
     pkeys = [fnv1a_str(f"prefix{p}") for p in range(n_prefixes)]
     up = _p99(500, 0.5)
     unprof = rng.random(n_requests) < 0.1
+    if n_keep is not None and n_keep < n_requests:
+        n_requests = n_keep
+        L, model, pre, plen, unprof = L[:n_keep], model[:n_keep], pre[:n_keep], plen[:n_keep], \
+            unprof[:n_keep]
     for r in range(n_requests):
         b.add(r, "i", pkeys[pre[r]], 0, int(plen[r]))
         b.add(r, "i", salt_key(f"b{r_base + r}"), 0, int(L[r] - plen[r]), fresh=True)
