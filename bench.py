@@ -237,7 +237,8 @@ def reference_run(args, n_steps, n_warm, threads, hash_once, sample, seconds=Non
         toks = tr.tokens_np()
         rw, rm = S.registry_pairs(tr.wf, tr.role)
         t0 = time.perf_counter()
-        ref.step(k, toks, tr.tok_off, tr.res, tr.group, tr.wf, tr.role, rw, rm, 1.0 + k)
+        ref.step(k, toks, tr.tok_off, tr.res, tr.group, tr.wf, tr.role, rw, rm, 1.0 + k,
+                 S.hold_of(k, args.requests, tr.R))
         dt = time.perf_counter() - t0
         if k >= n_warm:
             done += tr.R
@@ -322,7 +323,7 @@ class Arm:
         self.bursts = []
         for k in range(n_bursts):
             tr = S.make_burst(k, args.requests, args.seed, dev, args.workload, args.models)
-            self.bursts.append(S.upload_burst(tr, args.block, dev))
+            self.bursts.append(S.upload_burst(tr, args.block, dev, k))
             del tr
         self.st = S.Steady(self.ctx, cl, args.requests, dev)
         self.overlap = args.free_sms >= 0
@@ -363,8 +364,7 @@ class Arm:
             if e:
                 e[0].record(self.S_stream)
             self.PB.bind_current_stream(self.ctx)
-            if k >= self.S.HOLD:
-                self.st.complete(self.bursts[k - self.S.HOLD], k)
+            self.st.complete(self.bursts, k)
             self.st.compose_nodes(self.bursts[k - 1] if k >= 1 else None, k)
             self.st.registry(self.bursts[k])
             self.st.route_admit(self.bursts[k], k, 1.0 + k, e[1:] if e else None)
@@ -386,7 +386,7 @@ def run_ours(args):
     arm.run(0, W_)
     torch.cuda.synchronize(dev)
     ctx.check_device_error()
-    ctx.stats(reset=True)
+    ctx.counters(reset=True)
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
@@ -403,7 +403,7 @@ def run_ours(args):
     launches = arm.launches() - l0
     clk = clocks.stop()
     ctx.check_device_error()
-    stats = ctx.stats(reset=True)
+    stats = ctx.counters(reset=True)
     ms = t0.elapsed_time(t1)
     ms_step = ms / K
     R = args.requests
@@ -496,7 +496,7 @@ def run_e2e(args, arm, E, k_first):
     for i in range(E):
         k = k_first + i
         tr = S.make_burst(k, args.requests, args.seed, dev, args.workload, args.models)
-        b = S.upload_burst(tr, args.block, dev)  # device buffers (overwritten by the copies)
+        b = S.upload_burst(tr, args.block, dev, k)  # device buffers (overwritten by the copies)
         rw, rm = S.registry_pairs(tr.wf, tr.role)
         host.append({"tokens": tr.tokens.cpu().pin_memory(), "tok_off": pin(tr.tok_off),
                      "res": pin(tr.res.view(np.int64).reshape(tr.R, 4)), "group": pin(tr.group),
@@ -558,8 +558,7 @@ def run_e2e(args, arm, E, k_first):
         b = devb[i]
         arm.S_stream.wait_event(eh)
         PB.bind_current_stream(arm.ctx)
-        if k >= S.HOLD:
-            arm.st.complete(bursts[k - S.HOLD], k)
+        arm.st.complete(bursts, k)
         arm.st.compose_nodes(bursts[k - 1], k)
         arm.st.registry(b)
         o = arm.st.route_admit(b, k, 1.0 + k)
@@ -609,7 +608,7 @@ def run_check(args, dev):
     report = {"check": "steady-state bursts vs the unmodified reference", "bursts": K,
               "workload": describe(args, 1), "per_burst": []}
     ok = True
-    arm.ctx.stats(reset=True)
+    arm.ctx.counters(reset=True)
     for k in range(K):
         arm.run(k, 1)
         torch.cuda.synchronize(dev)
@@ -620,7 +619,7 @@ def run_check(args, dev):
         rw, rm = S.registry_pairs(b.wf, b.role)
         t0 = time.perf_counter()
         d, a, m3, stg = ref.step(k, toks, b.tok_off, b.res, b.group, b.wf, b.role, rw, rm,
-                                 1.0 + k, want_staged=True)
+                                 1.0 + k, b.hold_h, want_staged=True)
         t_ref = time.perf_counter() - t0
         R = b.R
         mc = stg.shape[1]
@@ -640,7 +639,7 @@ def run_check(args, dev):
         report["per_burst"].append(row)
         print(json.dumps(row), flush=True)
         del toks
-    stats = arm.ctx.stats()
+    stats = arm.ctx.counters()
     tiers_ok = True
     bad = []
     for n in range(cl.n_replicas):

@@ -192,6 +192,11 @@ int pyg_hash_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_
    whose K1 overlaps another ctx's step on a second stream leaves SMs free for the step's
    latency-bound kernels (route, admission) this way. */
 int pyg_set_hash_ctas(pyg_ctx* ctx, int32_t n_ctas);
+/* K1 hashes prompts of >= min_tokens tokens (default 8192; 0 = never) as split tasks: one
+   warp per prompt, 512 tokens at a time, through the low-byte decomposition of FNV-1a
+   (k_hash.cu) -- the same hashes, without the long-prompt tail of one lane per request.
+   Requires B % 16 == 0 (otherwise ignored). */
+int pyg_set_hash_split(pyg_ctx* ctx, int64_t min_tokens);
 
 /* K2: staged matrix.  For request r and its j-th candidate replica cand[cand_off[g_r]+j]
    (g_r = d_group[r] < n_groups), d_staged[r*max_cand + j] = tier(L2).matched_prefix(prompt_r)
@@ -264,13 +269,21 @@ int pyg_release_batch_dev(pyg_ctx* ctx, const int64_t* d_tok_off, const int64_t*
 
 /* Node-table bookkeeping between bursts (the steady-state step): d_out holds, per replica,
    the base reservations then the reservations d_req[d_placed[j]] of the requests a burst
-   placed there (d_placed_off/d_placed from pyg_route_batch_dev), in placement order -- the
-   pool order of reservation_of (engine.cpp:616-628, 686).  d_placed_off may be NULL (base
-   only).  d_out_off[n] = d_base_off[n] + d_placed_off[n]; d_out needs base + placed entries. */
+   placed there (d_placed_off/d_placed from pyg_route_batch_dev) that are still held
+   (d_hold[r] >= hold_min; d_hold NULL = all), in placement order -- the pool order of
+   reservation_of (engine.cpp:616-628, 686).  d_placed_off may be NULL (base only).
+   d_out needs base + placed entries; d_out_off [n_rep+1]. */
 int pyg_nodes_compose_dev(pyg_ctx* ctx, int32_t n_rep, const int64_t* d_base_off,
                           const pyg_reservation* d_base, const int32_t* d_placed_off,
                           const int32_t* d_placed, const pyg_reservation* d_req,
-                          int64_t* d_out_off, pyg_reservation* d_out);
+                          const uint8_t* d_hold, int32_t hold_min, int64_t* d_out_off,
+                          pyg_reservation* d_out);
+/* pyg_release_batch_dev restricted to requests with d_hold[r] == hold (their completion
+   step): unpin_chain(seq, len) of each (hierarchy.cpp:132-142). */
+int pyg_release_hold_dev(pyg_ctx* ctx, const int64_t* d_tok_off, const int64_t* d_hash_off,
+                         const uint64_t* d_hashes, int32_t n_req, const int32_t* d_placed_off,
+                         const int32_t* d_placed, const int32_t* d_admitted,
+                         const uint8_t* d_hold, int32_t hold);
 /* FutureRegistry::update (manager.cpp:13-23) for n DISTINCT workflows at once (a burst's
    issue-time updates, engine.cpp:605-609, last write per workflow); max_wf >= every id. */
 int pyg_registry_update_batch_dev(pyg_ctx* ctx, int32_t n, const int32_t* d_wf,

@@ -4,8 +4,10 @@ The steady-state burst sequence of paper_2604_25899_b200/steady.py driven throug
 UNMODIFIED reference (oracle/_ref/libpythia_ref{16,64}.so, oracle/ref_shim.cpp pref_burst /
 pref_release):
 
-  step k: release burst k-2's admitted requests        unpin_chain, hierarchy.cpp:132-142
-          node table = background + burst k-1's placements (pool order, engine.cpp:616-628)
+  step k: release burst k-1's admitted requests of hold 1 and burst k-2's of hold 2
+                                                          unpin_chain, hierarchy.cpp:132-142
+          node table = background + burst k-1's placements of hold 2 (pool order,
+                                                          engine.cpp:616-628)
           FutureRegistry updates of burst k's issue     engine.cpp:605-609
           pref_burst: node_view staged values, route with sequential commit, admission per
           replica in order against the live L3           engine.cpp:640-692, 799-829
@@ -47,12 +49,13 @@ class RefSteady:
         return n_fill
 
     def node_table(self, k):
-        """background + burst k-1's placements, per replica in placement order."""
+        """background + burst k-1's placements still held (hold 2), per replica in placement
+        order."""
         cl = self.cl
         base = [list(cl.asg[cl.asg_off[n]:cl.asg_off[n + 1]]) for n in range(cl.n_replicas)]
         if k - 1 in self.hist:
-            _, _, tgt, _, res = self.hist[k - 1]
-            for r in np.nonzero(tgt >= 0)[0]:
+            _, _, tgt, _, res, hold = self.hist[k - 1]
+            for r in np.nonzero((tgt >= 0) & (hold >= 2))[0]:
                 base[int(tgt[r])].append(res[r])
         off = np.zeros(cl.n_replicas + 1, np.int64)
         np.cumsum([len(x) for x in base], out=off[1:])
@@ -60,12 +63,15 @@ class RefSteady:
         asg = np.array(flat, RES_DTYPE) if flat else np.zeros(0, RES_DTYPE)
         return off, asg
 
-    def step(self, k, tokens, tok_off, res, group, wf, role, reg_wf, reg_mask, now,
+    def step(self, k, tokens, tok_off, res, group, wf, role, reg_wf, reg_mask, now, hold,
              want_staged=False):
+        """hold: uint8 [R] bursts each request of this burst holds its replica (1 or 2)."""
         ref, cl = self.ref, self.cl
-        if k - HOLD in self.hist:
-            t, o, tgt, adm, _ = self.hist.pop(k - HOLD)
-            ref.release(self.caches, t, o, tgt, adm)
+        for h in (1, 2):
+            if k - h in self.hist:
+                t, o, tgt, adm, _, hd = self.hist[k - h]
+                ref.release(self.caches, t, o, tgt, (adm & (hd == h)).astype(np.int32))
+        self.hist.pop(k - HOLD, None)
         off, asg = self.node_table(k)
         for w, m in zip(reg_wf.tolist(), reg_mask.tolist()):
             ref.reg_update(self.reg, int(w), int(m))
@@ -75,7 +81,8 @@ class RefSteady:
                                      self.threads, want_staged)
         # replica_id == replica index in these clusters (make_cluster, id_base 0)
         tgt = dec["target"].astype(np.int32)
-        self.hist[k] = (tokens, tok_off, tgt, adm.astype(np.int32), np.asarray(res, RES_DTYPE))
+        self.hist[k] = (tokens, tok_off, tgt, adm.astype(np.int32), np.asarray(res, RES_DTYPE),
+                        np.asarray(hold, np.uint8))
         return dec, adm, m3, st
 
     def dump(self, n, tier):

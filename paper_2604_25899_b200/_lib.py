@@ -134,7 +134,9 @@ _sig("pyg_shard_unpack_dev", vp, vp, i32, i32, i32, vp, vp, vp)
 _sig("pyg_shard_pull_dev", vp, vp, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64)
 _sig("pyg_shard_local_placed_dev", vp, vp, vp, vp, vp, vp, vp)
 _sig("pyg_stats", vp, vp, i32)
-_sig("pyg_nodes_compose_dev", vp, i32, vp, vp, vp, vp, vp, vp, vp)
+_sig("pyg_set_hash_split", vp, i64)
+_sig("pyg_nodes_compose_dev", vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp)
+_sig("pyg_release_hold_dev", vp, vp, vp, vp, i32, vp, vp, vp, vp, i32)
 _sig("pyg_registry_update_batch_dev", vp, i32, vp, vp, i32)
 _sig("pyg_shard_apply_lists_dev", vp, vp, i32, i32)
 _sig("pyg_shard_apply_lists_range_dev", vp, vp, i32, i32, i32, i32, i32)
@@ -227,8 +229,11 @@ class Context:
     def check_device_error(self):
         check(_lib.pyg_check_device_error(self.h))
 
-    def stats(self, reset=False) -> dict:
-        """pyg_stats: eviction counters (synchronizes the ctx stream)."""
+    def set_hash_split(self, min_tokens: int):
+        check(_lib.pyg_set_hash_split(self.h, int(min_tokens)))
+
+    def counters(self, reset=False) -> dict:
+        """pyg_stats: eviction / admission counters (synchronizes the ctx stream)."""
         out = np.zeros(8, np.int64)
         check(_lib.pyg_stats(self.h, out.ctypes.data, int(bool(reset))))
         return {"evicted_blocks": int(out[0]), "evicted_tokens": int(out[1]),

@@ -484,13 +484,14 @@ __global__ void k_l3_final(CtxDev c, L3Args a, int64_t* match3, uint64_t* list, 
 // warp per request; decrements commute (pin -= 1 only while pin > 0).
 __global__ void k_release(CtxDev c, const int64_t* tok_off, const int64_t* hash_off,
                           const uint64_t* hashes, const int32_t* placed_off,
-                          const int32_t* placed, const int32_t* admitted) {
+                          const int32_t* placed, const int32_t* admitted,
+                          const uint8_t* hold, int hold_val) {
   const int rep = blockIdx.x;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const TierDev& t = c.tiers[2 * rep];
   for (int32_t k = placed_off[rep] + w; k < placed_off[rep + 1]; k += nw) {
     const int r = placed[k];
-    if (admitted[r] != 1) continue;
+    if (admitted[r] != 1 || (hold && hold[r] != hold_val)) continue;
     const uint64_t* hs = hashes + hash_off[r];
     const int64_t nh = hash_off[r + 1] - hash_off[r];
     for (int64_t i = lane; i < nh; i += 32) {
@@ -545,23 +546,40 @@ __global__ void k_dir_clear(CtxDev c, const DirRecord* rec, int64_t n, const int
 }
 
 // Node table of the next burst: per replica the base reservations, then the reservations
-// of the requests the last burst placed there, in placement order (the pool order of
-// reservation_of, engine.cpp:616-628, 686).  out_off = base_off + placed_off.
-__global__ void k_nodes_compose(int32_t n_rep, const int64_t* base_off,
+// of the requests the last burst placed there that are still held (hold[r] >= hold_min), in
+// placement order (the pool order of reservation_of, engine.cpp:616-628, 686).  One CTA:
+// thread n counts replica n's entries, a block scan gives the offsets, thread n copies.
+__global__ void __launch_bounds__(1024) k_nodes_compose(int32_t n_rep, const int64_t* base_off,
                                 const pyg_reservation* base, const int32_t* placed_off,
                                 const int32_t* placed, const pyg_reservation* req,
-                                int64_t* out_off, pyg_reservation* out) {
-  const int n = blockIdx.x;
-  const int64_t b0 = base_off[n], nb = base_off[n + 1] - b0;
-  const int64_t p0 = placed_off ? placed_off[n] : 0;
-  const int64_t np = placed_off ? placed_off[n + 1] - p0 : 0;
-  const int64_t o = b0 + p0;
-  for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) out[o + i] = base[b0 + i];
-  for (int64_t i = threadIdx.x; i < np; i += blockDim.x) out[o + nb + i] = req[placed[p0 + i]];
-  if (threadIdx.x == 0) {
-    out_off[n] = o;
-    if (n == n_rep - 1) out_off[n_rep] = o + nb + np;
+                                const uint8_t* hold, int hold_min, int64_t* out_off,
+                                pyg_reservation* out) {
+  __shared__ int64_t sm[64];
+  int64_t carry = 0;
+  for (int n0 = 0; n0 < n_rep; n0 += blockDim.x) {
+    const int n = n0 + threadIdx.x;
+    int64_t cnt = 0;
+    int32_t p0 = 0, p1 = 0;
+    if (n < n_rep) {
+      cnt = base_off[n + 1] - base_off[n];
+      if (placed_off) {
+        p0 = placed_off[n];
+        p1 = placed_off[n + 1];
+        for (int32_t j = p0; j < p1; ++j) cnt += (!hold || hold[placed[j]] >= hold_min);
+      }
+    }
+    int64_t tot;
+    const int64_t o = carry + block_exscan(cnt, sm, &tot);
+    if (n < n_rep) {
+      out_off[n] = o;
+      int64_t w = o;
+      for (int64_t i = base_off[n]; i < base_off[n + 1]; ++i) out[w++] = base[i];
+      for (int32_t j = p0; j < p1; ++j)
+        if (!hold || hold[placed[j]] >= hold_min) out[w++] = req[placed[j]];
+    }
+    carry += tot;
   }
+  if (threadIdx.x == 0) out_off[n_rep] = carry;
 }
 
 // dst segment k = src segment idx[k] (CSR gather of uint64 rows: tokens / hashes)
@@ -778,12 +796,26 @@ int pyg_gather_csr_dev(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_src_o
 int pyg_nodes_compose_dev(pyg_ctx* c, int32_t n_rep, const int64_t* d_base_off,
                           const pyg_reservation* d_base, const int32_t* d_placed_off,
                           const int32_t* d_placed, const pyg_reservation* d_req,
-                          int64_t* d_out_off, pyg_reservation* d_out) {
+                          const uint8_t* d_hold, int32_t hold_min, int64_t* d_out_off,
+                          pyg_reservation* d_out) {
   if (!c || n_rep < 0 || (d_placed_off && (!d_placed || !d_req))) return PYG_EINVAL;
   if (!n_rep) return PYG_OK;
   PYG_CUDA(cudaSetDevice(c->device));
-  k_nodes_compose<<<n_rep, 128, 0, c->stream>>>(n_rep, d_base_off, d_base, d_placed_off,
-                                                d_placed, d_req, d_out_off, d_out);
+  k_nodes_compose<<<1, 1024, 0, c->stream>>>(n_rep, d_base_off, d_base, d_placed_off, d_placed,
+                                             d_req, d_hold, hold_min, d_out_off, d_out);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_release_hold_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d_hash_off,
+                         const uint64_t* d_hashes, int32_t R, const int32_t* d_placed_off,
+                         const int32_t* d_placed, const int32_t* d_admitted,
+                         const uint8_t* d_hold, int32_t hold) {
+  if (!c || R < 0) return PYG_EINVAL;
+  if (R == 0 || c->n_rep == 0) return PYG_OK;
+  PYG_CUDA(cudaSetDevice(c->device));
+  k_release<<<c->n_rep, 256, 0, c->stream>>>(c->hd, d_tok_off, d_hash_off, d_hashes,
+                                             d_placed_off, d_placed, d_admitted, d_hold, hold);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -794,7 +826,7 @@ int pyg_release_batch_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d
   if (!c || R < 0) return PYG_EINVAL;
   if (R == 0 || c->n_rep == 0) return PYG_OK;
   k_release<<<c->n_rep, 256, 0, c->stream>>>(c->hd, d_tok_off, d_hash_off, d_hashes,
-                                             d_placed_off, d_placed, d_admitted);
+                                             d_placed_off, d_placed, d_admitted, nullptr, 0);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

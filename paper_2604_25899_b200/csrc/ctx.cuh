@@ -43,6 +43,7 @@ struct pyg_ctx {
   int32_t rep_base = 0;      // global index of this ctx's replica 0
   int64_t dir_admits = 0;    // admission calls since the last build (cleared bits accumulate)
   int32_t hash_ctas = 0;     // K1 persistent grid cap (0 = one CTA per SM)
+  int64_t split_min = 8192;  // K1: prompts of >= split_min tokens are split tasks (0 = never)
   void* d_aux = nullptr;     // second on-demand buffer (fused assembly's chunk sources)
   size_t d_aux_size = 0;
   // ordered L3 resolution of batched admission (batch.cu): per-L3-block claims
@@ -63,6 +64,8 @@ inline void dir_touch(pyg_ctx* c) { c->dir_dirty = true; }
 int assemble_offsets(pyg_ctx* c, int32_t R, const int64_t* d_seg_off, const pyg_segment* d_segs,
                      int64_t* d_tok_off);
 inline void count_launch(pyg_ctx* c, int n = 1) { c->launches += n; }
+cudaError_t device_setup(int dev);  // k_hash.cu: per-device K1 attributes and constants
+int sm_count(int dev);              // SM count of a device (cached per device)
 }  // namespace pyg_host
 
 #define PYG_CUDA(call)                                                  \

@@ -138,23 +138,167 @@ __global__ void k_chunk_src(int R, const int64_t* __restrict__ seg_off,
   }
 }
 
+// ------------------------------------------------------------ split tasks
+// A long prompt's chain is serial per token, so one lane per request leaves the longest
+// prompts of a batch as a tail (~119 cycles/token: 2 ms for 32k tokens).  A SPLIT task
+// hashes one long request on a whole warp, 512 tokens (a "super-chunk") at a time, lane l
+// owning the 16-token segment [16 l, 16 l + 16).  FNV-1a's xor touches only the low byte,
+// so with l = h mod 256 and h = l + 256 u:
+//   chain_m(h) = chain_m(l) + 256 u * P^m  (mod 2^64)            (P = FNV prime, m bytes)
+// and the low byte evolves on its own, l' = ((l ^ b) * 0xB3) mod 256, a triangular map:
+// bit j of l' is bit j of (l ^ b) xor a function of the lower bits.  Pass A finds every
+// segment's start low byte 2 bits at a time: a lane runs its segment for both values of
+// bit j (packed in the two 16-bit halves of one register; bit j+1 starts at 0), which
+// gives the segment's map on (bit j, bit j+1) -- (a, d) -> (a ^ X, d ^ Y[a]) -- and a
+// warp scan of those maps gives every lane its start bits from the super-chunk's.  Pass B
+// runs the 64-bit chain of each segment from its start low byte alone, and a warp scan of
+// the affine maps D' = D * P^(8 n) + (chain & ~0xff) restores the high part (D = h - l).
+// Requests with len >= kSplitMin and B % 16 == 0 become split tasks; they run first.
+constexpr int kSplitTok = 16;                 // tokens per lane segment
+constexpr int kSuper = 32 * kSplitTok;        // tokens per super-chunk
+__constant__ uint64_t c_pw8[kSplitTok + 1];   // P^(8 t), t = 0..16
+
+__device__ __forceinline__ uint32_t map2_then(uint32_t f, uint32_t g) {
+  // maps on 2 bits as (X | Y0 << 1 | Y1 << 2): (a, d) -> (a ^ X, d ^ Y[a]); f first
+  const uint32_t xf = f & 1u;
+  const uint32_t gy0 = (g >> 1) & 1u, gy1 = (g >> 2) & 1u;
+  const uint32_t y0 = ((f >> 1) & 1u) ^ (xf ? gy1 : gy0);
+  const uint32_t y1 = ((f >> 2) & 1u) ^ (xf ? gy0 : gy1);
+  return (xf ^ (g & 1u)) | (y0 << 1) | (y1 << 2);
+}
+
+// one 8-bit-automaton step on both packed candidates
+// (volatile: the byte extraction stays inside its round; hoisted out of the round loop,
+// 128 extracted bytes per lane would not fit in registers)
+__device__ __forceinline__ uint32_t lo8_step(uint32_t x, uint32_t w, int bi) {
+  uint32_t bb;
+  asm volatile("prmt.b32 %0, %1, 0, %2;" : "=r"(bb) : "r"(w),
+               "r"(0x4040u | static_cast<uint32_t>(bi) | (static_cast<uint32_t>(bi) << 8)));
+  return ((x ^ bb) & 0x00FF00FFu) * 0xB3u;
+}
+
+// One split task: request of n tokens at src, boundary hashes to out (B % 16 == 0).
+// wbuf: this warp's 2 staging buffers (rows of kRowBytes, row l = segment l).
+__device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_t n, int B,
+                           uint64_t* __restrict__ out, unsigned char* wbuf) {
+  const int lane = threadIdx.x & 31;
+  const int nsc = static_cast<int>((n + kSuper - 1) / kSuper);
+  auto issue = [&](int sc) {
+    unsigned char* st = wbuf + (sc & 1) * kStageBytes;
+    const int64_t t0 = static_cast<int64_t>(sc) * kSuper;
+    const int64_t nv = min(static_cast<int64_t>(kSuper), n - t0);
+#pragma unroll
+    for (int i = 0; i < kSuper / 32; ++i) {
+      const int t = i * 32 + lane;  // token of the super-chunk: row t / 16, column t % 16
+      if (t < nv) cp_async8(st + (t >> 4) * kRowBytes + (t & 15) * 8, src + t0 + t, 8);
+    }
+    cp_commit();
+  };
+  uint64_t H0 = kFnvOffset;  // hash at the super-chunk start (warp-uniform)
+  issue(0);
+  for (int sc = 0; sc < nsc; ++sc) {
+    if (sc + 1 < nsc)
+      issue(sc + 1);
+    else
+      cp_commit();
+    cp_wait1();
+    __syncwarp();
+    const unsigned char* row = wbuf + (sc & 1) * kStageBytes + lane * kRowBytes;
+    const int64_t seg0 = static_cast<int64_t>(sc) * kSuper + lane * kSplitTok;
+    const int nt = static_cast<int>(max(int64_t{0}, min(static_cast<int64_t>(kSplitTok), n - seg0)));
+    uint32_t w[2 * kSplitTok];
+#pragma unroll
+    for (int x = 0; x < kSplitTok / 2; ++x) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + 16 * x);
+      w[4 * x] = v.x;
+      w[4 * x + 1] = v.y;
+      w[4 * x + 2] = v.z;
+      w[4 * x + 3] = v.w;
+    }
+    const uint32_t L0 = static_cast<uint32_t>(H0) & 0xffu;
+    // pass A: the segment's start low byte, two bits per round
+    uint32_t known = 0;
+#pragma unroll 1
+    for (int j = 0; j < 8; j += 2) {
+      uint32_t x = known | ((known | (1u << j)) << 16);
+      if (nt == kSplitTok) {
+#pragma unroll
+        for (int wi = 0; wi < 2 * kSplitTok; ++wi) {
+#pragma unroll
+          for (int bi = 0; bi < 4; ++bi) x = lo8_step(x, w[wi], bi);
+        }
+      } else {
+        for (int t = 0; t < nt; ++t) {
+          const uint2 v = *reinterpret_cast<const uint2*>(row + 8 * t);
+#pragma unroll
+          for (int bi = 0; bi < 4; ++bi) x = lo8_step(x, v.x, bi);
+#pragma unroll
+          for (int bi = 0; bi < 4; ++bi) x = lo8_step(x, v.y, bi);
+        }
+      }
+      uint32_t m = 0;  // empty segments are the identity
+      if (nt > 0)
+        m = ((x >> j) & 1u) | (((x >> (j + 1)) & 1u) << 1) | (((x >> (16 + j + 1)) & 1u) << 2);
+      uint32_t inc = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc = map2_then(y, inc);
+      }
+      uint32_t pre = __shfl_up_sync(kFull, inc, 1);
+      if (lane == 0) pre = 0;
+      const uint32_t a0 = (L0 >> j) & 1u, d0 = (L0 >> (j + 1)) & 1u;
+      const uint32_t a = a0 ^ (pre & 1u);
+      const uint32_t d = d0 ^ ((pre >> (1 + a0)) & 1u);
+      known |= (a << j) | (d << (j + 1));
+    }
+    // pass B: the 64-bit chain of the segment from its start low byte
+    uint64_t h = known;
+    if (nt == kSplitTok) {
+#pragma unroll
+      for (int t = 0; t < kSplitTok; ++t)
+        h = fnv_token(h, static_cast<uint64_t>(w[2 * t]) | (static_cast<uint64_t>(w[2 * t + 1]) << 32));
+    } else {
+      for (int t = 0; t < nt; ++t) h = fnv_token(h, *reinterpret_cast<const uint64_t*>(row + 8 * t));
+    }
+    // D_{l+1} = D_l * P^(8 nt_l) + (chain_l & ~0xff), D = hash - low byte at a segment start
+    uint64_t A = nt > 0 ? c_pw8[nt] : 1ull, Bq = nt > 0 ? (h & ~0xffull) : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t ya = __shfl_up_sync(kFull, A, o), yb = __shfl_up_sync(kFull, Bq, o);
+      if (lane >= o) {
+        Bq = yb * A + Bq;
+        A = ya * A;
+      }
+    }
+    uint64_t ea = __shfl_up_sync(kFull, A, 1), eb = __shfl_up_sync(kFull, Bq, 1);
+    if (lane == 0) {
+      ea = 1;
+      eb = 0;
+    }
+    const uint64_t D = (H0 - L0) * ea + eb;
+    const uint64_t hend = h + D * (nt > 0 ? c_pw8[nt] : 1ull);
+    const int64_t e = seg0 + nt;
+    if (nt > 0 && (e % B == 0 || e == n)) out[(e - 1) / B] = hend;  // hierarchy.cpp:26
+    const int64_t nv = min(static_cast<int64_t>(kSuper), n - static_cast<int64_t>(sc) * kSuper);
+    H0 = __shfl_sync(kFull, hend, static_cast<int>((nv - 1) / kSplitTok));
+    __syncwarp();
+  }
+}
+
 // Chunks are aligned to each request's own first token, so with B % 16 == 0 a
 // block boundary always coincides with the end of a chunk: the emit decision
 // is per chunk and warp-uniform (no per-token test).  The last, partial chunk
 // and B % 16 != 0 take the generic per-token path.
 //
-// Long-prompt tail: the chain of one request is serial, ~119 cycles/token when its warp
-// has a scheduler to itself but ~2x that when it shares one.  The first iso_ctas CTAs
-// therefore run only 4 warps (one per scheduler), each on one of the longest tasks
-// (tasks are sorted longest-first; those whose longest prompt reaches iso_min_key * 4
-// tokens), and the persistent pool starts after them.  Config 2 (prompts < 2,700
-// tokens) never qualifies; config 4's 32k-token prompts do.
+// Long prompts (>= the split threshold) are split tasks (split_task above); the rest run
+// one lane per request in 32-request tasks.
 template <bool kGather>
 __global__ void __launch_bounds__(kWarps * 32, 2)
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
               uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task, GatherSrc g,
-              const uint16_t* __restrict__ sorted_keys, int iso_ctas, int iso_min_key) {
+              const int* __restrict__ n_split_p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbuf = smem + warp * 2 * kStageBytes;
@@ -162,35 +306,23 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   unsigned long long* wbase = reinterpret_cast<unsigned long long*>(
       smem + kWarps * 2 * kStageBytes + warp * kMetaBytes);
   unsigned long long* lsl = wbase + 32;
-  const int ntasks = (R + 31) / 32;
-  // isolated long tasks: [0, n_long)
-  int n_long = 0;
-  if (iso_ctas > 0 && sorted_keys) {
-    for (int b = 0; b < iso_ctas * 4; b += 32) {  // 32 candidate tasks per ballot
-      const int tt = b + lane;
-      const bool lng = tt < iso_ctas * 4 && tt < ntasks &&
-                       static_cast<int>(sorted_keys[static_cast<int64_t>(tt) * 32]) >= iso_min_key;
-      n_long += __popc(__ballot_sync(kFull, lng));
-    }
-  }
-  int iso_task = -1;
-  if (static_cast<int>(blockIdx.x) * 4 < n_long) {
-    if (warp >= 4) return;
-    iso_task = blockIdx.x * 4 + warp;
-    if (iso_task >= n_long) return;
-  }
-  // persistent: each warp pulls 32-request tasks, longest first, until none are left
-  for (int it = 0;; ++it) {
+  // tasks: [0, n_split) one long request each (split_task, the longest first), then
+  // 32-request tasks over the rest of the length-sorted order
+  const int n_split = (!kGather && n_split_p) ? *n_split_p : 0;
+  const int ntasks = n_split + (R - n_split + 31) / 32;
+  // persistent: each warp pulls tasks, longest first, until none are left
+  for (;;) {
   int task = 0;
-  if (iso_task >= 0) {
-    if (it > 0) break;
-    task = iso_task;
-  } else {
-    if (lane == 0) task = n_long + atomicAdd(next_task, 1);
-    task = __shfl_sync(kFull, task, 0);
-  }
+  if (lane == 0) task = atomicAdd(next_task, 1);
+  task = __shfl_sync(kFull, task, 0);
   if (task >= ntasks) break;
-  const int idx = task * 32 + lane;
+  if (task < n_split) {
+    const int r = order[task];
+    const int64_t s0 = tok_off[r];
+    split_task(tokens + s0, tok_off[r + 1] - s0, B, hashes + hash_off[r], wbuf);
+    continue;
+  }
+  const int idx = n_split + (task - n_split) * 32 + lane;
   const bool valid = idx < R;
   const int r = valid ? (order ? order[idx] : idx) : 0;
   const int64_t s = valid ? tok_off[r] : 0;
@@ -325,12 +457,20 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   }  // task loop
 }
 
-__global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val) {
+__global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val,
+                           int64_t split_min, int* n_split) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= R) return;
-  const int64_t L = (tok_off[r + 1] - tok_off[r] + 3) >> 2;
-  key[r] = static_cast<uint16_t>(L > 65535 ? 65535 : L);
-  val[r] = r;
+  const int64_t n = r < R ? tok_off[r + 1] - tok_off[r] : 0;
+  if (r < R) {
+    const int64_t L = (n + 3) >> 2;
+    key[r] = static_cast<uint16_t>(L > 65535 ? 65535 : L);
+    val[r] = r;
+  }
+  // split tasks: the n_split requests of >= split_min tokens.  They lead the descending
+  // length order up to key ties at the threshold, which only decide which of two equally
+  // long requests is split -- either way exact.
+  const unsigned m = __ballot_sync(kFull, r < R && split_min > 0 && n >= split_min);
+  if (m && (threadIdx.x & 31) == 0) atomicAdd(n_split, __popc(m));
 }
 
 __global__ void k_nblocks(const int64_t* tok_off, int R, int B, int64_t* nb) {
@@ -367,6 +507,41 @@ int pyg_hash_offsets_dev(pyg_ctx* c, const int64_t* d_tok_off, int32_t R, int64_
 
 }  // extern "C"
 
+namespace pyg_host {
+// Per-device one-time setup of K1: its dynamic shared memory attribute and the P^(8t)
+// table of split tasks (both are per device, so cached per device id).
+cudaError_t device_setup(int dev) {
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (done[dev]) return cudaSuccess;
+  cudaError_t e = cudaSetDevice(dev);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_hash_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmemBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_hash_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmemBytes);
+  if (e != cudaSuccess) return e;
+  uint64_t pw[kSplitTok + 1];
+  uint64_t q = 1;
+  for (int t = 0; t <= kSplitTok; ++t) {
+    pw[t] = q;
+    for (int i = 0; i < 8; ++i) q *= kFnvPrime;
+  }
+  e = cudaMemcpyToSymbol(c_pw8, pw, sizeof(pw));
+  if (e != cudaSuccess) return e;
+  done[dev] = true;
+  return cudaSuccess;
+}
+
+int sm_count(int dev) {
+  static int n[64] = {};
+  if (dev < 0 || dev >= 64) return 1;
+  if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev] > 0 ? n[dev] : 1;
+}
+}  // namespace pyg_host
+
 // length sort (descending, for warp balance) + the persistent K1 launch
 template <bool kGather>
 static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_off, int32_t R,
@@ -378,7 +553,7 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   const size_t kb = (static_cast<size_t>(R) * 2 + 255) & ~size_t{255};
   const size_t vb = (static_cast<size_t>(R) * 4 + 255) & ~size_t{255};
   void* sp;
-  int rc = scratch(c, 2 * kb + 2 * vb + tmp + 512, &sp);
+  int rc = scratch(c, 2 * kb + 2 * vb + tmp + 768, &sp);
   if (rc) return rc;
   char* p = static_cast<char*>(sp);
   auto* k_in = reinterpret_cast<uint16_t*>(p);
@@ -386,29 +561,24 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   auto* v_in = reinterpret_cast<int32_t*>(p + 2 * kb);
   auto* v_out = reinterpret_cast<int32_t*>(p + 2 * kb + vb);
   void* d_tmp = p + 2 * kb + 2 * vb;
-  k_len_keys<<<(R + 255) / 256, 256, 0, c->stream>>>(d_tok_off, R, k_in, v_in);
+  auto* ctr0 = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
+  PYG_CUDA(cudaMemsetAsync(ctr0, 0, 8, c->stream));  // [0] task counter, [1] split requests
+  // split tasks: the fused-assembly loader and B % 16 != 0 keep one lane per request
+  const int64_t split_min0 = (!kGather && c->B % kSplitTok == 0) ? c->split_min : 0;
+  k_len_keys<<<(R + 255) / 256, 256, 0, c->stream>>>(d_tok_off, R, k_in, v_in, split_min0,
+                                                     ctr0 + 1);
   PYG_LAUNCHED(c);
   PYG_CUDA(cub::DeviceRadixSort::SortPairsDescending(d_tmp, tmp, k_in, k_out, v_in, v_out, R, 0,
                                                      16, c->stream));
   PYG_LAUNCHED(c);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_hash_staged<kGather>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
-    attr = true;
-  }
+  PYG_CUDA(pyg_host::device_setup(c->device));
   const int per_block = kWarps * 32;
-  const int tasks = (R + 31) / 32;
-  static int n_sm = 0;
-  if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
+  const int n_sm = pyg_host::sm_count(c->device);
   const int cap = c->hash_ctas > 0 ? std::min(c->hash_ctas, n_sm) : n_sm;
-  const int grid = std::min((tasks + kWarps - 1) / kWarps, cap);  // persistent: 1 CTA/SM
-  auto* ctr = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
-  PYG_CUDA(cudaMemsetAsync(ctr, 0, 4, c->stream));
-  // isolate the longest tasks (>= 8192-token prompts) on 16 SMs, one warp per scheduler
-  const int iso = grid >= 64 ? 16 : 0;
+  const int tasks_max = (R + 31) / 32 + (split_min0 ? R : 0);
+  const int grid = std::max(1, std::min((tasks_max + kWarps - 1) / kWarps, cap));  // 1 CTA/SM
   k_hash_staged<kGather><<<grid, per_block, kSmemBytes, c->stream>>>(
-      d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr, g, k_out, iso, 8192 / 4);
+      d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr0, g, ctr0 + 1);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -442,13 +612,18 @@ int pyg_assemble_hash_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
   auto* side = reinterpret_cast<uint64_t*>(static_cast<char*>(ap) + tb);
   auto* ctr = reinterpret_cast<unsigned long long*>(side + side_cap * kChunk);
   PYG_CUDA(cudaMemsetAsync(ctr, 0, 8, c->stream));
-  static int n_sm = 0;
-  if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
+  const int n_sm = pyg_host::sm_count(c->device);
   k_chunk_src<<<std::min((R + 7) / 8, 16 * n_sm), 256, 0, c->stream>>>(
       R, d_seg_off, d_segs, d_pool, d_tok_off, tab, tab_cap, side, side_cap, ctr, c->hd.error);
   PYG_LAUNCHED(c);
   return hash_launch<true>(c, d_pool, d_tok_off, R, d_hash_off, d_hashes,
                            GatherSrc{tab, d_tokens});
+}
+
+int pyg_set_hash_split(pyg_ctx* c, int64_t min_tokens) {
+  if (!c || min_tokens < 0) return PYG_EINVAL;
+  c->split_min = (min_tokens + 3) & ~int64_t{3};
+  return PYG_OK;
 }
 
 int pyg_set_hash_ctas(pyg_ctx* c, int32_t n_ctas) {

@@ -3,11 +3,13 @@
 A trace arrives as successive bursts (windows of the issue order).  Step k handles burst k
 on a cluster whose state carries over from the bursts before it:
 
-  1. completion of burst k-2: its admitted requests are released      (unpin_chain,
+  1. completions: a placed request holds its replica for hold(r) in {1, 2} bursts (by the
+     parity of its global request id); at step k the admitted requests of burst k-1 with
+     hold 1 and of burst k-2 with hold 2 are released         (unpin_chain,
      hierarchy.cpp:132-142; their blocks stay in L1, unpinned, so L1 fills and later
      admissions evict)
-  2. node table of burst k: background load + the reservations burst k-1 placed
-     (a placement holds its replica for two bursts; pool order, engine.cpp:616-628, 686)
+  2. node table of burst k: background load + the reservations of burst k-1's placements
+     still held (hold 2), in pool order                       (engine.cpp:616-628, 686)
   3. FutureRegistry updates of burst k's issue (engine.cpp:605-609)
   4. K2 staged matrix -> K3 sequential-commit route -> K4/K5 admission with eviction and
      the ordered L3 promotion (engine.cpp:640-692, 799-829)
@@ -30,7 +32,7 @@ from . import batch as PB
 from . import workload as W
 from ._lib import check
 
-HOLD = 2           # bursts a placement stays in the node table (completes at step k + HOLD)
+HOLD = 2           # longest hold: a placement of burst k completes at step k+1 or k+2
 N_MODELS = 8       # config 4 cluster: 8 models x 32 replicas = 256 replicas
 REPLICAS = 256
 
@@ -46,6 +48,12 @@ def registry_mask(role: np.ndarray) -> np.ndarray:
     one = np.uint64(1)
     return (one << r) | (one << ((r + np.uint64(3)) % np.uint64(16))) | \
         (one << ((r + np.uint64(7)) % np.uint64(16)))
+
+
+def hold_of(k: int, R: int, n: int) -> np.ndarray:
+    """Bursts each request of burst k (R requests per burst; the first n) holds its
+    replica once placed: 1 + parity of its global request id."""
+    return (1 + ((k * R + np.arange(n)) & 1)).astype(np.uint8)
 
 
 def registry_pairs(wf: np.ndarray, role: np.ndarray):
@@ -97,13 +105,16 @@ class Burst:
     reg_mask: torch.Tensor
     n_reg: int
     max_wf: int
+    hold: torch.Tensor        # uint8 [R], bursts a placement is held (hold_of)
+    hold_h: np.ndarray
 
     @property
     def R(self):
         return self.b.R
 
 
-def upload_burst(tr: W.Trace, B: int, device) -> Burst:
+def upload_burst(tr: W.Trace, B: int, device, k: int = 0, R_full: int = 0) -> Burst:
+    """Burst k of R_full requests per burst (tr may be its first tr.R requests)."""
     tok = tr.tokens if tr.tokens.device == torch.device(device) else tr.tokens.to(device)
     nb = (np.diff(tr.tok_off) + B - 1) // B
     hoff = np.zeros(tr.R + 1, np.int64)
@@ -115,9 +126,11 @@ def upload_burst(tr: W.Trace, B: int, device) -> Burst:
                         torch.from_numpy(tr.group).to(device), torch.from_numpy(tr.wf).to(device),
                         torch.from_numpy(tr.role).to(device), int(hoff[-1]), tr.n_tokens)
     rw, rm = registry_pairs(tr.wf, tr.role)
+    hold = hold_of(k, R_full or tr.R, tr.R)
     return Burst(db, tr.tok_off, tr.res, tr.group, tr.wf, tr.role,
                  torch.from_numpy(rw).to(device), torch.from_numpy(rm.view(np.int64)).to(device),
-                 len(rw), int(tr.wf.max()) if tr.R else 0)
+                 len(rw), int(tr.wf.max()) if tr.R else 0, torch.from_numpy(hold).to(device),
+                 hold)
 
 
 class Steady:
@@ -139,17 +152,26 @@ class Steady:
     def out(self, k) -> PB.StepOut:
         return self.outs[k % (HOLD + 1)]
 
-    def complete(self, burst: Burst, k):
-        """Step k's completions: release burst k - HOLD (call with that burst)."""
-        o = self.out(k - HOLD)
-        PB.release_batch(self.ctx, burst.b, o)
+    def complete(self, bursts, k):
+        """Step k's completions: burst k-1's admitted requests of hold 1, burst k-2's of
+        hold 2 (bursts indexable by burst number)."""
+        for h in (1, 2):
+            if k - h < 0:
+                continue
+            b, o = bursts[k - h], self.out(k - h)
+            check(_lib._lib.pyg_release_hold_dev(self.ctx.h, _ptr(b.b.tok_off),
+                                                 _ptr(b.b.hash_off), _ptr(b.b.hashes), b.R,
+                                                 _ptr(o.placed_off), _ptr(o.placed),
+                                                 _ptr(o.admitted), _ptr(b.hold), h))
 
     def compose_nodes(self, prev: Burst | None, k):
+        """node table of step k: base + burst k-1's placements still held (hold 2)."""
         o = self.out(k - 1) if prev is not None else None
         check(_lib._lib.pyg_nodes_compose_dev(
             self.ctx.h, self.cl.n_replicas, _ptr(self.base_off), _ptr(self.base),
             _ptr(o.placed_off) if o else None, _ptr(o.placed) if o else None,
-            _ptr(prev.b.res) if prev else None, _ptr(self.nodes.asg_off), _ptr(self.nodes.asg)))
+            _ptr(prev.b.res) if prev else None, _ptr(prev.hold) if prev else None, 2,
+            _ptr(self.nodes.asg_off), _ptr(self.nodes.asg)))
 
     def registry(self, burst: Burst):
         check(_lib._lib.pyg_registry_update_batch_dev(self.ctx.h, burst.n_reg, _ptr(burst.reg_wf),
@@ -173,8 +195,7 @@ class Steady:
         """Everything of step k after K1 (bursts[k].b.hashes ready); bursts is indexable by
         burst number for k-2 .. k."""
         PB.bind_current_stream(self.ctx)
-        if k >= HOLD:
-            self.complete(bursts[k - HOLD], k)
+        self.complete(bursts, k)
         self.compose_nodes(bursts[k - 1] if k >= 1 else None, k)
         self.registry(bursts[k])
         return self.route_admit(bursts[k], k, now, events)
@@ -238,7 +259,7 @@ def apply_ops_gpu(ctx, trace: W.Trace, ops):
             raise ValueError(op)
 
 
-def warm_fill_plan(warm: W.Trace, cl: W.Cluster, fill_frac=0.85):
+def warm_fill_plan(warm: W.Trace, cl: W.Cluster, fill_frac=0.9):
     """Placed CSR of the warm fill: warm requests assigned round-robin to their group's
     replicas until each replica's assigned tokens reach fill_frac of its KV capacity.  Admitted
     (pinned) then released, this leaves every L1 near full of unpinned blocks."""
@@ -270,7 +291,7 @@ def apply_warm_fill_gpu(ctx, warm: W.Trace, off, placed, B, device, now=0.5):
     """Admit the warm placements (K4/K5: lookup, evict, insert pinned) and release them.  Run
     it first, on empty tiers (then warm_ops): every replica stays under its KV capacity, so
     this leaves exactly insert_chain(L1, prompt, len, lineage, now, 0) per placement."""
-    wb = upload_burst(warm, B, device)
+    wb = upload_burst(warm, B, device, 0)
     PB.bind_current_stream(ctx)
     PB.hash_batch(ctx, wb.b)
     o = PB.StepOut(torch.zeros((warm.R, 3), dtype=torch.int64, device=device),

@@ -159,6 +159,37 @@ def test_hash_batch_long_prompts_isolated(B):
         assert np.array_equal(got[hoff[r]:hoff[r + 1]], want), (r, lens[r])
 
 
+@pytest.mark.parametrize("B", [16, 32, 64, 5])
+@pytest.mark.parametrize("split_min", [1, 100, 777])
+def test_hash_batch_split_tasks(B, split_min):
+    """K1 split tasks (one warp per prompt, low-byte decomposition of FNV-1a) with a low
+    threshold so every length class goes through them: 1..1,100 tokens (partial segments,
+    partial super-chunks, ragged block ends), super-chunk multiples, long prompts."""
+    from paper_2604_25899_b200 import Context
+    from paper_2604_25899_b200 import batch as PB
+    rng = np.random.default_rng(7 * B + split_min)
+    lens = np.concatenate([np.arange(0, 1100, 7), [511, 512, 513, 1024, 1025, 4096, 4097, 32768],
+                           rng.integers(1, 20000, 60)])
+    rng.shuffle(lens)
+    off = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    toks = rng.integers(0, 1 << 63, size=int(off[-1]), dtype=np.uint64) * np.uint64(3)
+    ctx = Context(1, 1000, 1000, B)
+    ctx.set_hash_split(split_min)
+    z = np.zeros(len(lens), np.int32)
+    res = np.zeros(len(lens), PB.RES_DTYPE)
+    db = PB.upload_batch(ctx, toks, off, res, z, z, z)
+    PB.bind_current_stream(ctx)
+    PB.hash_batch(ctx, db)
+    torch.cuda.synchronize()
+    got = db.hashes.cpu().numpy().view(np.uint64)
+    hoff = db.hash_off.cpu().numpy()
+    o = Restated(B)
+    for r in range(len(lens)):
+        want = o.chain_hashes(toks[off[r]:off[r + 1]])
+        assert np.array_equal(got[hoff[r]:hoff[r + 1]], want), (r, lens[r])
+
+
 def test_batch_config4_bursty_shape():
     """Config 4 shape: lognormal prompt lengths up to 32k, 4 models interleaved over the
     replicas, 10% unprofiled (alpha 0) reservations."""

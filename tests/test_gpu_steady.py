@@ -20,7 +20,7 @@ def _scenario(B, n_bursts, R, n_rep, n_models, kv, seed):
                     r_base=10_000_000, **kw)
     cl = W.make_cluster(n_rep, n_models, kv=kv, l2=kv, seed=seed)
     ops = S.warm_ops(warm, cl, l3_prefixes=16, l2_per_group=8, seed=seed)
-    off, placed = S.warm_fill_plan(warm, cl)
+    off, placed = S.warm_fill_plan(warm, cl, fill_frac=0.97)
     return bursts, warm, cl, ops, off, placed
 
 
@@ -33,7 +33,7 @@ def _ref_run(B, bursts, warm, cl, ops, off, placed):
     for k, tr in enumerate(bursts):
         rw, rm = S.registry_pairs(tr.wf, tr.role)
         outs.append(ref.step(k, tr.tokens_np(), tr.tok_off, tr.res, tr.group, tr.wf, tr.role,
-                             rw, rm, 1.0 + k, want_staged=True))
+                             rw, rm, 1.0 + k, S.hold_of(k, tr.R, tr.R), want_staged=True))
     return ref, outs
 
 
@@ -65,9 +65,9 @@ def test_steady_sequence_matches_reference(B, seed):
     ctx = Context(cl.n_replicas, cl.kv_capacity, cl.l2_capacity, B)
     assert S.apply_warm_fill_gpu(ctx, warm, off, placed, B, dev) == len(placed)
     S.apply_ops_gpu(ctx, warm, ops)
-    db = [S.upload_burst(tr, B, dev) for tr in bursts]
+    db = [S.upload_burst(tr, B, dev, k) for k, tr in enumerate(bursts)]
     st = S.Steady(ctx, cl, max(b.R for b in db), dev)
-    ctx.stats(reset=True)
+    ctx.counters(reset=True)
     for k in range(len(db)):
         PB.bind_current_stream(ctx)
         PB.hash_batch(ctx, db[k].b)
@@ -90,4 +90,4 @@ def test_steady_sequence_matches_reference(B, seed):
         for t in (0, 1):
             assert ctx.dump(n, t).tobytes() == ref.dump(n, t).tobytes(), (n, t)
     assert ctx.dump(0, 2).tobytes() == ref.dump(0, 2).tobytes()
-    assert ctx.stats()["evicted_blocks"] > 0
+    assert ctx.counters()["evicted_blocks"] > 0
