@@ -77,6 +77,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
+    ap.add_argument("--split-min", type=int, default=8192,
+                    help="K1: prompts of >= this many tokens are split tasks (0 = never)")
     ap.add_argument("--free-sms", type=int, default=8,
                     help="K1 of step k+1 overlaps step k on a second stream, its grid capped at "
                          "(SMs - free_sms); -1 = no overlap (serial step)")
@@ -333,6 +335,7 @@ class Arm:
         if self.overlap:
             n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
             self.hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
+        self.hctx.set_hash_split(args.split_min)
         self.ev_h = {}
         torch.cuda.synchronize(dev)
         self.ctx.check_device_error()
