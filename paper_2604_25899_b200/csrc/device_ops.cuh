@@ -345,19 +345,70 @@ struct EvictOut {
 
 // evict_for_space (manager.cpp:102-138) on one tier, whole CTA.
 // excess = base + needed - capacity must be computed by the caller (base =
-// l1_occupancy for L1).  Candidates = alive unpinned blocks (pin <= 0);
-// sorted by the reference key; the shortest prefix with sum(size) >= excess
-// is erased (all candidates if that is unsatisfiable).  freed ids are written
-// in eviction order to out_ids[0..cap).  smem_keys: kSmemSortCap*12 bytes or
-// nullptr (then the tier scratch is used); sm: >= 33 int64.
-__device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t excess, int speculative,
-                                uint64_t* out_ids, int64_t cap, unsigned char* smem_keys,
-                                int64_t* sm) {
+// l1_occupancy for L1).  Candidates = alive unpinned blocks (pin <= 0), in the
+// reference order (dead first, last_access ascending, block id ascending); the
+// shortest prefix with sum(size) >= excess is erased (all candidates if that is
+// unsatisfiable).  freed ids are written in eviction order to out_ids[0..cap).
+// smem_keys: kSmemSortCap*12 bytes or nullptr (then the tier scratch is used);
+// sm: >= 48 int64.
+//
+// The candidates are gathered once (key = order(last_access) + class | size |
+// log index, log index = id order).  Then, group by group -- a group = the
+// candidates sharing (class, last_access) -- the smallest remaining group is
+// found with one block reduction; it is taken whole while it does not reach the
+// remaining excess, else the cut falls inside it and its members are taken in
+// id (= gather) order.  Last-access values are event times, so the cut is
+// usually a few groups in; after kEvictGroups groups the remainder is finished
+// by a full bitonic sort (block_evict_sorted), which continues the same order.
+constexpr int kEvictGroups = 24;
+
+struct EvGroup {  // a (class, last_access) key + the total size of its members
+  uint32_t cls;   // 0 dead, 1 live, 2 none
+  uint64_t h;
+  int64_t sz;
+};
+
+__device__ __forceinline__ bool grp_less(uint32_t ac, uint64_t ah, uint32_t bc, uint64_t bh) {
+  return ac != bc ? ac < bc : ah < bh;
+}
+
+__device__ __forceinline__ EvGroup grp_min(EvGroup a, EvGroup b) {
+  if (a.cls == b.cls && a.h == b.h) return EvGroup{a.cls, a.h, a.sz + b.sz};
+  return grp_less(a.cls, a.h, b.cls, b.h) ? a : b;
+}
+
+__device__ inline EvGroup block_grp_min(EvGroup g, int64_t* sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    EvGroup y{__shfl_xor_sync(kFull, g.cls, o), __shfl_xor_sync(kFull, g.h, o),
+              __shfl_xor_sync(kFull, g.sz, o)};
+    g = grp_min(g, y);
+  }
+  if (lane == 0) {
+    sm[3 * w] = g.cls;
+    sm[3 * w + 1] = static_cast<int64_t>(g.h);
+    sm[3 * w + 2] = g.sz;
+  }
+  __syncthreads();
+  EvGroup r{2u, ~0ull, 0};
+  for (int k = 0; k < nw; ++k)
+    r = grp_min(r, EvGroup{static_cast<uint32_t>(sm[3 * k]), static_cast<uint64_t>(sm[3 * k + 1]),
+                           sm[3 * k + 2]});
+  __syncthreads();
+  return r;
+}
+
+// The sorted remainder (used after kEvictGroups groups, and for candidate sets larger than
+// the shared key buffer): the shortest sorted prefix of the alive unpinned blocks with
+// sum(size) >= excess, bitonic sort of (class, order(last_access), log index).
+__device__ inline EvictOut block_evict_sorted(const CtxDev& c, TierDev* tp, int64_t excess,
+                                              int speculative, uint64_t* out_ids, int64_t cap,
+                                              unsigned char* smem_keys, int64_t* sm) {
   EvictOut r{0, 0, 1};
   if (excess <= 0) return r;
   const TierDev t = *tp;
   const int64_t n = t.log_len;
-  // count candidates
   int64_t mine = 0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const Block& b = t.log[i];
@@ -376,7 +427,6 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
     khi = t.scratch;
     klo = reinterpret_cast<uint32_t*>(t.scratch + 2 * t.log_cap);
   }
-  // gather (chunked stable compaction into the key buffer)
   int64_t write = 0;
   for (int64_t base = 0; base < n; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
@@ -411,7 +461,6 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
   }
   __syncthreads();
   block_bitonic(khi, klo, np2);
-  // shortest sorted prefix with cumulative size >= excess
   int64_t cum = 0, cut = ncand;  // cut = number of victims
   for (int64_t base = 0; base < ncand; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
@@ -422,7 +471,6 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
     }
     int64_t tot;
     const int64_t before = cum + block_exscan(sz, sm, &tot);
-    // victim i is taken iff the running total before it is < excess
     const bool stop_here = i < ncand && before < excess && before + sz >= excess;
     if (stop_here) sm[40] = i + 1;
     __syncthreads();
@@ -435,7 +483,6 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
     cum += tot;
     __syncthreads();
   }
-  // erase victims, emit ids
   int64_t freed = 0;
   for (int64_t i = threadIdx.x; i < cut; i += blockDim.x) {
     const int64_t li = klo[i] & 0x7fffffffu;
@@ -447,18 +494,156 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
   if (threadIdx.x == 0) {
     tp->occupancy -= ftot;
     tp->n_alive -= cut;
-    if (c.stats) {
-      atomicAdd(c.stats, static_cast<unsigned long long>(cut));
-      atomicAdd(c.stats + 1, static_cast<unsigned long long>(ftot));
-      atomicAdd(c.stats + 2, 1ULL);
-      if (ftot < excess) atomicAdd(c.stats + 3, 1ULL);
-    }
   }
   __syncthreads();
   r.n_freed = cut;
   r.freed_tokens = ftot;
   r.satisfied = ftot >= excess;
   return r;
+}
+
+__device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t excess, int speculative,
+                                uint64_t* out_ids, int64_t cap, unsigned char* smem_keys,
+                                int64_t* sm) {
+  EvictOut res{0, 0, 1};
+  if (excess <= 0) return res;
+  const TierDev t = *tp;
+  const int64_t n = t.log_len;
+  int64_t mine = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const Block& b = t.log[i];
+    mine += ((b.flags & kAlive) && b.pin <= 0) ? 1 : 0;
+  }
+  int64_t ncand;
+  block_exscan(mine, sm, &ncand);
+  int64_t opos = 0, rem = excess, taken = 0, ftok = 0;
+  bool done = false;
+  // the grouped path needs the keys in shared memory: log index < 2^24, size < 128
+  if (smem_keys && ncand <= kSmemSortCap && n < (1 << 24) && c.B < 128) {
+    uint64_t* khi = reinterpret_cast<uint64_t*>(smem_keys);
+    uint32_t* klo = reinterpret_cast<uint32_t*>(smem_keys + kSmemSortCap * 8);
+    int64_t write = 0;
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+      const int64_t i = base + threadIdx.x;
+      bool cand = false;
+      uint64_t h = 0;
+      uint32_t l = 0;
+      if (i < n) {
+        const Block& b = t.log[i];
+        cand = (b.flags & kAlive) && b.pin <= 0;
+        if (cand) {
+          bool dead = false;
+          if (speculative) {
+            const bool live = b.wf >= 0 && b.wf < c.reg_cap && c.reg_present[b.wf] &&
+                              b.role >= 0 && b.role < 64 &&
+                              ((c.reg_mask[b.wf] >> b.role) & 1ULL);
+            dead = !live;  // FutureRegistry::lineage_live (manager.cpp:19-23)
+          }
+          h = order_double(b.la);
+          l = (dead ? 0u : 0x80000000u) | (static_cast<uint32_t>(b.e - b.s) << 24) |
+              static_cast<uint32_t>(i);
+        }
+      }
+      int64_t tot;
+      const int64_t pos = write + block_exscan(cand ? 1 : 0, sm, &tot);
+      if (cand) {
+        khi[pos] = h;
+        klo[pos] = l;
+      }
+      write += tot;
+    }
+    __syncthreads();
+    uint32_t pc = 0;   // groups <= (pc, ph) are taken; pc = 0, ph = 0 with first = true: none
+    uint64_t ph = 0;
+    bool first = true;
+    for (int g = 0; g < kEvictGroups; ++g) {
+      EvGroup loc{2u, ~0ull, 0};
+      for (int64_t i = threadIdx.x; i < ncand; i += blockDim.x) {
+        const uint32_t cl = klo[i] >> 31;
+        const uint64_t h = khi[i];
+        if (!first && !grp_less(pc, ph, cl, h)) continue;
+        loc = grp_min(loc, EvGroup{cl, h, static_cast<int64_t>((klo[i] >> 24) & 0x7fu)});
+      }
+      const EvGroup m = block_grp_min(loc, sm + 8);
+      if (m.cls == 2u) {  // nothing left: every candidate is freed, unsatisfied
+        done = true;
+        break;
+      }
+      const bool whole = m.sz < rem;
+      // members of group m in id order: take all, or while the running size before < rem
+      int64_t run = 0;
+      for (int64_t base = 0; base < ncand; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        bool mem = false;
+        int64_t sz = 0;
+        uint32_t lo = 0;
+        if (i < ncand) {
+          lo = klo[i];
+          mem = (lo >> 31) == m.cls && khi[i] == m.h;
+          sz = mem ? static_cast<int64_t>((lo >> 24) & 0x7fu) : 0;
+        }
+        int64_t tot;
+        const int64_t before = run + block_exscan(sz, sm, &tot);
+        const bool take = mem && (whole || before < rem);
+        int64_t ntk;
+        const int64_t rank = block_exscan(take ? 1 : 0, sm, &ntk);
+        if (take) {
+          const int64_t li = lo & 0xffffffu;
+          const int64_t at = opos + rank;
+          if (out_ids && at < cap) out_ids[at] = t.log[li].id;
+          erase_at(t, li);
+        }
+        opos += ntk;
+        run += tot;
+        if (!whole && run >= rem) break;  // uniform: the cut is inside this chunk
+      }
+      taken = opos;
+      if (!whole) {
+        done = true;
+        break;
+      }
+      rem -= m.sz;
+      pc = m.cls;
+      ph = m.h;
+      first = false;
+    }
+    {  // tokens freed by the grouped phase: the sizes of the erased candidates
+      int64_t f = 0;
+      for (int64_t i = threadIdx.x; i < ncand; i += blockDim.x) {
+        const uint32_t lo = klo[i];
+        if (!(t.log[lo & 0xffffffu].flags & kAlive)) f += (lo >> 24) & 0x7fu;
+      }
+      block_exscan(f, sm, &ftok);
+      rem = excess - ftok;
+    }
+    if (threadIdx.x == 0) {
+      tp->occupancy -= ftok;
+      tp->n_alive -= taken;
+    }
+    __syncthreads();
+    res.n_freed = taken;
+    res.freed_tokens = ftok;
+    res.satisfied = ftok >= excess;
+    if (!done) {  // more than kEvictGroups groups: finish with the sorted path
+      const EvictOut rest = block_evict_sorted(c, tp, rem, speculative,
+                                               out_ids ? out_ids + opos : nullptr,
+                                               out_ids ? max(int64_t{0}, cap - opos) : 0,
+                                               smem_keys, sm);
+      res.n_freed += rest.n_freed;
+      res.freed_tokens += rest.freed_tokens;
+      res.satisfied = res.freed_tokens >= excess;
+    }
+  } else {
+    res = block_evict_sorted(c, tp, excess, speculative, out_ids, cap, smem_keys, sm);
+  }
+  if (threadIdx.x == 0 && c.stats) {
+    atomicAdd(c.stats, static_cast<unsigned long long>(res.n_freed));
+    atomicAdd(c.stats + 1, static_cast<unsigned long long>(res.freed_tokens));
+    atomicAdd(c.stats + 2, 1ULL);
+    if (!res.satisfied) atomicAdd(c.stats + 3, 1ULL);
+  }
+  __syncthreads();
+  return res;
 }
 
 // ----------------------------------------------------------------- routing
