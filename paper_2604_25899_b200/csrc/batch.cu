@@ -598,6 +598,7 @@ __global__ void k_gather_csr(const uint64_t* src, const int64_t* src_off, const 
 extern "C" {
 
 int pyg_check_device_error(pyg_ctx* c) {
+  PYG_ON_DEVICE(c);
   int32_t e = 0;
   PYG_CUDA(cudaMemcpyAsync(&e, c->hd.error, 4, cudaMemcpyDeviceToHost, c->stream));
   PYG_CUDA(cudaMemsetAsync(c->hd.error, 0, 4, c->stream));
@@ -610,6 +611,7 @@ int pyg_check_device_error(pyg_ctx* c) {
 }
 
 int pyg_stats(pyg_ctx* c, int64_t* out, int32_t reset) {
+  PYG_ON_DEVICE(c);
   if (!c || !out) return PYG_EINVAL;
   PYG_CUDA(cudaSetDevice(c->device));
   PYG_CUDA(cudaMemcpyAsync(out, c->hd.stats, 64, cudaMemcpyDeviceToHost, c->stream));
@@ -621,6 +623,7 @@ int pyg_stats(pyg_ctx* c, int64_t* out, int32_t reset) {
 int pyg_lookup_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off,
                          const int64_t* d_hash_off, const uint64_t* d_hashes, int32_t R,
                          const int32_t* d_rep, int32_t with_l3, int64_t* d_match3) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0) return PYG_EINVAL;
   if (R == 0) return PYG_OK;
   k_lookup_batch<<<(R + 127) / 128, 128, 0, c->stream>>>(c->hd, d_tokens, d_tok_off, d_hash_off,
@@ -726,6 +729,7 @@ int pyg_admit_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_t
                         const int32_t* d_role, int32_t R, const int32_t* d_placed_off,
                         const int32_t* d_placed, double now, int32_t speculative,
                         int32_t* d_admitted, int64_t* d_match3) {
+  PYG_ON_DEVICE(c);
   int rc = admit_core(c, d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, R,
                       d_placed_off, d_placed, now, speculative, d_admitted, d_match3, nullptr, 0,
                       nullptr);
@@ -740,6 +744,7 @@ int pyg_admit_shard_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_t
                         const int32_t* d_placed, double now, int32_t speculative,
                         int32_t* d_admitted, int64_t* d_match3, void* d_l2_erased,
                         int64_t l2_cap, int64_t* d_counts) {
+  PYG_ON_DEVICE(c);
   if (!d_counts || (l2_cap && !d_l2_erased)) return PYG_EINVAL;
   return admit_core(c, d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, R, d_placed_off,
                     d_placed, now, speculative, d_admitted, d_match3, d_l2_erased, l2_cap,
@@ -752,6 +757,7 @@ int pyg_shard_l3_resolve_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t
                              const int32_t* d_admitted, int64_t* d_match3,
                              uint64_t* d_l3_hashes, int64_t l3_cap, int64_t l2_cap,
                              int64_t* d_counts) {
+  PYG_ON_DEVICE(c);
   if (!d_counts || (l3_cap && !d_l3_hashes)) return PYG_EINVAL;
   int rc = l3_stage(c, d_tokens, d_tok_off, d_hash_off, d_hashes, R, d_placed_off, d_placed,
                     d_admitted, d_match3, d_l3_hashes, l3_cap, d_counts);
@@ -764,6 +770,7 @@ int pyg_shard_l3_resolve_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t
 
 int pyg_l3_erase_hashes_dev(pyg_ctx* c, const uint64_t* d_hashes, int64_t n,
                             const int64_t* d_count) {
+  PYG_ON_DEVICE(c);
   if (!c || n < 0) return PYG_EINVAL;
   if (!n) return PYG_OK;
   k_l3_erase_list<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(c->hd, d_hashes, n,
@@ -773,6 +780,7 @@ int pyg_l3_erase_hashes_dev(pyg_ctx* c, const uint64_t* d_hashes, int64_t n,
 }
 
 int pyg_dir_clear_dev(pyg_ctx* c, const void* d_records, int64_t n, const int64_t* d_count) {
+  PYG_ON_DEVICE(c);
   if (!c || n < 0) return PYG_EINVAL;
   if (!n) return PYG_OK;
   k_dir_clear<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(
@@ -784,6 +792,7 @@ int pyg_dir_clear_dev(pyg_ctx* c, const void* d_records, int64_t n, const int64_
 int pyg_gather_csr_dev(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_src_off,
                        const int64_t* d_idx, int64_t n_idx, const int64_t* d_dst_off,
                        uint64_t* d_dst) {
+  PYG_ON_DEVICE(c);
   if (!c || n_idx < 0) return PYG_EINVAL;
   if (!n_idx) return PYG_OK;
   if (n_idx > 0x7fffffff) return PYG_EINVAL;
@@ -798,6 +807,7 @@ int pyg_nodes_compose_dev(pyg_ctx* c, int32_t n_rep, const int64_t* d_base_off,
                           const int32_t* d_placed, const pyg_reservation* d_req,
                           const uint8_t* d_hold, int32_t hold_min, int64_t* d_out_off,
                           pyg_reservation* d_out) {
+  PYG_ON_DEVICE(c);
   if (!c || n_rep < 0 || (d_placed_off && (!d_placed || !d_req))) return PYG_EINVAL;
   if (!n_rep) return PYG_OK;
   PYG_CUDA(cudaSetDevice(c->device));
@@ -811,6 +821,7 @@ int pyg_release_hold_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d_
                          const uint64_t* d_hashes, int32_t R, const int32_t* d_placed_off,
                          const int32_t* d_placed, const int32_t* d_admitted,
                          const uint8_t* d_hold, int32_t hold) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0) return PYG_EINVAL;
   if (R == 0 || c->n_rep == 0) return PYG_OK;
   PYG_CUDA(cudaSetDevice(c->device));
@@ -823,6 +834,7 @@ int pyg_release_hold_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d_
 int pyg_release_batch_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d_hash_off,
                           const uint64_t* d_hashes, int32_t R, const int32_t* d_placed_off,
                           const int32_t* d_placed, const int32_t* d_admitted) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0) return PYG_EINVAL;
   if (R == 0 || c->n_rep == 0) return PYG_OK;
   k_release<<<c->n_rep, 256, 0, c->stream>>>(c->hd, d_tok_off, d_hash_off, d_hashes,
@@ -839,6 +851,7 @@ int pyg_release_batch_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d
 extern "C" int pyg_step_host(pyg_ctx* c, const pyg_batch_host* b, const pyg_nodes_host* nd,
                              int32_t mode, double eps, double now, int32_t spec, int32_t release,
                              pyg_decision* out_dec, int32_t* out_adm, int64_t* out_m3) {
+  PYG_ON_DEVICE(c);
   if (!c || !b || !nd || b->n_req < 0 || nd->n_groups < 0) return PYG_EINVAL;
   const int32_t R = b->n_req;
   const int nrep = c->n_rep;

@@ -267,6 +267,7 @@ int pyg_create(const pyg_config* cfg, pyg_ctx** out) {
 void pyg_destroy(pyg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  cudaSetDevice(c->device);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   if (c->stream && c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
   for (auto& t : c->tiers)
@@ -289,12 +290,14 @@ void pyg_destroy(pyg_ctx* c) {
 }
 
 int pyg_set_stream(pyg_ctx* c, void* s) {
+  PYG_ON_DEVICE(c);
   if (!c) return PYG_EINVAL;
   c->stream = static_cast<cudaStream_t>(s);  // NULL = the default (legacy) stream
   return PYG_OK;
 }
 
 int pyg_synchronize(pyg_ctx* c) {
+  PYG_ON_DEVICE(c);
   PYG_CUDA(cudaStreamSynchronize(c->stream));
   return PYG_OK;
 }
@@ -302,6 +305,7 @@ int pyg_synchronize(pyg_ctx* c) {
 int64_t pyg_kernel_launches(pyg_ctx* c) { return c ? c->launches : 0; }
 
 int pyg_set_capacity(pyg_ctx* c, int32_t replica, int64_t l1_capacity, int64_t l2_capacity) {
+  PYG_ON_DEVICE(c);
   if (!c || replica < 0 || replica >= c->n_rep || l1_capacity < 0 || l2_capacity < 0)
     return PYG_EINVAL;
   const int64_t caps[2] = {l1_capacity, l2_capacity};

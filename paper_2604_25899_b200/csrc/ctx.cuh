@@ -74,6 +74,21 @@ int sm_count(int dev);              // SM count of a device (cached per device)
     if (_rc != PYG_OK) return _rc;                                      \
   } while (0)
 
+// Every entry point runs on its ctx's device, whatever the caller's current device is
+// (a single host thread may drive ctxs on several GPUs).  void entry points skip the check.
+#define PYG_ON_DEVICE(c)                                                \
+  do {                                                                  \
+    if (c) {                                                            \
+      int _d = -1;                                                      \
+      if (cudaGetDevice(&_d) != cudaSuccess || _d != (c)->device) {     \
+        if (cudaSetDevice((c)->device) != cudaSuccess) {                \
+          PYG_ON_DEVICE_FAIL;                                           \
+        }                                                               \
+      }                                                                 \
+    }                                                                   \
+  } while (0)
+#define PYG_ON_DEVICE_FAIL return PYG_ECUDA
+
 #define PYG_LAUNCHED(c)                                                 \
   do {                                                                  \
     pyg_host::count_launch(c);                                          \

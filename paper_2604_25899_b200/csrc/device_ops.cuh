@@ -350,7 +350,7 @@ struct EvictOut {
 // shortest prefix with sum(size) >= excess is erased (all candidates if that is
 // unsatisfiable).  freed ids are written in eviction order to out_ids[0..cap).
 // smem_keys: kSmemSortCap*12 bytes or nullptr (then the tier scratch is used);
-// sm: >= 48 int64.
+// sm: >= 41 int64.
 //
 // The candidates are gathered once (key = order(last_access) + class | size |
 // log index, log index = id order).  Then, group by group -- a group = the
@@ -377,7 +377,8 @@ __device__ __forceinline__ EvGroup grp_min(EvGroup a, EvGroup b) {
   return grp_less(a.cls, a.h, b.cls, b.h) ? a : b;
 }
 
-__device__ inline EvGroup block_grp_min(EvGroup g, int64_t* sm) {
+__device__ inline EvGroup block_grp_min(EvGroup g) {
+  __shared__ int64_t sm[3 * 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -564,7 +565,7 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
         if (!first && !grp_less(pc, ph, cl, h)) continue;
         loc = grp_min(loc, EvGroup{cl, h, static_cast<int64_t>((klo[i] >> 24) & 0x7fu)});
       }
-      const EvGroup m = block_grp_min(loc, sm + 8);
+      const EvGroup m = block_grp_min(loc);
       if (m.cls == 2u) {  // nothing left: every candidate is freed, unsatisfied
         done = true;
         break;

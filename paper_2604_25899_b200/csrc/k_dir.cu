@@ -431,6 +431,7 @@ int ensure_dir(pyg_ctx* c) {
 extern "C" {
 
 int pyg_set_shard(pyg_ctx* c, int32_t rep_base, int32_t n_global) {
+  PYG_ON_DEVICE(c);
   if (!c || rep_base < 0 || n_global < rep_base + c->n_rep || n_global > 64 * kDirMaxWords) {
     set_error("pyg_set_shard: need 0 <= rep_base, rep_base + n_replicas <= n_global <= 1024");
     return PYG_EINVAL;
@@ -445,6 +446,7 @@ int pyg_set_shard(pyg_ctx* c, int32_t rep_base, int32_t n_global) {
 }
 
 int pyg_dir_export_dev(pyg_ctx* c, void* d_records, int64_t cap, int64_t* n_out) {
+  PYG_ON_DEVICE(c);
   if (!c || cap < 0 || (cap && !d_records) || !n_out) return PYG_EINVAL;
   void* sp;
   int rc = scratch(c, 64, &sp);
@@ -465,6 +467,7 @@ int pyg_dir_export_dev(pyg_ctx* c, void* d_records, int64_t cap, int64_t* n_out)
 int64_t pyg_dir_export_cap(pyg_ctx* c) { return c ? export_cap(c) : 0; }
 
 int pyg_dir_build_dev(pyg_ctx* c, const void* d_records, int64_t n) {
+  PYG_ON_DEVICE(c);
   if (!c || n < 0 || (n && !d_records)) return PYG_EINVAL;
   return dir_build(c, static_cast<const DirRecord*>(d_records), n);
 }
@@ -475,6 +478,7 @@ int pyg_staged_matrix_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d
                                  const int32_t* d_group, int32_t n_groups,
                                  const int32_t* d_cand_off, const int32_t* d_cand,
                                  int32_t max_cand, int32_t* d_staged) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0 || max_cand < 0) return PYG_EINVAL;
   if (R == 0 || max_cand == 0) return PYG_OK;
   int rc = ensure_dir(c);

@@ -485,6 +485,7 @@ extern "C" {
 
 int pyg_hash_offsets_dev(pyg_ctx* c, const int64_t* d_tok_off, int32_t R, int64_t* d_hash_off,
                          int64_t* total) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0) return PYG_EINVAL;
   size_t tmp = 0;
   PYG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, static_cast<int64_t*>(nullptr), d_hash_off,
@@ -587,6 +588,7 @@ extern "C" {
 
 int pyg_hash_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok_off, int32_t R,
                        const int64_t* d_hash_off, uint64_t* d_hashes) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0) return PYG_EINVAL;
   if (R == 0) return PYG_OK;
   return hash_launch<false>(c, d_tokens, d_tok_off, R, d_hash_off, d_hashes, GatherSrc{});
@@ -596,6 +598,7 @@ int pyg_assemble_hash_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
                           const pyg_segment* d_segs, int64_t n_segs, const uint64_t* d_pool,
                           int64_t n_tokens, int64_t* d_tok_off, uint64_t* d_tokens,
                           int64_t* d_hash_off, uint64_t* d_hashes) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0 || n_segs < 0 || n_tokens < 0) return PYG_EINVAL;
   int rc = pyg_host::assemble_offsets(c, R, d_seg_off, d_segs, d_tok_off);
   if (rc) return rc;
@@ -621,12 +624,14 @@ int pyg_assemble_hash_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
 }
 
 int pyg_set_hash_split(pyg_ctx* c, int64_t min_tokens) {
+  PYG_ON_DEVICE(c);
   if (!c || min_tokens < 0) return PYG_EINVAL;
   c->split_min = (min_tokens + 3) & ~int64_t{3};
   return PYG_OK;
 }
 
 int pyg_set_hash_ctas(pyg_ctx* c, int32_t n_ctas) {
+  PYG_ON_DEVICE(c);
   if (!c || n_ctas < 0) return PYG_EINVAL;
   c->hash_ctas = n_ctas;
   return PYG_OK;

@@ -236,6 +236,7 @@ int pyg_next_use_dev(pyg_ctx* c, const pyg_path_node* d_nodes, int32_t n_nodes,
                      const int32_t* d_ch_list, int32_t n_cursors, const int32_t* d_frame_off,
                      const int32_t* d_frame_node, const int32_t* d_frame_prog, int32_t n_roles,
                      double* d_dist, uint64_t* d_future) {
+  PYG_ON_DEVICE(c);
   if (!c || n_nodes < 0 || n_cursors < 0 || n_roles < 1 || n_roles > 64) return PYG_EINVAL;
   if (!n_cursors) return PYG_OK;
   auto al = [](size_t x) { return (x + 255) & ~size_t{255}; };
@@ -261,6 +262,7 @@ int pyg_next_use_dev(pyg_ctx* c, const pyg_path_node* d_nodes, int32_t n_nodes,
 int pyg_block_next_use_dev(pyg_ctx* c, int32_t replica, int32_t tier, const int32_t* d_wf_cursor,
                            int32_t n_wf, const double* d_dist, int32_t n_roles, double* d_out,
                            int64_t cap, int64_t* d_count) {
+  PYG_ON_DEVICE(c);
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
   if (rc) return rc;
@@ -273,6 +275,7 @@ int pyg_block_next_use_dev(pyg_ctx* c, int32_t replica, int32_t tier, const int3
 int pyg_registry_from_cursors_dev(pyg_ctx* c, int32_t n, int32_t max_wf, const int32_t* d_wf,
                                   const int32_t* d_cursor, const uint64_t* d_future,
                                   const int32_t* d_current_role) {
+  PYG_ON_DEVICE(c);
   if (!c || n < 0 || max_wf < 0) return PYG_EINVAL;
   int rc = reg_ensure(c, max_wf);
   if (rc) return rc;

@@ -84,12 +84,12 @@ int assemble_offsets(pyg_ctx* c, int32_t R, const int64_t* d_seg_off, const pyg_
 extern "C" int pyg_assemble_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
                                 const pyg_segment* d_segs, const uint64_t* d_pool,
                                 int64_t* d_tok_off, uint64_t* d_tokens) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0) return PYG_EINVAL;
   int rc = assemble_offsets(c, R, d_seg_off, d_segs, d_tok_off);
   if (rc) return rc;
   if (R) {
-    static int n_sm = 0;
-    if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
+    const int n_sm = pyg_host::sm_count(c->device);
     k_gather<<<std::min(R, 8 * n_sm), 256, 0, c->stream>>>(R, d_seg_off, d_segs, d_pool, d_tok_off,
                                                            d_tokens);
     PYG_LAUNCHED(c);

@@ -635,6 +635,7 @@ extern "C" int pyg_route_batch_dev(pyg_ctx* c, int32_t mode, const pyg_nodes_dev
                                    const int32_t* d_cand, int32_t max_cand,
                                    const int32_t* d_staged, double eps, pyg_decision* d_out,
                                    int32_t* d_placed_off, int32_t* d_placed) {
+  PYG_ON_DEVICE(c);
   if (!c || !nodes || R < 0 || G < 0) return PYG_EINVAL;
   if (mode != PYG_ROUTE_SNAPSHOT && mode != PYG_ROUTE_SEQ_COMMIT) {
     set_error("unknown route mode");

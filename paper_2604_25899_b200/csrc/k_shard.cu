@@ -364,6 +364,7 @@ int pyg_ipc_export(const void* d_ptr, void* handle_out, int64_t* offset_out) {
 }
 
 int pyg_ipc_import(pyg_ctx* c, const void* handle, int64_t offset, void** d_ptr_out) {
+  PYG_ON_DEVICE(c);
   if (!c || !handle || !d_ptr_out) return PYG_EINVAL;
   const std::string key(static_cast<const char*>(handle), sizeof(cudaIpcMemHandle_t));
   auto& m = ipc_cache();
@@ -387,6 +388,7 @@ int pyg_shard_recv_plan_dev(pyg_ctx* c, int32_t R_total, const pyg_decision* d_d
                             int64_t cap, int32_t* d_recv_gidx, int64_t* d_recv_count,
                             int64_t* d_recv_toff, int64_t* d_recv_hoff, int32_t* d_recv_wf,
                             int32_t* d_recv_role) {
+  PYG_ON_DEVICE(c);
   if (!c || R_total < 0 || cap < 0 || !c->sharded) return PYG_EINVAL;
   const int32_t lo = c->rep_base, hi = c->rep_base + c->n_rep;
   size_t t1 = 0, t2 = 0;
@@ -436,6 +438,7 @@ int pyg_shard_recv_plan_dev(pyg_ctx* c, int32_t R_total, const pyg_decision* d_d
 int pyg_shard_pack_dev(pyg_ctx* c, const pyg_reservation* d_req, const int32_t* d_group,
                        const int32_t* d_staged, int32_t R, int32_t mc, int32_t s16,
                        int32_t* d_rows) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0 || mc < 0) return PYG_EINVAL;
   if (!R) return PYG_OK;
   k_pack<<<(R + 255) / 256, 256, 0, c->stream>>>(d_req, d_group, d_staged, R, mc, s16, d_rows);
@@ -445,6 +448,7 @@ int pyg_shard_pack_dev(pyg_ctx* c, const pyg_reservation* d_req, const int32_t* 
 
 int pyg_shard_unpack_dev(pyg_ctx* c, const int32_t* d_rows, int32_t R, int32_t mc, int32_t s16,
                          pyg_reservation* d_req, int32_t* d_group, int32_t* d_staged) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0 || mc < 0) return PYG_EINVAL;
   if (!R) return PYG_OK;
   k_unpack<<<(R + 255) / 256, 256, 0, c->stream>>>(d_rows, R, mc, s16, d_req, d_group, d_staged);
@@ -455,6 +459,7 @@ int pyg_shard_unpack_dev(pyg_ctx* c, const int32_t* d_rows, int32_t R, int32_t m
 int pyg_shard_unpack_peer_dev(pyg_ctx* c, const int64_t* d_rows_of, int32_t world,
                               const int64_t* d_req_off, int32_t R, int32_t mc, int32_t s16,
                               pyg_reservation* d_req, int32_t* d_group, int32_t* d_staged) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0 || mc < 0 || world < 1) return PYG_EINVAL;
   if (!R) return PYG_OK;
   k_unpack_peer<<<(R + 255) / 256, 256, 0, c->stream>>>(d_rows_of, world, d_req_off, R, mc, s16,
@@ -465,6 +470,7 @@ int pyg_shard_unpack_peer_dev(pyg_ctx* c, const int64_t* d_rows_of, int32_t worl
 
 int pyg_shard_signal_dev(pyg_ctx* c, const int64_t* d_flag_of, int32_t world, int32_t me,
                          int64_t seq) {
+  PYG_ON_DEVICE(c);
   if (!c || world < 1 || world > 1024 || me < 0 || me >= world) return PYG_EINVAL;
   k_signal<<<1, 32 * ((world + 31) / 32), 0, c->stream>>>(d_flag_of, world, me, seq);
   PYG_LAUNCHED(c);
@@ -472,6 +478,7 @@ int pyg_shard_signal_dev(pyg_ctx* c, const int64_t* d_flag_of, int32_t world, in
 }
 
 int pyg_shard_wait_dev(pyg_ctx* c, const int64_t* d_flags, int32_t world, int64_t seq) {
+  PYG_ON_DEVICE(c);
   if (!c || world < 1 || world > 1024) return PYG_EINVAL;
   k_wait<<<1, 32 * ((world + 31) / 32), 0, c->stream>>>(d_flags, world, seq, c->hd.error);
   PYG_LAUNCHED(c);
@@ -483,6 +490,7 @@ int pyg_shard_pull_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world,
                        const int64_t* d_recv_count, const int64_t* d_recv_toff,
                        const int64_t* d_recv_hoff, uint64_t* d_tok_out, int64_t tok_cap,
                        uint64_t* d_hash_out, int64_t hash_cap) {
+  PYG_ON_DEVICE(c);
   if (!c || world < 1) return PYG_EINVAL;
   k_pull<<<592, 256, 0, c->stream>>>(d_peers, world, d_req_off, d_recv_gidx, d_recv_count,
                                      d_recv_toff, d_recv_hoff, d_tok_out, d_hash_out, tok_cap,
@@ -494,6 +502,7 @@ int pyg_shard_pull_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world,
 int pyg_shard_local_placed_dev(pyg_ctx* c, const int32_t* d_placed_off, const int32_t* d_placed,
                                const int32_t* d_recv_gidx, const int64_t* d_recv_count,
                                int32_t* d_p_off, int32_t* d_p_loc) {
+  PYG_ON_DEVICE(c);
   if (!c || !c->sharded) return PYG_EINVAL;
   k_local_placed<<<148, 256, 0, c->stream>>>(d_placed_off, d_placed, c->rep_base, c->n_rep,
                                              d_recv_gidx, d_recv_count, d_p_off, d_p_loc);
@@ -502,6 +511,7 @@ int pyg_shard_local_placed_dev(pyg_ctx* c, const int32_t* d_placed_off, const in
 }
 
 int pyg_shard_apply_lists_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world, int32_t me) {
+  PYG_ON_DEVICE(c);
   if (!c || world < 1) return PYG_EINVAL;
   k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, 0, world, 1);
   PYG_LAUNCHED(c);
@@ -510,6 +520,7 @@ int pyg_shard_apply_lists_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world
 
 int pyg_shard_apply_lists_range_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world,
                                     int32_t me, int32_t l3_lo, int32_t l3_hi, int32_t with_l2) {
+  PYG_ON_DEVICE(c);
   if (!c || world < 1 || l3_lo < 0 || l3_hi > world) return PYG_EINVAL;
   if (l3_lo >= l3_hi && !with_l2) return PYG_OK;
   k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, l3_lo, l3_hi, with_l2);
@@ -520,6 +531,7 @@ int pyg_shard_apply_lists_range_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t
 int pyg_shard_results_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world,
                           const int64_t* d_rep_off, const pyg_decision* d_dec, int64_t req_base,
                           int32_t R_local, int32_t* d_admitted, int64_t* d_match3) {
+  PYG_ON_DEVICE(c);
   if (!c || world < 1 || R_local < 0) return PYG_EINVAL;
   if (!R_local) return PYG_OK;
   k_results<<<(R_local + 255) / 256, 256, 0, c->stream>>>(d_peers, world, d_rep_off, d_dec,

@@ -79,6 +79,7 @@ extern "C" int pyg_stage_plan_dev(pyg_ctx* c, const uint64_t* d_tokens, const in
                                   const int32_t* d_cand_off, const int32_t* d_cand,
                                   int32_t max_cand, const int32_t* d_replica_id,
                                   const int8_t* d_gpu_idle, pyg_stage_action* d_out) {
+  PYG_ON_DEVICE(c);
   if (!c || R < 0 || max_cand < 0) return PYG_EINVAL;
   if (!R) return PYG_OK;
   auto al = [](size_t x) { return (x + 255) & ~size_t{255}; };

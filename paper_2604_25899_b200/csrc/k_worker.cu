@@ -150,14 +150,12 @@ int pyg_form_batch_dev(pyg_ctx* c, int32_t n_sets, const int64_t* d_off,
                        const pyg_queue_item* d_items, const int64_t* d_active_reservation,
                        const int64_t* d_capacity, double now, double aging_rate, int32_t* d_order,
                        int32_t* d_n_admitted) {
+  PYG_ON_DEVICE(c);
   if (!c || n_sets < 0) return PYG_EINVAL;
   if (!n_sets) return PYG_OK;
   const int smem = kMaxQueue * static_cast<int>(sizeof(QKey));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_form_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  // the attribute is per device: set on every call (cheap) rather than cached per process
+  PYG_CUDA(cudaFuncSetAttribute(k_form_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_form_batch<<<n_sets, 512, smem, c->stream>>>(d_off, d_items, d_active_reservation, d_capacity, now,
                                               aging_rate, d_order, d_n_admitted, c->hd.error);
   PYG_LAUNCHED(c);
@@ -167,6 +165,7 @@ int pyg_form_batch_dev(pyg_ctx* c, int32_t n_sets, const int64_t* d_off,
 int pyg_preemption_victim_dev(pyg_ctx* c, int32_t n_sets, const int64_t* d_off,
                               const pyg_queue_item* d_items, double now, double aging_rate,
                               int32_t* d_victim) {
+  PYG_ON_DEVICE(c);
   if (!c || n_sets < 0) return PYG_EINVAL;
   if (!n_sets) return PYG_OK;
   k_victim<<<n_sets, 256, 0, c->stream>>>(d_off, d_items, now, aging_rate, d_victim);

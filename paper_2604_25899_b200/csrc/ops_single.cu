@@ -417,6 +417,7 @@ extern "C" {
 
 int pyg_chain_hashes(pyg_ctx* c, const uint64_t* tokens, int64_t n, uint64_t* out,
                      int64_t* n_out) {
+  PYG_ON_DEVICE(c);
   if (!c || n < 0 || (n && (!tokens || !out))) return PYG_EINVAL;
   uint64_t *dt, *dh;
   int rc = upload_tokens(c, tokens, n, &dt, &dh);
@@ -431,6 +432,7 @@ int pyg_chain_hashes(pyg_ctx* c, const uint64_t* tokens, int64_t n, uint64_t* ou
 
 int pyg_tier_put(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t hash, int64_t s, int64_t e,
                  int32_t wf, int32_t role, double now, int32_t pin, uint64_t* out_id) {
+  PYG_ON_DEVICE(c);
   if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
@@ -453,6 +455,7 @@ int pyg_tier_put(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t hash, int64
 }
 
 int pyg_tier_erase(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t id) {
+  PYG_ON_DEVICE(c);
   if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
@@ -465,6 +468,7 @@ int pyg_tier_erase(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t id) {
 
 int pyg_tier_find(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t hash, pyg_block* out,
                   int32_t* found) {
+  PYG_ON_DEVICE(c);
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
   if (rc) return rc;
@@ -486,6 +490,7 @@ int pyg_tier_find(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t hash, pyg_
 
 int pyg_tier_stats(pyg_ctx* c, int32_t replica, int32_t tier, int64_t* occ, int64_t* cap,
                    int64_t* nb) {
+  PYG_ON_DEVICE(c);
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
   if (rc) return rc;
@@ -499,6 +504,7 @@ int pyg_tier_stats(pyg_ctx* c, int32_t replica, int32_t tier, int64_t* occ, int6
 
 int pyg_tier_dump(pyg_ctx* c, int32_t replica, int32_t tier, pyg_block* out, int64_t cap,
                   int64_t* n) {
+  PYG_ON_DEVICE(c);
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
   if (rc) return rc;
@@ -522,6 +528,7 @@ int pyg_tier_dump(pyg_ctx* c, int32_t replica, int32_t tier, pyg_block* out, int
 
 int pyg_matched_prefix(pyg_ctx* c, int32_t replica, int32_t tier, const uint64_t* tokens,
                        int64_t n, int64_t* out) {
+  PYG_ON_DEVICE(c);
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
   if (rc) return rc;
@@ -538,6 +545,7 @@ int pyg_matched_prefix(pyg_ctx* c, int32_t replica, int32_t tier, const uint64_t
 
 int pyg_lookup(pyg_ctx* c, int32_t replica, const uint64_t* tokens, int64_t n, int32_t with_l3,
                int64_t out[3]) {
+  PYG_ON_DEVICE(c);
   if (!c || replica < 0 || replica >= c->n_rep || n < 0 || (n && !tokens) || !out) {
     set_error("pyg_lookup: bad arguments");
     return PYG_EINVAL;
@@ -556,6 +564,7 @@ int pyg_lookup(pyg_ctx* c, int32_t replica, const uint64_t* tokens, int64_t n, i
 
 int pyg_insert_chain(pyg_ctx* c, int32_t replica, int32_t tier, const uint64_t* tokens, int64_t n,
                      int64_t upto, int32_t wf, int32_t role, double now, int32_t pin) {
+  PYG_ON_DEVICE(c);
   if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, true, &ti);
@@ -574,6 +583,7 @@ int pyg_insert_chain(pyg_ctx* c, int32_t replica, int32_t tier, const uint64_t* 
 
 int pyg_unpin_chain(pyg_ctx* c, int32_t replica, const uint64_t* tokens, int64_t n,
                     int64_t upto) {
+  PYG_ON_DEVICE(c);
   if (!c || replica < 0 || replica >= c->n_rep || n < 0 || (n && !tokens)) return PYG_EINVAL;
   const int64_t nput = blocks_upto(n, upto, c->B);
   if (nput == 0) return PYG_OK;
@@ -588,6 +598,7 @@ int pyg_unpin_chain(pyg_ctx* c, int32_t replica, const uint64_t* tokens, int64_t
 
 int pyg_erase_chain_span(pyg_ctx* c, int32_t replica, int32_t tier, const uint64_t* tokens,
                          int64_t n, int64_t from, int64_t to) {
+  PYG_ON_DEVICE(c);
   if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, false, &ti);
@@ -603,6 +614,7 @@ int pyg_erase_chain_span(pyg_ctx* c, int32_t replica, int32_t tier, const uint64
 }
 
 int pyg_add_decode_tokens(pyg_ctx* c, int32_t replica, int64_t n) {
+  PYG_ON_DEVICE(c);
   if (!c || replica < 0 || replica >= c->n_rep) return PYG_EINVAL;
   k_add_decode<<<1, 1, 0, c->stream>>>(c->hd, replica, n);
   PYG_LAUNCHED(c);
@@ -610,6 +622,7 @@ int pyg_add_decode_tokens(pyg_ctx* c, int32_t replica, int64_t n) {
 }
 
 int pyg_l1_occupancy(pyg_ctx* c, int32_t replica, int64_t* out) {
+  PYG_ON_DEVICE(c);
   if (!c || replica < 0 || replica >= c->n_rep || !out) return PYG_EINVAL;
   TierDev t;
   int rc = read_tier(c, 2 * replica, &t);
@@ -621,6 +634,7 @@ int pyg_l1_occupancy(pyg_ctx* c, int32_t replica, int64_t* out) {
 }
 
 int pyg_set_replica_off(pyg_ctx* c, int32_t replica, int32_t off) {
+  PYG_ON_DEVICE(c);
   if (!c || replica < 0 || replica >= c->n_rep) return PYG_EINVAL;
   int32_t v = off ? 1 : 0;
   PYG_CUDA(cudaMemcpyAsync(c->hd.off + replica, &v, 4, cudaMemcpyHostToDevice, c->stream));
@@ -653,6 +667,7 @@ static int reg_grow(pyg_ctx* c, int32_t wf) {
 
 
 int pyg_registry_update(pyg_ctx* c, int32_t wf, uint64_t mask) {
+  PYG_ON_DEVICE(c);
   if (!c || wf < 0) return PYG_EINVAL;
   int rc = reg_grow(c, wf);
   if (rc) return rc;
@@ -663,6 +678,7 @@ int pyg_registry_update(pyg_ctx* c, int32_t wf, uint64_t mask) {
 
 int pyg_registry_update_batch_dev(pyg_ctx* c, int32_t n, const int32_t* d_wf,
                                   const uint64_t* d_mask, int32_t max_wf) {
+  PYG_ON_DEVICE(c);
   if (!c || n < 0 || max_wf < 0) return PYG_EINVAL;
   if (!n) return PYG_OK;
   PYG_CUDA(cudaSetDevice(c->device));
@@ -674,6 +690,7 @@ int pyg_registry_update_batch_dev(pyg_ctx* c, int32_t n, const int32_t* d_wf,
 }
 
 int pyg_registry_drop(pyg_ctx* c, int32_t wf) {
+  PYG_ON_DEVICE(c);
   if (!c || wf < 0) return PYG_EINVAL;
   if (wf >= c->hd.reg_cap) return PYG_OK;
   k_reg_set<<<1, 1, 0, c->stream>>>(c->hd, wf, 0, 0);
@@ -684,6 +701,7 @@ int pyg_registry_drop(pyg_ctx* c, int32_t wf) {
 int pyg_evict_for_space(pyg_ctx* c, int32_t replica, int32_t tier, int64_t needed,
                         int32_t speculative, uint64_t* freed, int64_t cap, int64_t* n_freed,
                         int64_t* freed_tokens, int32_t* satisfied) {
+  PYG_ON_DEVICE(c);
   if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   int ti;
   int rc = tier_index(c, replica, tier, true, &ti);
@@ -696,7 +714,7 @@ int pyg_evict_for_space(pyg_ctx* c, int32_t replica, int32_t tier, int64_t neede
   auto* dstats = static_cast<int64_t*>(sp);
   auto* dids = reinterpret_cast<uint64_t*>(dstats + 4);
   const size_t smem = kSmemSortCap * 12;
-  cudaFuncSetAttribute(k_evict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  PYG_CUDA(cudaFuncSetAttribute(k_evict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_evict<<<1, 1024, smem, c->stream>>>(c->hd, ti, tier == 0 ? replica : -1, needed,
                                         speculative, dids, room, dstats);
   PYG_LAUNCHED(c);
@@ -769,6 +787,7 @@ static int complete_reps(pyg_ctx* c, const std::vector<int32_t>& reps, int32_t w
 
 int pyg_complete(pyg_ctx* c, int32_t replica, int32_t wf, uint64_t future, int32_t profiled,
                  double now, int64_t* n_actions) {
+  PYG_ON_DEVICE(c);
   if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   if (!c || replica < 0 || replica >= c->n_rep) return PYG_EINVAL;
   if (!profiled) {  // req.unprofiled() => no actions (manager.cpp:28)
@@ -779,6 +798,7 @@ int pyg_complete(pyg_ctx* c, int32_t replica, int32_t wf, uint64_t future, int32
 }
 
 int pyg_l3_dead_sweep(pyg_ctx* c, int32_t wf, uint64_t future) {
+  PYG_ON_DEVICE(c);
   if (!c) return PYG_EINVAL;
   k_l3_dead_sweep<<<148, 256, 0, c->stream>>>(c->hd, wf, future);
   PYG_LAUNCHED(c);
@@ -787,6 +807,7 @@ int pyg_l3_dead_sweep(pyg_ctx* c, int32_t wf, uint64_t future) {
 }
 
 int pyg_completion_policy(pyg_ctx* c, int32_t wf, uint64_t future, double now) {
+  PYG_ON_DEVICE(c);
   if (c) dir_touch(c);  // may change an L2 tier: the directory is rebuilt before use
   if (!c || wf < 0) return PYG_EINVAL;
   int rc = pyg_registry_update(c, wf, future);  // engine.cpp:1064-1065
@@ -805,6 +826,7 @@ int pyg_completion_policy(pyg_ctx* c, int32_t wf, uint64_t future, double now) {
 int pyg_route(pyg_ctx* c, int32_t nn, const int32_t* rid, const int64_t* kv, const int64_t* off,
               const pyg_reservation* asg, const int64_t* staged, const pyg_reservation* req,
               double eps, pyg_decision* out) {
+  PYG_ON_DEVICE(c);
   if (!c || nn < 0 || !req || !out || (nn && (!rid || !kv || !off || !staged))) return PYG_EINVAL;
   const int64_t na = nn ? off[nn] : 0;
   const size_t bytes = nn * 4 + nn * 8 * 3 + 8 + na * sizeof(pyg_reservation) + 64 + 256;
@@ -839,6 +861,7 @@ int pyg_route(pyg_ctx* c, int32_t nn, const int32_t* rid, const int64_t* kv, con
 
 int pyg_route_least_outstanding(pyg_ctx* c, int32_t nn, const int32_t* rid, const int64_t* off,
                                 int32_t* out) {
+  PYG_ON_DEVICE(c);
   // route_least_outstanding (router.cpp:52-62): fewest assigned, ties to lowest id.
   // Evaluated with the route kernel: headroom = -assigned count, staged 0.
   if (!c || nn < 0 || !out) return PYG_EINVAL;
