@@ -278,12 +278,13 @@ int pyg_nodes_compose_dev(pyg_ctx* ctx, int32_t n_rep, const int64_t* d_base_off
                           const int32_t* d_placed, const pyg_reservation* d_req,
                           const uint8_t* d_hold, int32_t hold_min, int64_t* d_out_off,
                           pyg_reservation* d_out);
-/* pyg_release_batch_dev restricted to requests with d_hold[r] == hold (their completion
-   step): unpin_chain(seq, len) of each (hierarchy.cpp:132-142). */
+/* pyg_release_batch_dev restricted to requests with d_hold[i] == hold (their completion
+   step), i = d_hold_index[r] (NULL: i = r; the sharded step maps receive slots to global
+   request indices): unpin_chain(seq, len) of each (hierarchy.cpp:132-142). */
 int pyg_release_hold_dev(pyg_ctx* ctx, const int64_t* d_tok_off, const int64_t* d_hash_off,
                          const uint64_t* d_hashes, int32_t n_req, const int32_t* d_placed_off,
                          const int32_t* d_placed, const int32_t* d_admitted,
-                         const uint8_t* d_hold, int32_t hold);
+                         const uint8_t* d_hold, int32_t hold, const int32_t* d_hold_index);
 /* FutureRegistry::update (manager.cpp:13-23) for n DISTINCT workflows at once (a burst's
    issue-time updates, engine.cpp:605-609, last write per workflow); max_wf >= every id. */
 int pyg_registry_update_batch_dev(pyg_ctx* ctx, int32_t n, const int32_t* d_wf,

@@ -103,6 +103,15 @@ def apply_warm_oracle(o, caches, l3, reg, trace, ops):
             o.l3_dead_sweep(l3, w, mask)
         elif op[0] == "reg":
             o.reg_update(reg, op[1], op[2])
+        elif op[0] == "l3put":  # TierStore::put into the shared L3 (hierarchy.cpp:44-66)
+            _, r, upto, wf, role, now = op
+            p = trace.prompt(r)
+            B = o.B
+            for i, h in enumerate(o.chain_hashes(p)):
+                s0, e0 = i * B, min((i + 1) * B, len(p))
+                if e0 > upto:
+                    break
+                o.put(caches[0], l3, 2, int(h), s0, e0, wf, role, now, 0)
         elif op[0] == "esp":
             _, n, tier, r, frm, to = op
             o.erase_chain_span(caches[n], None, tier, trace.prompt(r), frm, to)

@@ -136,7 +136,7 @@ _sig("pyg_shard_local_placed_dev", vp, vp, vp, vp, vp, vp, vp)
 _sig("pyg_stats", vp, vp, i32)
 _sig("pyg_set_hash_split", vp, i64)
 _sig("pyg_nodes_compose_dev", vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp)
-_sig("pyg_release_hold_dev", vp, vp, vp, vp, i32, vp, vp, vp, vp, i32)
+_sig("pyg_release_hold_dev", vp, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp)
 _sig("pyg_registry_update_batch_dev", vp, i32, vp, vp, i32)
 _sig("pyg_shard_apply_lists_dev", vp, vp, i32, i32)
 _sig("pyg_shard_apply_lists_range_dev", vp, vp, i32, i32, i32, i32, i32)

@@ -485,13 +485,13 @@ __global__ void k_l3_final(CtxDev c, L3Args a, int64_t* match3, uint64_t* list, 
 __global__ void k_release(CtxDev c, const int64_t* tok_off, const int64_t* hash_off,
                           const uint64_t* hashes, const int32_t* placed_off,
                           const int32_t* placed, const int32_t* admitted,
-                          const uint8_t* hold, int hold_val) {
+                          const uint8_t* hold, int hold_val, const int32_t* hold_index) {
   const int rep = blockIdx.x;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const TierDev& t = c.tiers[2 * rep];
   for (int32_t k = placed_off[rep] + w; k < placed_off[rep + 1]; k += nw) {
     const int r = placed[k];
-    if (admitted[r] != 1 || (hold && hold[r] != hold_val)) continue;
+    if (admitted[r] != 1 || (hold && hold[hold_index ? hold_index[r] : r] != hold_val)) continue;
     const uint64_t* hs = hashes + hash_off[r];
     const int64_t nh = hash_off[r + 1] - hash_off[r];
     for (int64_t i = lane; i < nh; i += 32) {
@@ -820,13 +820,14 @@ int pyg_nodes_compose_dev(pyg_ctx* c, int32_t n_rep, const int64_t* d_base_off,
 int pyg_release_hold_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d_hash_off,
                          const uint64_t* d_hashes, int32_t R, const int32_t* d_placed_off,
                          const int32_t* d_placed, const int32_t* d_admitted,
-                         const uint8_t* d_hold, int32_t hold) {
+                         const uint8_t* d_hold, int32_t hold, const int32_t* d_hold_index) {
   PYG_ON_DEVICE(c);
   if (!c || R < 0) return PYG_EINVAL;
   if (R == 0 || c->n_rep == 0) return PYG_OK;
   PYG_CUDA(cudaSetDevice(c->device));
   k_release<<<c->n_rep, 256, 0, c->stream>>>(c->hd, d_tok_off, d_hash_off, d_hashes,
-                                             d_placed_off, d_placed, d_admitted, d_hold, hold);
+                                             d_placed_off, d_placed, d_admitted, d_hold, hold,
+                                             d_hold_index);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -838,7 +839,8 @@ int pyg_release_batch_dev(pyg_ctx* c, const int64_t* d_tok_off, const int64_t* d
   if (!c || R < 0) return PYG_EINVAL;
   if (R == 0 || c->n_rep == 0) return PYG_OK;
   k_release<<<c->n_rep, 256, 0, c->stream>>>(c->hd, d_tok_off, d_hash_off, d_hashes,
-                                             d_placed_off, d_placed, d_admitted, nullptr, 0);
+                                             d_placed_off, d_placed, d_admitted, nullptr, 0,
+                                             nullptr);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

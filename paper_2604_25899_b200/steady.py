@@ -162,7 +162,7 @@ class Steady:
             check(_lib._lib.pyg_release_hold_dev(self.ctx.h, _ptr(b.b.tok_off),
                                                  _ptr(b.b.hash_off), _ptr(b.b.hashes), b.R,
                                                  _ptr(o.placed_off), _ptr(o.placed),
-                                                 _ptr(o.admitted), _ptr(b.hold), h))
+                                                 _ptr(o.admitted), _ptr(b.hold), h, None))
 
     def compose_nodes(self, prev: Burst | None, k):
         """node table of step k: base + burst k-1's placements still held (hold 2)."""
@@ -202,18 +202,16 @@ class Steady:
 
 
 def warm_ops(warm: W.Trace, cl: W.Cluster, l3_prefixes=128, l2_per_group=64, seed=0):
-    """Deterministic warm-up ops (oracle.step op format + 'esp' = erase_chain_span):
-      * shared-prefix chains staged into L2 (forward staging, manager.cpp:60-100): prefix p
-        of a request of model g on replica p % (replicas of g) of group g;
-      * l3_prefixes prefix chains written to the shared L3 through the completion sweep
-        (RetainAndWriteL3, manager.cpp:44-58) of one carrier workflow on the last replica,
-        whose L2 copies are then erased."""
+    """Deterministic warm-up ops (oracle.step op format):
+      ("ins", replica, 1, r, upto, wf, role, now, 0): request r's blocks up to `upto` staged
+          into a replica's L2 (forward staging, manager.cpp:60-100) -- the first half of a
+          few requests per group, spread over the group's replicas;
+      ("l3put", r, upto, wf, role, now): the same chain blocks put straight into the shared
+          L3 store (TierStore::put, hierarchy.cpp:44-66), as the completion sweep's
+          RetainAndWriteL3 does (manager.cpp:44-58) -- identical on every GPU's replica."""
     rng = np.random.default_rng(seed)
     L = np.diff(warm.tok_off)
     ops = []
-    plen = {}
-    # group-local staging: a few distinct requests per group, their first half (which holds
-    # most of the shared prefix)
     for g in range(len(cl.cand_off) - 1):
         cands = cl.cand[cl.cand_off[g]:cl.cand_off[g + 1]]
         rs = np.nonzero(warm.group == g)[0][:l2_per_group]
@@ -222,39 +220,41 @@ def warm_ops(warm: W.Trace, cl: W.Cluster, l3_prefixes=128, l2_per_group=64, see
             upto = int(min(L[r], max(64, L[r] // 2)))
             ops.append(("ins", rep, 1, int(r), upto, int(warm.wf[r]), int(warm.role[r]), 0.25, 0))
     carrier = 1 << 28
-    last = cl.n_replicas - 1
-    rs = rng.choice(warm.R, size=min(l3_prefixes, warm.R), replace=False)
-    for r in rs:
+    for r in rng.choice(warm.R, size=min(l3_prefixes, warm.R), replace=False):
         upto = int(min(L[r], max(64, L[r] // 2)))
-        ops.append(("ins", last, 1, int(r), upto, carrier, 1, 0.5, 0))
-        plen[int(r)] = upto
-    ops.append(("reg", carrier, 0b10))
-    ops.append(("cmp", carrier, 0b10, 0.75))
-    for r in rs:
-        ops.append(("esp", last, 1, int(r), 0, plen[int(r)]))
-    ops.append(("drop", carrier))
+        ops.append(("l3put", int(r), upto, carrier, 1, 0.75))
     return ops
 
 
-def apply_ops_gpu(ctx, trace: W.Trace, ops):
-    """Apply warm_ops through the drop-in API (one call per op)."""
+def chain_blocks(hashes: np.ndarray, n: int, upto: int, B: int):
+    """(hash, span_start, span_end) of the blocks insert_chain(tokens, upto) puts
+    (hierarchy.cpp:119-130): boundary i spans [iB, min((i+1)B, n)) and stops past upto."""
+    out = []
+    for i, h in enumerate(hashes):
+        s, e = i * B, min((i + 1) * B, n)
+        if e > upto:
+            break
+        out.append((int(h), s, e))
+    return out
+
+
+def apply_ops_gpu(ctx, trace: W.Trace, ops, rep_base=0):
+    """Apply warm_ops through the drop-in API (one call per op).  Sharded: this ctx holds
+    global replicas [rep_base, rep_base + ctx.n_replicas); ops on other replicas are
+    skipped, L3 ops (the replicated shared L3) always apply."""
     for op in ops:
         k = op[0]
         if k == "ins":
             _, n, tier, r, upto, wf, role, now, pin = op
-            ctx.insert_chain(n, tier, trace.prompt(r), upto, wf, role, now, pin)
-        elif k == "cmp":
-            _, w, mask, now = op
-            for n in range(ctx.n_replicas):
-                ctx.complete(n, w, mask, now)
-            ctx.l3_dead_sweep(w, mask)
-        elif k == "esp":
-            _, n, tier, r, frm, to = op
-            ctx.erase_chain_span(n, tier, trace.prompt(r), frm, to)
+            if rep_base <= n < rep_base + ctx.n_replicas:
+                ctx.insert_chain(n - rep_base, tier, trace.prompt(r), upto, wf, role, now, pin)
+        elif k == "l3put":
+            _, r, upto, wf, role, now = op
+            p = trace.prompt(r)
+            for h, s0, e0 in chain_blocks(ctx.chain_hashes(p), len(p), upto, ctx.B):
+                ctx.put(0, 2, h, s0, e0, wf, role, now, 0)
         elif k == "reg":
             ctx.registry_update(op[1], op[2])
-        elif k == "drop":
-            ctx.registry_drop(op[1])
         else:
             raise ValueError(op)
 
