@@ -295,7 +295,7 @@ def run_reference(args):
                              "sample": cpu_sample_desc(args, n, cores, False, ml, sample)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
@@ -328,6 +328,7 @@ class Arm:
             self.bursts.append(S.upload_burst(tr, args.block, dev, k))
             del tr
         self.st = S.Steady(self.ctx, cl, args.requests, dev)
+        self.st.reserve(self.bursts)
         self.overlap = args.free_sms >= 0
         self.H = torch.cuda.Stream(device=dev, priority=0) if self.overlap else self.S_stream
         self.hctx = Context(0, [], [], args.block, device=dev.index)
@@ -484,7 +485,7 @@ def run_ours(args):
         "phase_ms": phase_ms, "clocks": clk, "gpu_launches": int(launches),
         "e2e": e2e, "cpu_baseline": cpu, "cpu_baseline_hash_once": cpu_h1,
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 def run_e2e(args, arm, E, k_first):
@@ -693,6 +694,7 @@ def run_sharded(args):
         bursts.append(S.upload_burst(tr, args.block, dev, k * ws + rank))
         del tr
     sh = ShardedSteady(ctx, cl, rank, ws, bursts, args.block, dev)
+    sh.reserve()
     sh.build_directory()
     H = torch.cuda.Stream(device=dev, priority=0)
     hctx = Context(0, [], [], args.block, device=local)
@@ -788,7 +790,7 @@ def run_sharded(args):
             "clocks": clk, "gpu_launches": int(cnt[3].item()), "e2e": None,
             "cpu_baseline": None,
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -289,6 +289,9 @@ int pyg_release_hold_dev(pyg_ctx* ctx, const int64_t* d_tok_off, const int64_t* 
    issue-time updates, engine.cpp:605-609, last write per workflow); max_wf >= every id. */
 int pyg_registry_update_batch_dev(pyg_ctx* ctx, int32_t n, const int32_t* d_wf,
                                   const uint64_t* d_mask, int32_t max_wf);
+/* Grow the device registry to hold workflow ids 0..max_wf now (synchronizes), so later
+   updates never reallocate inside a stream-ordered step. */
+int pyg_registry_reserve(pyg_ctx* ctx, int32_t max_wf);
 
 /* ------------------------------------------------------ sharded step (multi-GPU) */
 /* With pyg_set_shard, pyg_route_batch_dev routes over the WHOLE cluster: the node table,

@@ -138,6 +138,7 @@ _sig("pyg_set_hash_split", vp, i64)
 _sig("pyg_nodes_compose_dev", vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp)
 _sig("pyg_release_hold_dev", vp, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp)
 _sig("pyg_registry_update_batch_dev", vp, i32, vp, vp, i32)
+_sig("pyg_registry_reserve", vp, i32)
 _sig("pyg_shard_apply_lists_dev", vp, vp, i32, i32)
 _sig("pyg_shard_apply_lists_range_dev", vp, vp, i32, i32, i32, i32, i32)
 _sig("pyg_shard_results_dev", vp, vp, i32, vp, vp, i64, i32, vp, vp)
@@ -228,6 +229,9 @@ class Context:
 
     def check_device_error(self):
         check(_lib.pyg_check_device_error(self.h))
+
+    def registry_reserve(self, max_wf: int):
+        check(_lib.pyg_registry_reserve(self.h, int(max_wf)))
 
     def set_hash_split(self, min_tokens: int):
         check(_lib.pyg_set_hash_split(self.h, int(min_tokens)))

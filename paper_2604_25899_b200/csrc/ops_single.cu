@@ -689,6 +689,12 @@ int pyg_registry_update_batch_dev(pyg_ctx* c, int32_t n, const int32_t* d_wf,
   return PYG_OK;
 }
 
+int pyg_registry_reserve(pyg_ctx* c, int32_t max_wf) {
+  PYG_ON_DEVICE(c);
+  if (!c || max_wf < 0) return PYG_EINVAL;
+  return reg_grow(c, max_wf);
+}
+
 int pyg_registry_drop(pyg_ctx* c, int32_t wf) {
   PYG_ON_DEVICE(c);
   if (!c || wf < 0) return PYG_EINVAL;

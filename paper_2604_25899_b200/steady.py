@@ -146,6 +146,7 @@ class Steady:
         self.nodes.asg_off = torch.zeros_like(self.base_off)
         self.nodes.asg = torch.zeros((A + R_max + 1, 4), dtype=torch.int64, device=device)
         dummy = PB.DeviceBatch(R_max, None, None, None, None, None, None, None, None, 0, 0)
+        self.reserved_wf = -1
         self.outs = [PB.alloc_out(ctx, dummy, self.nodes, device=device) for _ in range(HOLD + 1)]
         self.placed_total = 0
 
@@ -172,6 +173,14 @@ class Steady:
             _ptr(o.placed_off) if o else None, _ptr(o.placed) if o else None,
             _ptr(prev.b.res) if prev else None, _ptr(prev.hold) if prev else None, 2,
             _ptr(self.nodes.asg_off), _ptr(self.nodes.asg)))
+
+    def reserve(self, bursts):
+        """Size the device registry for every burst's workflows up front (a growth inside the
+        step would synchronize)."""
+        mx = max(b.max_wf for b in bursts)
+        if mx > self.reserved_wf:
+            self.ctx.registry_reserve(mx)
+            self.reserved_wf = mx
 
     def registry(self, burst: Burst):
         check(_lib._lib.pyg_registry_update_batch_dev(self.ctx.h, burst.n_reg, _ptr(burst.reg_wf),

@@ -200,6 +200,10 @@ class ShardedSteady:
                              torch.from_numpy(rm.view(np.int64)).to(device), len(rw),
                              int(wf.max()) if len(wf) else 0))
 
+    def reserve(self):
+        """Size the device registry for every burst's workflows (replicated registry)."""
+        self.ctx.registry_reserve(max(r[3] for r in self.reg))
+
     def build_directory(self):
         self.steps[0].build_directory()
 
