@@ -10,6 +10,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <string>
 
 #include "ctx.cuh"
 #include "device_ops.cuh"
@@ -603,8 +604,14 @@ int pyg_check_device_error(pyg_ctx* c) {
   PYG_CUDA(cudaMemcpyAsync(&e, c->hd.error, 4, cudaMemcpyDeviceToHost, c->stream));
   PYG_CUDA(cudaMemsetAsync(c->hd.error, 0, 4, c->stream));
   PYG_CUDA(cudaStreamSynchronize(c->stream));
+  if (e == 7) {
+    set_error("16-bit route rows got a staged value >= 65536 (prompt of >= 64k tokens): "
+              "rebuild the exchange with 32-bit rows");
+    return PYG_ECAPACITY;
+  }
   if (e) {
-    set_error("device-side log capacity exhausted in a batched kernel");
+    set_error("device-side capacity exhausted in a batched kernel (code " + std::to_string(e) +
+              ")");
     return PYG_ECAPACITY;
   }
   return PYG_OK;

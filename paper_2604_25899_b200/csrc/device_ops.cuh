@@ -503,35 +503,84 @@ __device__ inline EvictOut block_evict_sorted(const CtxDev& c, TierDev* tp, int6
   return r;
 }
 
+// Warp-segmented ordered passes: warp w of the CTA owns the contiguous range
+// [w*seg, min(n, (w+1)*seg)); a range total per warp, one block-level prefix over the
+// warps, then each warp walks its range in order with warp scans -- one CTA barrier per
+// pass instead of one per 512 elements.
+struct WarpSeg {
+  int64_t lo, hi;
+};
+__device__ __forceinline__ WarpSeg warp_seg(int64_t n) {
+  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5;
+  const int64_t seg = (n + nw - 1) / nw;
+  const int64_t lo = min(n, w * seg);
+  return WarpSeg{lo, min(n, lo + seg)};
+}
+// exclusive prefix of the per-warp totals (every lane of warp w gets the sum over warps < w);
+// total over all warps to *tot.  swp: >= 32 int64 of shared memory.
+__device__ __forceinline__ int64_t warp_seg_prefix(int64_t wtot, int64_t* swp, int64_t* tot) {
+  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) swp[w] = wtot;
+  __syncthreads();
+  int64_t pre = 0, all = 0;
+  for (int k = 0; k < nw; ++k) {
+    const int64_t v = swp[k];
+    pre += k < w ? v : 0;
+    all += v;
+  }
+  __syncthreads();
+  *tot = all;
+  return pre;
+}
+__device__ __forceinline__ int64_t warp_incl_scan(int64_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+__device__ __forceinline__ bool evict_candidate(const Block& b) {
+  return (b.flags & kAlive) && b.pin <= 0;
+}
+
 __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t excess, int speculative,
                                 uint64_t* out_ids, int64_t cap, unsigned char* smem_keys,
                                 int64_t* sm) {
+  __shared__ int64_t swp[32];
   EvictOut res{0, 0, 1};
   if (excess <= 0) return res;
   const TierDev t = *tp;
   const int64_t n = t.log_len;
-  int64_t mine = 0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const Block& b = t.log[i];
-    mine += ((b.flags & kAlive) && b.pin <= 0) ? 1 : 0;
+  const int lane = threadIdx.x & 31;
+  // candidates per warp range of the log
+  const WarpSeg ls = warp_seg(n);
+  int64_t wc = 0;
+  for (int64_t base = ls.lo; base < ls.hi; base += 32) {
+    const int64_t i = base + lane;
+    const bool cand = i < ls.hi && evict_candidate(t.log[i]);
+    wc += __popc(__ballot_sync(kFull, cand));
   }
   int64_t ncand;
-  block_exscan(mine, sm, &ncand);
-  int64_t opos = 0, rem = excess, taken = 0, ftok = 0;
+  const int64_t wbase = warp_seg_prefix(wc, swp, &ncand);
+  int64_t opos = 0, rem = excess, ftok = 0;
   bool done = false;
   // the grouped path needs the keys in shared memory: log index < 2^24, size < 128
   if (smem_keys && ncand <= kSmemSortCap && n < (1 << 24) && c.B < 128) {
     uint64_t* khi = reinterpret_cast<uint64_t*>(smem_keys);
     uint32_t* klo = reinterpret_cast<uint32_t*>(smem_keys + kSmemSortCap * 8);
-    int64_t write = 0;
-    for (int64_t base = 0; base < n; base += blockDim.x) {
-      const int64_t i = base + threadIdx.x;
+    // gather in log (= id) order: key = order(last_access) | class, size, log index
+    int64_t wpos = wbase;
+    for (int64_t base = ls.lo; base < ls.hi; base += 32) {
+      const int64_t i = base + lane;
       bool cand = false;
       uint64_t h = 0;
       uint32_t l = 0;
-      if (i < n) {
+      if (i < ls.hi) {
         const Block& b = t.log[i];
-        cand = (b.flags & kAlive) && b.pin <= 0;
+        cand = evict_candidate(b);
         if (cand) {
           bool dead = false;
           if (speculative) {
@@ -545,16 +594,17 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
               static_cast<uint32_t>(i);
         }
       }
-      int64_t tot;
-      const int64_t pos = write + block_exscan(cand ? 1 : 0, sm, &tot);
+      const unsigned m = __ballot_sync(kFull, cand);
       if (cand) {
+        const int64_t pos = wpos + __popc(m & lanemask_lt());
         khi[pos] = h;
         klo[pos] = l;
       }
-      write += tot;
+      wpos += __popc(m);
     }
     __syncthreads();
-    uint32_t pc = 0;   // groups <= (pc, ph) are taken; pc = 0, ph = 0 with first = true: none
+    const WarpSeg cs = warp_seg(ncand);
+    uint32_t pc = 0;   // groups <= (pc, ph) are taken (none while `first`)
     uint64_t ph = 0;
     bool first = true;
     for (int g = 0; g < kEvictGroups; ++g) {
@@ -571,34 +621,61 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
         break;
       }
       const bool whole = m.sz < rem;
-      // members of group m in id order: take all, or while the running size before < rem
-      int64_t run = 0;
-      for (int64_t base = 0; base < ncand; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        bool mem = false;
-        int64_t sz = 0;
-        uint32_t lo = 0;
-        if (i < ncand) {
-          lo = klo[i];
-          mem = (lo >> 31) == m.cls && khi[i] == m.h;
-          sz = mem ? static_cast<int64_t>((lo >> 24) & 0x7fu) : 0;
+      if (whole && !out_ids) {
+        // the whole group goes; order is irrelevant without an id list
+        int64_t cnt = 0;
+        for (int64_t i = threadIdx.x; i < ncand; i += blockDim.x) {
+          const uint32_t lo = klo[i];
+          if ((lo >> 31) == m.cls && khi[i] == m.h) {
+            erase_at(t, lo & 0xffffffu);
+            ++cnt;
+          }
         }
-        int64_t tot;
-        const int64_t before = run + block_exscan(sz, sm, &tot);
-        const bool take = mem && (whole || before < rem);
+        int64_t ct;
+        warp_seg_prefix(warp_sum(cnt), swp, &ct);
+        opos += ct;
+      } else {
+        // members in id order: sizes before each member within the group decide the cut
+        int64_t ms = 0, mc = 0;
+        for (int64_t base = cs.lo; base < cs.hi; base += 32) {
+          const int64_t i = base + lane;
+          const bool mem = i < cs.hi && (klo[i] >> 31) == m.cls && khi[i] == m.h;
+          ms += warp_sum(mem ? static_cast<int64_t>((klo[i] >> 24) & 0x7fu) : int64_t{0});
+        }
+        int64_t all;
+        int64_t run = warp_seg_prefix(ms, swp, &all);
+        // count of taken members before this warp's range (for the id list positions)
+        for (int64_t base = cs.lo; base < cs.hi; base += 32) {
+          const int64_t i = base + lane;
+          const bool mem = i < cs.hi && (klo[i] >> 31) == m.cls && khi[i] == m.h;
+          const int64_t sz = mem ? static_cast<int64_t>((klo[i] >> 24) & 0x7fu) : 0;
+          const int64_t incl = warp_incl_scan(sz);
+          const bool take = mem && (whole || run + incl - sz < rem);
+          mc += __popc(__ballot_sync(kFull, take));
+          run += __shfl_sync(kFull, incl, 31);
+        }
         int64_t ntk;
-        const int64_t rank = block_exscan(take ? 1 : 0, sm, &ntk);
-        if (take) {
-          const int64_t li = lo & 0xffffffu;
-          const int64_t at = opos + rank;
-          if (out_ids && at < cap) out_ids[at] = t.log[li].id;
-          erase_at(t, li);
+        int64_t tpos = opos + warp_seg_prefix(mc, swp, &ntk);
+        run = warp_seg_prefix(ms, swp, &all);
+        for (int64_t base = cs.lo; base < cs.hi; base += 32) {
+          const int64_t i = base + lane;
+          const bool mem = i < cs.hi && (klo[i] >> 31) == m.cls && khi[i] == m.h;
+          const int64_t sz = mem ? static_cast<int64_t>((klo[i] >> 24) & 0x7fu) : 0;
+          const int64_t incl = warp_incl_scan(sz);
+          const bool take = mem && (whole || run + incl - sz < rem);
+          const unsigned tm = __ballot_sync(kFull, take);
+          if (take) {
+            const int64_t li = klo[i] & 0xffffffu;
+            const int64_t at = tpos + __popc(tm & lanemask_lt());
+            if (out_ids && at < cap) out_ids[at] = t.log[li].id;
+            erase_at(t, li);
+          }
+          tpos += __popc(tm);
+          run += __shfl_sync(kFull, incl, 31);
         }
         opos += ntk;
-        run += tot;
-        if (!whole && run >= rem) break;  // uniform: the cut is inside this chunk
+        __syncthreads();
       }
-      taken = opos;
       if (!whole) {
         done = true;
         break;
@@ -614,15 +691,15 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
         const uint32_t lo = klo[i];
         if (!(t.log[lo & 0xffffffu].flags & kAlive)) f += (lo >> 24) & 0x7fu;
       }
-      block_exscan(f, sm, &ftok);
+      warp_seg_prefix(warp_sum(f), swp, &ftok);
       rem = excess - ftok;
     }
     if (threadIdx.x == 0) {
       tp->occupancy -= ftok;
-      tp->n_alive -= taken;
+      tp->n_alive -= opos;
     }
     __syncthreads();
-    res.n_freed = taken;
+    res.n_freed = opos;
     res.freed_tokens = ftok;
     res.satisfied = ftok >= excess;
     if (!done) {  // more than kEvictGroups groups: finish with the sorted path

@@ -102,7 +102,7 @@ __global__ void k_recv_lens(const int32_t* sel, const int64_t* count, const pyg_
 }
 
 __global__ void k_pack(const pyg_reservation* req, const int32_t* group, const int32_t* staged,
-                       int R, int mc, int s16, int32_t* rows) {
+                       int R, int mc, int s16, int32_t* rows, int32_t* err) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
   const int wd = 5 + (s16 ? (mc + 1) / 2 : mc);
@@ -117,6 +117,10 @@ __global__ void k_pack(const pyg_reservation* req, const int32_t* group, const i
   o[4] = group[r];
   const int32_t* st = staged + static_cast<int64_t>(r) * mc;
   if (s16) {
+    // 16-bit staged values: a prompt of >= 65536 tokens (staged value > 0xffff) would be
+    // truncated -- flag it (error 7) so the caller switches to 32-bit rows
+    for (int j = 0; j < mc; ++j)
+      if (static_cast<uint32_t>(st[j]) > 0xffffu) atomicExch(err, 7);
     for (int j = 0; j < mc; j += 2) {
       const uint32_t lo = static_cast<uint32_t>(st[j]) & 0xffffu;
       const uint32_t hi = j + 1 < mc ? (static_cast<uint32_t>(st[j + 1]) & 0xffffu) : 0u;
@@ -441,7 +445,8 @@ int pyg_shard_pack_dev(pyg_ctx* c, const pyg_reservation* d_req, const int32_t* 
   PYG_ON_DEVICE(c);
   if (!c || R < 0 || mc < 0) return PYG_EINVAL;
   if (!R) return PYG_OK;
-  k_pack<<<(R + 255) / 256, 256, 0, c->stream>>>(d_req, d_group, d_staged, R, mc, s16, d_rows);
+  k_pack<<<(R + 255) / 256, 256, 0, c->stream>>>(d_req, d_group, d_staged, R, mc, s16, d_rows,
+                                                 c->hd.error);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
