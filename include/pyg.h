@@ -131,6 +131,10 @@ int pyg_matched_prefix(pyg_ctx* ctx, int32_t replica, int32_t tier, const uint64
 int pyg_lookup(pyg_ctx* ctx, int32_t replica, const uint64_t* tokens, int64_t n,
                int32_t with_l3, int64_t out[3]);
 /* CacheHierarchy::insert_chain (hierarchy.cpp:119-130) */
+/* CacheHierarchy::lookup of ONE prompt on replicas 0..n_rep-1 at once (the engine's node_view
+   loop, engine.cpp:640-648): out[3r..3r+2] = replica r's (l1, l2, l3). */
+int pyg_lookup_all(pyg_ctx* ctx, const uint64_t* tokens, int64_t n, int32_t with_l3,
+                   int32_t n_rep, int64_t* out);
 int pyg_insert_chain(pyg_ctx* ctx, int32_t replica, int32_t tier, const uint64_t* tokens,
                      int64_t n, int64_t upto, int32_t workflow, int32_t role, double now,
                      int32_t pin_delta);

@@ -36,6 +36,18 @@ struct Backend {
   pyg_ctx* ctx = nullptr;
   int32_t next_slot = 0;
   int32_t max_slots = 0;
+  // node_view memo: the engine asks lookup(prompt, nullptr) of every ready replica in turn
+  // (engine.cpp:640-648); the first call computes all replicas' lookups in one device call
+  // (pyg_lookup_all) and the next ones are served from here until any tier changes
+  uint64_t epoch = 0;  // bumped by every mutating call
+  struct {
+    bool valid = false;
+    uint64_t epoch = 0;
+    int32_t n_slots = 0;
+    std::vector<uint64_t> tokens;
+    std::vector<int64_t> m;  // 3 per slot
+  } view;
+  void bump() { ++epoch; }
   std::unordered_map<std::string, int32_t> wf_ids, role_ids;
   std::vector<std::string> wf_names, role_names;
   std::vector<pyg_block> dump_buf;
@@ -158,6 +170,7 @@ CacheBlock* TierStore::find_chain_mut(uint64_t chain_hash) {
 uint64_t TierStore::put(uint64_t chain_hash, int64_t span_start, int64_t span_end,
                         const Lineage& lineage, double now, int pin_delta, uint64_t*) {
   Backend& b = Backend::get();
+  b.bump();
   uint64_t id = 0;
   check(pyg_tier_put(b.ctx, api_slot(slot_), tier_, chain_hash, span_start, span_end,
                      b.wf(lineage.workflow_id), b.role(lineage.role_id), now, pin_delta, &id));
@@ -165,6 +178,7 @@ uint64_t TierStore::put(uint64_t chain_hash, int64_t span_start, int64_t span_en
 }
 
 void TierStore::erase(uint64_t block_id) {
+  Backend::get().bump();
   check(pyg_tier_erase(Backend::get().ctx, api_slot(slot_), tier_, block_id));
 }
 
@@ -180,6 +194,7 @@ int64_t TierStore::matched_prefix(const workflow::TokenSeq& tokens,
 CacheHierarchy::CacheHierarchy(int64_t l1_capacity, int64_t l2_capacity)
     : slot_(Backend::get().next_slot++), l1_(slot_, 0), l2_(slot_, 1) {
   Backend& b = Backend::get();
+  b.bump();
   if (slot_ >= b.max_slots)
     throw std::runtime_error("libpyg_b200 adapter: raise PYG_ENGINE_MAX_REPLICAS");
   check(pyg_set_capacity(b.ctx, slot_, l1_capacity, l2_capacity));
@@ -187,21 +202,36 @@ CacheHierarchy::CacheHierarchy(int64_t l1_capacity, int64_t l2_capacity)
 
 CacheHierarchy::Match CacheHierarchy::lookup(const workflow::TokenSeq& prompt,
                                              const SharedL3* l3) const {
+  Backend& b = Backend::get();
+  if (l3 == nullptr) {  // node_view: every replica at once, memoized until a tier changes
+    auto& v = b.view;
+    if (!(v.valid && v.epoch == b.epoch && slot_ < v.n_slots && v.tokens == prompt)) {
+      v.n_slots = b.next_slot;
+      v.m.resize(3 * static_cast<size_t>(v.n_slots));
+      check(pyg_lookup_all(b.ctx, prompt.data(), static_cast<int64_t>(prompt.size()), 0,
+                           v.n_slots, v.m.data()));
+      v.tokens = prompt;
+      v.epoch = b.epoch;
+      v.valid = true;
+    }
+    return {v.m[3 * slot_], v.m[3 * slot_ + 1], 0};
+  }
   int64_t m[3];
-  check(pyg_lookup(Backend::get().ctx, slot_, prompt.data(), static_cast<int64_t>(prompt.size()),
-                   l3 != nullptr, m));
+  check(pyg_lookup(b.ctx, slot_, prompt.data(), static_cast<int64_t>(prompt.size()), 1, m));
   return {m[0], m[1], m[2]};
 }
 
 void CacheHierarchy::insert_chain(Tier t, const workflow::TokenSeq& tokens, int64_t upto,
                                   const Lineage& lineage, double now, int pin_delta) {
   Backend& b = Backend::get();
+  b.bump();
   check(pyg_insert_chain(b.ctx, slot_, static_cast<int32_t>(t), tokens.data(),
                          static_cast<int64_t>(tokens.size()), upto, b.wf(lineage.workflow_id),
                          b.role(lineage.role_id), now, pin_delta));
 }
 
 void CacheHierarchy::unpin_chain(const workflow::TokenSeq& tokens, int64_t upto) {
+  Backend::get().bump();
   check(pyg_unpin_chain(Backend::get().ctx, slot_, tokens.data(),
                         static_cast<int64_t>(tokens.size()), upto));
 }
@@ -324,6 +354,7 @@ std::vector<StageAction> on_prefetch_requested(const workflow::RequestEnvelope& 
 EvictionResult evict_for_space(CacheHierarchy& cache, Tier tier, int64_t needed,
                                const FutureRegistry&, bool speculative) {
   Backend& b = Backend::get();
+  b.bump();
   static std::vector<uint64_t> ids(1 << 20);
   int64_t n = 0, ft = 0;
   int32_t ok = 0;

@@ -134,6 +134,7 @@ _sig("pyg_shard_unpack_dev", vp, vp, i32, i32, i32, vp, vp, vp)
 _sig("pyg_shard_pull_dev", vp, vp, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64)
 _sig("pyg_shard_local_placed_dev", vp, vp, vp, vp, vp, vp, vp)
 _sig("pyg_stats", vp, vp, i32)
+_sig("pyg_lookup_all", vp, vp, i64, i32, i32, vp)
 _sig("pyg_set_hash_split", vp, i64)
 _sig("pyg_nodes_compose_dev", vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp)
 _sig("pyg_release_hold_dev", vp, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp)
@@ -289,6 +290,15 @@ class Context:
         return out.value
 
     # -- CacheHierarchy level
+    def lookup_all(self, tokens, with_l3=True, n_rep=None):
+        """pyg_lookup_all: (l1, l2, l3) of one prompt on replicas 0..n_rep-1."""
+        t = np.ascontiguousarray(tokens, np.uint64)
+        n = self.n_replicas if n_rep is None else int(n_rep)
+        out = np.zeros((max(n, 1), 3), np.int64)
+        check(_lib.pyg_lookup_all(self.h, t.ctypes.data, len(t), int(bool(with_l3)), n,
+                                  out.ctypes.data))
+        return out[:n]
+
     def lookup(self, replica, tokens, with_l3=True):
         t = _u64(tokens)
         out = np.zeros(3, np.int64)

@@ -283,6 +283,7 @@ void pyg_destroy(pyg_ctx* c) {
   cudaFree(c->d_scratch);
   cudaFree(c->d_aux);
   cudaFree(c->d_claim);
+  cudaFree(c->memo);
   cudaFree(c->d_list);
   cudaFree(c->dir_mem);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);

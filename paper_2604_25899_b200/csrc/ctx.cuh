@@ -46,6 +46,13 @@ struct pyg_ctx {
   int64_t split_min = 8192;  // K1: prompts of >= split_min tokens are split tasks (0 = never)
   void* d_aux = nullptr;     // second on-demand buffer (fused assembly's chunk sources)
   size_t d_aux_size = 0;
+  // drop-in calls: the last uploaded token sequence and its boundary hashes stay on the
+  // device, so consecutive calls on the same sequence (lookup on every candidate replica,
+  // lookup -> evict -> insert -> unpin of one admission) upload and hash it once
+  void* memo = nullptr;
+  size_t memo_size = 0;
+  std::vector<uint64_t> memo_tokens;
+  bool memo_valid = false;
   // ordered L3 resolution of batched admission (batch.cu): per-L3-block claims
   void* d_claim = nullptr;
   int64_t claim_cap = 0;
@@ -65,6 +72,7 @@ int assemble_offsets(pyg_ctx* c, int32_t R, const int64_t* d_seg_off, const pyg_
                      int64_t* d_tok_off);
 inline void count_launch(pyg_ctx* c, int n = 1) { c->launches += n; }
 cudaError_t device_setup(int dev);  // k_hash.cu: per-device K1 attributes and constants
+int hash_seq_launch(pyg_ctx* c, const uint64_t* d_tok, int64_t n, uint64_t* d_hash);
 int sm_count(int dev);              // SM count of a device (cached per device)
 }  // namespace pyg_host
 

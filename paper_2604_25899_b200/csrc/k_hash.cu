@@ -457,6 +457,24 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   }  // task loop
 }
 
+// chain_boundary_hashes of ONE sequence (the drop-in calls): a split task on one warp, or
+// one thread when B % 16 != 0 or the sequence is short.
+__global__ void __launch_bounds__(32) k_hash_seq(const uint64_t* __restrict__ tokens, int64_t n,
+                                                 int B, uint64_t* __restrict__ out, int split) {
+  __shared__ __align__(16) unsigned char wbuf[2 * kStageBytes];
+  if (split) {
+    split_task(tokens, n, B, out, wbuf);
+    return;
+  }
+  if (threadIdx.x) return;
+  uint64_t h = kFnvOffset;
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    h = fnv_token(h, tokens[i]);
+    if ((i + 1) % B == 0 || i + 1 == n) out[k++] = h;  // hierarchy.cpp:26
+  }
+}
+
 __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val,
                            int64_t split_min, int* n_split) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -540,6 +558,17 @@ int sm_count(int dev) {
   if (dev < 0 || dev >= 64) return 1;
   if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
   return n[dev] > 0 ? n[dev] : 1;
+}
+}  // namespace pyg_host
+
+namespace pyg_host {
+int hash_seq_launch(pyg_ctx* c, const uint64_t* d_tok, int64_t n, uint64_t* d_hash) {
+  if (n <= 0) return PYG_OK;
+  PYG_CUDA(device_setup(c->device));
+  const int split = (c->B % kSplitTok == 0 && n >= 64) ? 1 : 0;
+  k_hash_seq<<<1, 32, 0, c->stream>>>(d_tok, n, c->B, d_hash, split);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
 }
 }  // namespace pyg_host
 

@@ -16,17 +16,6 @@ using namespace pyg_host;
 namespace {
 
 // ---------------------------------------------------------------- kernels
-// chain_boundary_hashes (hierarchy.cpp:21-30) of one sequence, one thread.
-__global__ void k_hash_one(const uint64_t* tokens, int64_t n, int B, uint64_t* out) {
-  if (threadIdx.x || blockIdx.x) return;
-  uint64_t h = kFnvOffset;
-  int64_t k = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    h = fnv_token(h, tokens[i]);
-    if ((i + 1) % B == 0 || i + 1 == n) out[k++] = h;
-  }
-}
-
 struct ChainGet {
   const uint64_t* hashes;
   int64_t n;
@@ -174,6 +163,25 @@ __global__ void k_lookup(CtxDev c, int t0, int t1, int t2, const uint64_t* token
     if (lane == 0) out[k] = ragged_extend(t, t.log, tokens, n, hashes, m, c.B);
     __syncwarp();
   }
+}
+
+// CacheHierarchy::lookup (hierarchy.cpp:109-117) of ONE prompt on replicas [0, n_rep): a
+// warp per (replica, tier) -- the engine's node_view loop (engine.cpp:640-648) in one launch.
+__global__ void k_lookup_all(CtxDev c, int n_rep, int with_l3, const uint64_t* tokens, int64_t n,
+                             const uint64_t* hashes, int64_t* out) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= 3 * n_rep) return;
+  const int rep = w / 3, k = w % 3;
+  if (k == 2 && !with_l3) {
+    if (lane == 0) out[3 * rep + 2] = 0;
+    return;
+  }
+  const TierDev t = c.tiers[k < 2 ? 2 * rep + k : 2 * c.n_rep];
+  const int64_t nh = blocks_of(n, c.B);
+  const int64_t kb = warp_walk(t, hashes, nh);
+  const int64_t m = kb ? matched_from_blocks(kb, n, c.B) : 0;
+  if (lane == 0) out[3 * rep + k] = ragged_extend(t, t.log, tokens, n, hashes, m, c.B);
 }
 
 __global__ void k_evict(CtxDev c, int ti, int rep_for_decode, int64_t needed, int spec,
@@ -385,20 +393,40 @@ __global__ void k_route_one(int32_t nn, const int32_t* rid, const int64_t* cap,
 }
 
 // ------------------------------------------------------------ host helpers
+// The sequence on the device + its boundary hashes, with room for 64 int64 of outputs
+// after the hashes (at *d_hash + nh + 1).  Memoized: the same tokens as the last call reuse
+// the device copy (no upload, no hashing).
 int upload_tokens(pyg_ctx* c, const uint64_t* tokens, int64_t n, uint64_t** d_tok,
                   uint64_t** d_hash) {
   const int64_t nh = (n + c->B - 1) / c->B;
-  void* s;
-  int rc = scratch(c, (n + nh + 8) * sizeof(uint64_t) + 64, &s);
-  if (rc) return rc;
-  *d_tok = static_cast<uint64_t*>(s);
+  const size_t need = static_cast<size_t>(n + nh + 8 + 64) * sizeof(uint64_t) + 64;
+  if (c->memo_valid && static_cast<int64_t>(c->memo_tokens.size()) == n &&
+      (n == 0 || std::memcmp(c->memo_tokens.data(), tokens, n * sizeof(uint64_t)) == 0)) {
+    *d_tok = static_cast<uint64_t*>(c->memo);
+    *d_hash = *d_tok + n + 4;
+    return PYG_OK;
+  }
+  if (need > c->memo_size) {
+    if (c->memo) {
+      PYG_CUDA(cudaStreamSynchronize(c->stream));
+      PYG_CUDA(cudaFree(c->memo));
+      c->memo = nullptr;
+    }
+    const size_t sz = std::max<size_t>(need * 2, 1 << 16);
+    PYG_CUDA(cudaMalloc(&c->memo, sz));
+    c->memo_size = sz;
+  }
+  c->memo_valid = false;
+  *d_tok = static_cast<uint64_t*>(c->memo);
   *d_hash = *d_tok + n + 4;
   if (n) {
     PYG_CUDA(cudaMemcpyAsync(*d_tok, tokens, n * sizeof(uint64_t), cudaMemcpyHostToDevice,
                              c->stream));
-    k_hash_one<<<1, 1, 0, c->stream>>>(*d_tok, n, c->B, *d_hash);
-    PYG_LAUNCHED(c);
+    int rc = hash_seq_launch(c, *d_tok, n, *d_hash);
+    if (rc) return rc;
   }
+  c->memo_tokens.assign(tokens, tokens + n);
+  c->memo_valid = true;
   return PYG_OK;
 }
 
@@ -558,6 +586,29 @@ int pyg_lookup(pyg_ctx* c, int32_t replica, const uint64_t* tokens, int64_t n, i
                                     with_l3 ? 2 * c->n_rep : -1, dt, n, dh, dout);
   PYG_LAUNCHED(c);
   PYG_CUDA(cudaMemcpyAsync(out, dout, 24, cudaMemcpyDeviceToHost, c->stream));
+  PYG_CUDA(cudaStreamSynchronize(c->stream));
+  return PYG_OK;
+}
+
+int pyg_lookup_all(pyg_ctx* c, const uint64_t* tokens, int64_t n, int32_t with_l3,
+                   int32_t n_rep, int64_t* out) {
+  PYG_ON_DEVICE(c);
+  if (!c || n < 0 || (n && !tokens) || !out || n_rep < 0 || n_rep > c->n_rep) {
+    set_error("pyg_lookup_all: bad arguments");
+    return PYG_EINVAL;
+  }
+  if (!n_rep) return PYG_OK;
+  uint64_t *dt, *dh;
+  int rc = upload_tokens(c, tokens, n, &dt, &dh);
+  if (rc) return rc;
+  void* sp;
+  if ((rc = scratch(c, static_cast<size_t>(n_rep) * 24 + 64, &sp))) return rc;
+  auto* dout = static_cast<int64_t*>(sp);
+  const int warps = 3 * n_rep;
+  k_lookup_all<<<(warps + 3) / 4, 128, 0, c->stream>>>(c->hd, n_rep, with_l3, dt, n, dh, dout);
+  PYG_LAUNCHED(c);
+  PYG_CUDA(cudaMemcpyAsync(out, dout, static_cast<size_t>(n_rep) * 24, cudaMemcpyDeviceToHost,
+                           c->stream));
   PYG_CUDA(cudaStreamSynchronize(c->stream));
   return PYG_OK;
 }
