@@ -47,7 +47,17 @@ struct Backend {
     std::vector<uint64_t> tokens;
     std::vector<int64_t> m;  // 3 per slot
   } view;
+  // per-tier change epochs (key: 2*slot + tier for replica tiers, the last key for L3) so
+  // a tier's snapshot (TierStore::blocks) is re-read only after that tier changed
+  std::vector<uint64_t> tier_epoch;
+  size_t tkey(int32_t slot, int32_t tier) const {
+    return tier == 2 || slot < 0 ? 2 * static_cast<size_t>(max_slots) : 2 * static_cast<size_t>(slot) + tier;
+  }
   void bump() { ++epoch; }
+  void bump(int32_t slot, int32_t tier) {
+    ++epoch;
+    ++tier_epoch[tkey(slot, tier)];
+  }
   std::unordered_map<std::string, int32_t> wf_ids, role_ids;
   std::vector<std::string> wf_names, role_names;
   std::vector<pyg_block> dump_buf;
@@ -66,6 +76,7 @@ struct Backend {
     pyg_config cfg{static_cast<int32_t>(pythia::cache::kBlockTokens), max_slots, d ? std::atoi(d) : 0,
                    0, zero.data(), zero.data(), 4096};
     check(pyg_create(&cfg, &ctx));
+    tier_epoch.assign(2 * static_cast<size_t>(max_slots) + 1, 0);
   }
 
   int32_t wf(const std::string& s) {
@@ -139,6 +150,9 @@ int64_t TierStore::occupancy() const {
 
 const std::map<uint64_t, CacheBlock>& TierStore::blocks() const {
   Backend& b = Backend::get();
+  const uint64_t ep = b.tier_epoch[b.tkey(slot_, tier_)];
+  if (view_epoch_ == ep) return view_;
+  view_epoch_ = ep;
   int64_t n = 0;
   if (b.dump_buf.empty()) b.dump_buf.resize(1 << 14);
   for (;;) {
@@ -170,7 +184,7 @@ CacheBlock* TierStore::find_chain_mut(uint64_t chain_hash) {
 uint64_t TierStore::put(uint64_t chain_hash, int64_t span_start, int64_t span_end,
                         const Lineage& lineage, double now, int pin_delta, uint64_t*) {
   Backend& b = Backend::get();
-  b.bump();
+  b.bump(slot_, tier_);
   uint64_t id = 0;
   check(pyg_tier_put(b.ctx, api_slot(slot_), tier_, chain_hash, span_start, span_end,
                      b.wf(lineage.workflow_id), b.role(lineage.role_id), now, pin_delta, &id));
@@ -178,7 +192,7 @@ uint64_t TierStore::put(uint64_t chain_hash, int64_t span_start, int64_t span_en
 }
 
 void TierStore::erase(uint64_t block_id) {
-  Backend::get().bump();
+  Backend::get().bump(slot_, tier_);
   check(pyg_tier_erase(Backend::get().ctx, api_slot(slot_), tier_, block_id));
 }
 
@@ -194,10 +208,11 @@ int64_t TierStore::matched_prefix(const workflow::TokenSeq& tokens,
 CacheHierarchy::CacheHierarchy(int64_t l1_capacity, int64_t l2_capacity)
     : slot_(Backend::get().next_slot++), l1_(slot_, 0), l2_(slot_, 1) {
   Backend& b = Backend::get();
-  b.bump();
   if (slot_ >= b.max_slots)
     throw std::runtime_error("libpyg_b200 adapter: raise PYG_ENGINE_MAX_REPLICAS");
   check(pyg_set_capacity(b.ctx, slot_, l1_capacity, l2_capacity));
+  b.bump(slot_, 0);
+  b.bump(slot_, 1);
 }
 
 CacheHierarchy::Match CacheHierarchy::lookup(const workflow::TokenSeq& prompt,
@@ -224,14 +239,14 @@ CacheHierarchy::Match CacheHierarchy::lookup(const workflow::TokenSeq& prompt,
 void CacheHierarchy::insert_chain(Tier t, const workflow::TokenSeq& tokens, int64_t upto,
                                   const Lineage& lineage, double now, int pin_delta) {
   Backend& b = Backend::get();
-  b.bump();
+  b.bump(slot_, t == Tier::L1 ? 0 : 1);  // tier(L3) aliases L2
   check(pyg_insert_chain(b.ctx, slot_, static_cast<int32_t>(t), tokens.data(),
                          static_cast<int64_t>(tokens.size()), upto, b.wf(lineage.workflow_id),
                          b.role(lineage.role_id), now, pin_delta));
 }
 
 void CacheHierarchy::unpin_chain(const workflow::TokenSeq& tokens, int64_t upto) {
-  Backend::get().bump();
+  Backend::get().bump(slot_, 0);
   check(pyg_unpin_chain(Backend::get().ctx, slot_, tokens.data(),
                         static_cast<int64_t>(tokens.size()), upto));
 }
@@ -354,7 +369,7 @@ std::vector<StageAction> on_prefetch_requested(const workflow::RequestEnvelope& 
 EvictionResult evict_for_space(CacheHierarchy& cache, Tier tier, int64_t needed,
                                const FutureRegistry&, bool speculative) {
   Backend& b = Backend::get();
-  b.bump();
+  b.bump(cache.tier(Tier::L1).slot(), tier == Tier::L1 ? 0 : 1);  // tier(L3) aliases L2
   static std::vector<uint64_t> ids(1 << 20);
   int64_t n = 0, ft = 0;
   int32_t ok = 0;

@@ -162,7 +162,11 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t sm[64];
   __shared__ int64_t bc[4];
+  __shared__ uint32_t sdup[1024];
+  __shared__ EvCache ec;
   const int rep = blockIdx.x;
+  if (threadIdx.x == 0) ec.valid = 0;
+  __syncthreads();
   TierDev* t1p = c.tiers + 2 * rep;
   TierDev* t2p = c.tiers + 2 * rep + 1;
   const TierDev& t3 = c.tiers[2 * c.n_rep];
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     // evict_for_space(L1, needed): base = l1_occupancy() (manager.cpp:106)
     const int64_t excess = t1p->occupancy + c.decode[rep] + (L - m[0]) - t1p->capacity;
     __syncthreads();
-    const EvictOut ev = block_evict(c, t1p, excess, a.spec, nullptr, 0, smem, sm);
+    const EvictOut ev = block_evict_admit(c, t1p, excess, a.spec, smem, sm, &ec);
     if (!ev.satisfied) {
       if (threadIdx.x == 0) {
         if (c.stats) atomicAdd(c.stats + 4, 1ULL);
@@ -248,14 +252,21 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     if (t1p->log_len + nh > t1p->log_cap) {
       __syncthreads();
       block_compact(c, t1p, sm);
+      if (threadIdx.x == 0) ec.valid = 0;  // log indices moved
     }
     const bool room = t1p->log_len + nh <= t1p->log_cap;
     __syncthreads();
     if (room) {
-      if (threadIdx.x < 32) {
-        ChainGetB gget{hs, L, c.B, a.wf[r], a.role[r]};
-        warp_put_ordered(c, t1p, nh, gget, a.now, +1);
-      }
+      ChainGetB gget{hs, L, c.B, a.wf[r], a.role[r]};
+      // blocks the insert touches get pinned: no longer eviction candidates
+      uint32_t* klo = reinterpret_cast<uint32_t*>(smem + kSmemSortCap * 8);
+      const bool cached = ec.valid != 0;
+      const int64_t nc = ec.ncand;
+      auto drop = [&](int64_t li) {
+        if (cached) ev_cache_drop(klo, nc, li);
+      };
+      if (block_put_ordered(c, t1p, nh, gget, a.now, +1, sdup, sm, drop) && threadIdx.x == 0)
+        ec.valid = 0;
     } else if (threadIdx.x == 0) {
       atomicExch(c.error, 1);
     }
@@ -481,22 +492,49 @@ __global__ void k_l3_final(CtxDev c, L3Args a, int64_t* match3, uint64_t* list, 
   }
 }
 
-// unpin_chain(seq, len) (hierarchy.cpp:132-142) for admitted requests: one
-// warp per request; decrements commute (pin -= 1 only while pin > 0).
+// unpin_chain(seq, len) (hierarchy.cpp:132-142) of the admitted requests placed on one
+// replica (one CTA per replica).  The (request, block) pairs of up to kRelChunk requests are
+// flattened over the whole CTA, so a 32k-token prompt's 2,048 unpins take 8 rounds of the
+// CTA, not 64 of one warp; decrements commute (pin -= 1 only while pin > 0).
+constexpr int kRelChunk = 256;
+
 __global__ void k_release(CtxDev c, const int64_t* tok_off, const int64_t* hash_off,
                           const uint64_t* hashes, const int32_t* placed_off,
                           const int32_t* placed, const int32_t* admitted,
                           const uint8_t* hold, int hold_val, const int32_t* hold_index) {
+  __shared__ int64_t s_end[kRelChunk];  // inclusive prefix of the selected requests' blocks
+  __shared__ int32_t s_req[kRelChunk];
+  __shared__ int64_t sm[64];
   const int rep = blockIdx.x;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const TierDev& t = c.tiers[2 * rep];
-  for (int32_t k = placed_off[rep] + w; k < placed_off[rep + 1]; k += nw) {
-    const int r = placed[k];
-    if (admitted[r] != 1 || (hold && hold[hold_index ? hold_index[r] : r] != hold_val)) continue;
-    const uint64_t* hs = hashes + hash_off[r];
-    const int64_t nh = hash_off[r + 1] - hash_off[r];
-    for (int64_t i = lane; i < nh; i += 32) {
-      const int64_t li = idx_find(t, hs[i]);
+  const TierDev t = c.tiers[2 * rep];
+  const int32_t p0 = placed_off[rep], p1 = placed_off[rep + 1];
+  for (int32_t q0 = p0; q0 < p1; q0 += kRelChunk) {
+    const int32_t q = q0 + static_cast<int32_t>(threadIdx.x);
+    int64_t nh = 0;
+    int32_t r = -1;
+    if (threadIdx.x < kRelChunk && q < p1) {
+      r = placed[q];
+      const bool sel = admitted[r] == 1 && (!hold || hold[hold_index ? hold_index[r] : r] == hold_val);
+      if (sel) nh = hash_off[r + 1] - hash_off[r];
+    }
+    int64_t tot;
+    const int64_t before = block_exscan(nh, sm, &tot);
+    if (threadIdx.x < kRelChunk) {
+      s_end[threadIdx.x] = before + nh;
+      s_req[threadIdx.x] = r;
+    }
+    __syncthreads();
+    const int nq = min(kRelChunk, p1 - q0);
+    for (int64_t j = threadIdx.x; j < tot; j += blockDim.x) {
+      int lo = 0, hi = nq - 1;  // first request whose end > j
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_end[mid] > j) hi = mid;
+        else lo = mid + 1;
+      }
+      const int rr = s_req[lo];
+      const int64_t i = j - (s_end[lo] - (hash_off[rr + 1] - hash_off[rr]));
+      const int64_t li = idx_find(t, hashes[hash_off[rr] + i]);
       if (li < 0) continue;
       int* pp = &t.log[li].pin;
       int old = *reinterpret_cast<volatile int*>(pp);
@@ -506,6 +544,7 @@ __global__ void k_release(CtxDev c, const int64_t* tok_off, const int64_t* hash_
         old = prev;
       }
     }
+    __syncthreads();
   }
 }
 

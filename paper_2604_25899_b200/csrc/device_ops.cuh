@@ -144,6 +144,132 @@ __device__ uint64_t warp_put_ordered(const CtxDev& c, TierDev* tp, int64_t n, Ge
   return last_id;
 }
 
+// warp_put_ordered on a whole CTA (same semantics, item order = id order): items are taken
+// blockDim at a time; each probes the index in parallel, new blocks get consecutive ids
+// and log slots by a block scan, existing ones are touched.  Exact only when no two items
+// of a chunk share a hash (the sequential loop would insert the first and touch it with the
+// second): a 1024-slot shared filter on the low 32 hash bits detects possible repeats and
+// such a chunk (never seen with chain hashes) runs through warp_put_ordered instead.
+// sdup: 1024 uint32 of shared memory; sm: >= 41 int64.  touch(log index) is called for every
+// existing block the puts touch (not for chunks that took the warp path); returns whether
+// any chunk took the warp path.
+struct NoTouch {
+  __device__ __forceinline__ void operator()(int64_t) const {}
+};
+template <class Get, class Touch = NoTouch>
+__device__ bool block_put_ordered(const CtxDev& c, TierDev* tp, int64_t n, Get get, double now,
+                                  int32_t pin_delta, uint32_t* sdup, int64_t* sm,
+                                  Touch touch = Touch()) {
+  bool slow = false;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t cnt = min(static_cast<int64_t>(blockDim.x), n - base);
+    for (int j = threadIdx.x; j < 1024; j += blockDim.x) sdup[j] = 0;
+    if (threadIdx.x == 0) sm[40] = 0;
+    __syncthreads();
+    const bool act = threadIdx.x < cnt;
+    PutItem it{};
+    if (act) {
+      it = get(base + threadIdx.x);
+      uint32_t k = static_cast<uint32_t>(it.hash) | 1u;  // 0 marks an empty slot
+      uint32_t sl = (static_cast<uint32_t>(it.hash >> 32) * 2654435761u) >> 22;
+      for (;;) {
+        const uint32_t prev = atomicCAS(sdup + sl, 0u, k);
+        if (prev == 0u) break;
+        if (prev == k) {
+          sm[40] = 1;  // possible repeat (or a 32-bit filter collision)
+          break;
+        }
+        sl = (sl + 1) & 1023u;
+      }
+    }
+    __syncthreads();
+    if (sm[40]) {  // exact sequential semantics for this chunk
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        struct Shift {
+          Get g;
+          int64_t b;
+          __device__ PutItem operator()(int64_t i) const { return g(b + i); }
+        } sh{get, base};
+        warp_put_ordered(c, tp, cnt, sh, now, pin_delta);
+      }
+      __syncthreads();
+      slow = true;
+      continue;
+    }
+    const TierDev t = *tp;
+    int64_t li = -1;
+    if (act) li = idx_find(t, it.hash);
+    const bool isnew = act && li < 0;
+    int64_t nnew;
+    const int64_t rank = block_exscan(isnew ? 1 : 0, sm, &nnew);
+    int64_t sz = 0;
+    bool rag = false;
+    if (isnew) {
+      const int64_t pos = t.log_len + rank;
+      Block b;
+      b.id = c.counters[t.counter] + static_cast<uint64_t>(rank);
+      b.hash = it.hash;
+      b.parent = it.parent;
+      b.s = it.s;
+      b.e = it.e;
+      b.la = now;
+      b.wf = it.wf;
+      b.role = it.role;
+      b.pin = pin_delta > 0 ? pin_delta : 0;
+      b.flags = kAlive | (it.orphan ? kOrphan : 0);
+      t.log[pos] = b;
+      idx_insert(t, it.hash, pos);
+      sz = b.e - b.s;
+      rag = (it.s % c.B == 0) && (it.e % c.B != 0);
+    } else if (act) {
+      Block& b = t.log[li];
+      b.la = now;
+      b.pin += pin_delta;
+      touch(li);
+    }
+    int64_t occ_add, nrag;
+    block_exscan(sz, sm, &occ_add);
+    block_exscan(rag ? 1 : 0, sm, &nrag);
+    // ragged-index notes: one thread when several (they may share a parent key)
+    if (nrag == 1 && rag) {
+      Block b;
+      b.s = it.s;
+      b.e = it.e;
+      b.parent = it.parent;
+      b.flags = it.orphan ? kOrphan : 0;
+      ridx_note(t, b, c.B);
+      if (it.orphan && (it.e - it.s) >= 64)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&tp->n_long_orphans), 1ULL);
+    }
+    if (nrag > 1) {
+      for (int64_t j = 0; j < cnt; ++j) {
+        if (threadIdx.x == j && rag) {
+          Block b;
+          b.s = it.s;
+          b.e = it.e;
+          b.parent = it.parent;
+          b.flags = it.orphan ? kOrphan : 0;
+          ridx_note(t, b, c.B);
+          if (it.orphan && (it.e - it.s) >= 64)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&tp->n_long_orphans), 1ULL);
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tp->log_len += nnew;
+      tp->n_alive += nnew;
+      tp->occupancy += occ_add;
+      tp->idx_used += nnew;
+      c.counters[t.counter] += static_cast<uint64_t>(nnew);
+    }
+    __syncthreads();
+  }
+  return slow;
+}
+
 // ------------------------------------------------------------- compaction
 // In-place stable compaction of a tier's log (drops dead records, keeps id
 // order) and rebuild of idx / ridx.  Whole CTA; smem >= 33 int64.
@@ -714,6 +840,202 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
   } else {
     res = block_evict_sorted(c, tp, excess, speculative, out_ids, cap, smem_keys, sm);
   }
+  if (threadIdx.x == 0 && c.stats) {
+    atomicAdd(c.stats, static_cast<unsigned long long>(res.n_freed));
+    atomicAdd(c.stats + 1, static_cast<unsigned long long>(res.freed_tokens));
+    atomicAdd(c.stats + 2, 1ULL);
+    if (!res.satisfied) atomicAdd(c.stats + 3, 1ULL);
+  }
+  __syncthreads();
+  return res;
+}
+
+// evict_for_space for the batched admission kernel, which evicts on one replica's L1 many
+// times in a row (k_admit: one CTA per replica, placements in order).  Between two of its
+// evictions the candidate set only shrinks -- victims are erased, blocks touched by the
+// admission's insert_chain become pinned, new blocks arrive pinned, nothing is unpinned
+// and the registry is fixed -- so the gathered candidate list (same layout as block_evict)
+// stays in shared memory for the CTA's next evictions: erased and pinned entries are marked
+// removed (size field 0x7f) instead of re-reading the whole log.  ec->valid = 0 forces a
+// fresh gather (first eviction, after a log compaction).  Same selection as block_evict.
+struct EvCache {
+  int64_t ncand;
+  int32_t valid;
+};
+constexpr uint32_t kRemoved = 0x7fu << 24;
+
+__device__ __forceinline__ bool ev_removed(uint32_t lo) { return ((lo >> 24) & 0x7fu) == 0x7fu; }
+
+// marks log index li removed from the cached candidates (binary search: gathered in log order)
+__device__ __forceinline__ void ev_cache_drop(uint32_t* klo, int64_t ncand, int64_t li) {
+  int64_t lo = 0, hi = ncand;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (static_cast<int64_t>(klo[mid] & 0xffffffu) < li) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < ncand && static_cast<int64_t>(klo[lo] & 0xffffffu) == li) klo[lo] |= kRemoved;
+}
+
+__device__ inline EvictOut block_evict_admit(const CtxDev& c, TierDev* tp, int64_t excess,
+                                             int speculative, unsigned char* smem_keys,
+                                             int64_t* sm, EvCache* ec) {
+  __shared__ int64_t swp[32];
+  EvictOut res{0, 0, 1};
+  if (excess <= 0) return res;
+  const TierDev t = *tp;
+  const int lane = threadIdx.x & 31;
+  uint64_t* khi = reinterpret_cast<uint64_t*>(smem_keys);
+  uint32_t* klo = reinterpret_cast<uint32_t*>(smem_keys + kSmemSortCap * 8);
+  if (!ec->valid) {
+    const int64_t n = t.log_len;
+    const WarpSeg ls = warp_seg(n);
+    int64_t wc = 0;
+    for (int64_t base = ls.lo; base < ls.hi; base += 32) {
+      const int64_t i = base + lane;
+      wc += __popc(__ballot_sync(kFull, i < ls.hi && evict_candidate(t.log[i])));
+    }
+    int64_t ncand;
+    const int64_t wbase = warp_seg_prefix(wc, swp, &ncand);
+    if (ncand > kSmemSortCap || n >= (1 << 24) || c.B >= 127) {
+      res = block_evict_sorted(c, tp, excess, speculative, nullptr, 0, smem_keys, sm);
+      goto stats;
+    }
+    int64_t wpos = wbase;
+    for (int64_t base = ls.lo; base < ls.hi; base += 32) {
+      const int64_t i = base + lane;
+      bool cand = false;
+      uint64_t h = 0;
+      uint32_t l = 0;
+      if (i < ls.hi) {
+        const Block& b = t.log[i];
+        cand = evict_candidate(b);
+        if (cand) {
+          bool dead = false;
+          if (speculative) {
+            const bool live = b.wf >= 0 && b.wf < c.reg_cap && c.reg_present[b.wf] &&
+                              b.role >= 0 && b.role < 64 &&
+                              ((c.reg_mask[b.wf] >> b.role) & 1ULL);
+            dead = !live;  // FutureRegistry::lineage_live (manager.cpp:19-23)
+          }
+          h = order_double(b.la);
+          l = (dead ? 0u : 0x80000000u) | (static_cast<uint32_t>(b.e - b.s) << 24) |
+              static_cast<uint32_t>(i);
+        }
+      }
+      const unsigned m = __ballot_sync(kFull, cand);
+      if (cand) {
+        const int64_t pos = wpos + __popc(m & lanemask_lt());
+        khi[pos] = h;
+        klo[pos] = l;
+      }
+      wpos += __popc(m);
+    }
+    if (threadIdx.x == 0) {
+      ec->ncand = ncand;
+      ec->valid = 1;
+    }
+    __syncthreads();
+  }
+  {
+    const int64_t ncand = ec->ncand;
+    const WarpSeg cs = warp_seg(ncand);
+    int64_t rem = excess, nfreed = 0, ftok = 0;
+    uint32_t pc = 0;
+    uint64_t ph = 0;
+    bool first = true, done = false;
+    for (int g = 0; g < kEvictGroups; ++g) {
+      EvGroup loc{2u, ~0ull, 0};
+      for (int64_t i = threadIdx.x; i < ncand; i += blockDim.x) {
+        const uint32_t lo = klo[i];
+        if (ev_removed(lo)) continue;
+        const uint32_t cl = lo >> 31;
+        const uint64_t h = khi[i];
+        if (!first && !grp_less(pc, ph, cl, h)) continue;
+        loc = grp_min(loc, EvGroup{cl, h, static_cast<int64_t>((lo >> 24) & 0x7fu)});
+      }
+      const EvGroup m = block_grp_min(loc);
+      if (m.cls == 2u) {  // nothing left: every candidate freed, unsatisfied
+        done = true;
+        break;
+      }
+      const bool whole = m.sz < rem;
+      int64_t tk = 0, tsz = 0;
+      if (whole) {
+        for (int64_t i = threadIdx.x; i < ncand; i += blockDim.x) {
+          const uint32_t lo = klo[i];
+          if (!ev_removed(lo) && (lo >> 31) == m.cls && khi[i] == m.h) {
+            erase_at(t, lo & 0xffffffu);
+            klo[i] = lo | kRemoved;
+            ++tk;
+          }
+        }
+        tsz = m.sz;
+      } else {
+        int64_t ms = 0;
+        for (int64_t base = cs.lo; base < cs.hi; base += 32) {
+          const int64_t i = base + lane;
+          bool mem = false;
+          uint32_t lo = 0;
+          if (i < cs.hi) {
+            lo = klo[i];
+            mem = !ev_removed(lo) && (lo >> 31) == m.cls && khi[i] == m.h;
+          }
+          ms += warp_sum(mem ? static_cast<int64_t>((lo >> 24) & 0x7fu) : int64_t{0});
+        }
+        int64_t all;
+        int64_t run = warp_seg_prefix(ms, swp, &all);
+        for (int64_t base = cs.lo; base < cs.hi; base += 32) {
+          const int64_t i = base + lane;
+          bool mem = false;
+          uint32_t lo = 0;
+          if (i < cs.hi) {
+            lo = klo[i];
+            mem = !ev_removed(lo) && (lo >> 31) == m.cls && khi[i] == m.h;
+          }
+          const int64_t sz = mem ? static_cast<int64_t>((lo >> 24) & 0x7fu) : 0;
+          const int64_t incl = warp_incl_scan(sz);
+          if (mem && run + incl - sz < rem) {
+            erase_at(t, lo & 0xffffffu);
+            klo[i] = lo | kRemoved;
+            ++tk;
+            tsz += sz;
+          }
+          run += __shfl_sync(kFull, incl, 31);
+        }
+      }
+      int64_t s1, s2;
+      warp_seg_prefix(warp_sum(tk), swp, &s1);
+      warp_seg_prefix(warp_sum(tsz), swp, &s2);
+      nfreed += s1;
+      ftok += s2;
+      if (!whole) {
+        done = true;
+        break;
+      }
+      rem -= m.sz;
+      pc = m.cls;
+      ph = m.h;
+      first = false;
+    }
+    if (threadIdx.x == 0) {
+      tp->occupancy -= ftok;
+      tp->n_alive -= nfreed;
+    }
+    __syncthreads();
+    res.n_freed = nfreed;
+    res.freed_tokens = ftok;
+    res.satisfied = ftok >= excess;
+    if (!done) {  // more than kEvictGroups groups: the sorted path finishes (regathers)
+      if (threadIdx.x == 0) ec->valid = 0;
+      const EvictOut rest = block_evict_sorted(c, tp, excess - ftok, speculative, nullptr, 0,
+                                               smem_keys, sm);
+      res.n_freed += rest.n_freed;
+      res.freed_tokens += rest.freed_tokens;
+      res.satisfied = res.freed_tokens >= excess;
+    }
+  }
+stats:
   if (threadIdx.x == 0 && c.stats) {
     atomicAdd(c.stats, static_cast<unsigned long long>(res.n_freed));
     atomicAdd(c.stats + 1, static_cast<unsigned long long>(res.freed_tokens));

@@ -184,7 +184,7 @@ __global__ void k_lookup_all(CtxDev c, int n_rep, int with_l3, const uint64_t* t
   if (lane == 0) out[3 * rep + k] = ragged_extend(t, t.log, tokens, n, hashes, m, c.B);
 }
 
-__global__ void k_evict(CtxDev c, int ti, int rep_for_decode, int64_t needed, int spec,
+__global__ void __launch_bounds__(512) k_evict(CtxDev c, int ti, int rep_for_decode, int64_t needed, int spec,
                         uint64_t* out_ids, int64_t cap, int64_t* out_stats) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t sm[64];
@@ -772,7 +772,7 @@ int pyg_evict_for_space(pyg_ctx* c, int32_t replica, int32_t tier, int64_t neede
   auto* dids = reinterpret_cast<uint64_t*>(dstats + 4);
   const size_t smem = kSmemSortCap * 12;
   PYG_CUDA(cudaFuncSetAttribute(k_evict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_evict<<<1, 1024, smem, c->stream>>>(c->hd, ti, tier == 0 ? replica : -1, needed,
+  k_evict<<<1, 512, smem, c->stream>>>(c->hd, ti, tier == 0 ? replica : -1, needed,
                                         speculative, dids, room, dstats);
   PYG_LAUNCHED(c);
   int64_t st[3];
