@@ -968,9 +968,9 @@ __device__ inline EvictOut block_evict_admit(const CtxDev& c, TierDev* tp, int64
             erase_at(t, lo & 0xffffffu);
             klo[i] = lo | kRemoved;
             ++tk;
+            tsz += (lo >> 24) & 0x7fu;
           }
         }
-        tsz = m.sz;
       } else {
         int64_t ms = 0;
         for (int64_t base = cs.lo; base < cs.hi; base += 32) {

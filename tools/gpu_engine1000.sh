@@ -7,10 +7,10 @@ make -s -C oracle restated > /dev/null 2>&1
 WF=${WF:-1000}
 for s in ${SEEDS:-1 2 3}; do
   mkdir -p gpurun_out/e$s/ref gpurun_out/e$s/b200
-  ( t0=$(date +%s.%N); ./oracle/_ref/engine_ref16 gpurun_out/e$s/ref $WF $s > gpurun_out/e$s/ref.out 2>&1; echo "ref rc=$? wall $(echo "$(date +%s.%N) - $t0" | bc)" >> gpurun_out/e$s/ref.out ) &
+  ( t0=$(date +%s%N); ./oracle/_ref/engine_ref16 gpurun_out/e$s/ref $WF $s > gpurun_out/e$s/ref.out 2>&1; echo "ref rc=$? wall_ms $(( ($(date +%s%N) - t0) / 1000000 ))" >> gpurun_out/e$s/ref.out ) &
 done
 for s in ${SEEDS:-1 2 3}; do
-  t0=$(date +%s.%N); ./integration/_build/engine_b200 gpurun_out/e$s/b200 $WF $s > gpurun_out/e$s/b200.out 2>&1; echo "b200 rc=$? wall $(echo "$(date +%s.%N) - $t0" | bc)" >> gpurun_out/e$s/b200.out
+  t0=$(date +%s%N); PYG_ENGINE_MAX_REPLICAS=${MAXREP:-1024} ./integration/_build/engine_b200 gpurun_out/e$s/b200 $WF $s > gpurun_out/e$s/b200.out 2>&1; echo "b200 rc=$? wall_ms $(( ($(date +%s%N) - t0) / 1000000 ))" >> gpurun_out/e$s/b200.out
 done
 wait
 for s in ${SEEDS:-1 2 3}; do
