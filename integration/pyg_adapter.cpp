@@ -13,6 +13,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -31,6 +34,46 @@ namespace {
 void check(int rc) {
   if (rc != PYG_OK) throw std::runtime_error(std::string("libpyg_b200: ") + pyg_last_error());
 }
+
+// PYG_ADAPTER_PROFILE=1: calls and wall time per C-ABI entry, printed to stderr at exit
+struct Prof {
+  struct Row {
+    int64_t calls = 0;
+    double ms = 0;
+  };
+  std::map<std::string, Row> rows;
+  bool on = std::getenv("PYG_ADAPTER_PROFILE") != nullptr;
+  ~Prof() {
+    if (!on) return;
+    std::vector<std::pair<double, std::string>> v;
+    for (auto& [k, r] : rows) v.emplace_back(r.ms, k);
+    std::sort(v.rbegin(), v.rend());
+    for (auto& [ms, k] : v)
+      std::fprintf(stderr, "%10.1f ms %9lld calls  %s\n", ms, static_cast<long long>(rows[k].calls),
+                   k.c_str());
+  }
+  static Prof& get() {
+    static Prof p;
+    return p;
+  }
+};
+template <class F>
+struct Timed {
+  const char* name;
+  F f;
+  template <class... A>
+  int operator()(A&&... a) const {
+    Prof& p = Prof::get();
+    if (!p.on) return f(std::forward<A>(a)...);
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rc = f(std::forward<A>(a)...);
+    auto& r = p.rows[name];
+    r.calls += 1;
+    r.ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+  }
+};
+#define PYG_T(fn) Timed<decltype(&fn)>{#fn, &fn}
 
 struct Backend {
   pyg_ctx* ctx = nullptr;
@@ -75,7 +118,7 @@ struct Backend {
     std::vector<int64_t> zero(max_slots, 0);
     pyg_config cfg{static_cast<int32_t>(pythia::cache::kBlockTokens), max_slots, d ? std::atoi(d) : 0,
                    0, zero.data(), zero.data(), 4096};
-    check(pyg_create(&cfg, &ctx));
+    check(PYG_T(pyg_create)(&cfg, &ctx));
     tier_epoch.assign(2 * static_cast<size_t>(max_slots) + 1, 0);
   }
 
@@ -128,7 +171,7 @@ std::vector<uint64_t> chain_boundary_hashes(const workflow::TokenSeq& tokens) {
   Backend& b = Backend::get();
   std::vector<uint64_t> out((tokens.size() + kBlockTokens - 1) / kBlockTokens);
   int64_t n = 0;
-  check(pyg_chain_hashes(b.ctx, tokens.data(), static_cast<int64_t>(tokens.size()), out.data(), &n));
+  check(PYG_T(pyg_chain_hashes)(b.ctx, tokens.data(), static_cast<int64_t>(tokens.size()), out.data(), &n));
   out.resize(n);
   return out;
 }
@@ -138,13 +181,13 @@ TierStore::TierStore(int64_t) : slot_(-1), tier_(2) {}
 
 int64_t TierStore::capacity() const {
   int64_t occ, cap, n;
-  check(pyg_tier_stats(Backend::get().ctx, api_slot(slot_), tier_, &occ, &cap, &n));
+  check(PYG_T(pyg_tier_stats)(Backend::get().ctx, api_slot(slot_), tier_, &occ, &cap, &n));
   return cap;
 }
 
 int64_t TierStore::occupancy() const {
   int64_t occ, cap, n;
-  check(pyg_tier_stats(Backend::get().ctx, api_slot(slot_), tier_, &occ, &cap, &n));
+  check(PYG_T(pyg_tier_stats)(Backend::get().ctx, api_slot(slot_), tier_, &occ, &cap, &n));
   return occ;
 }
 
@@ -156,7 +199,7 @@ const std::map<uint64_t, CacheBlock>& TierStore::blocks() const {
   int64_t n = 0;
   if (b.dump_buf.empty()) b.dump_buf.resize(1 << 14);
   for (;;) {
-    check(pyg_tier_dump(b.ctx, api_slot(slot_), tier_, b.dump_buf.data(),
+    check(PYG_T(pyg_tier_dump)(b.ctx, api_slot(slot_), tier_, b.dump_buf.data(),
                         static_cast<int64_t>(b.dump_buf.size()), &n));
     if (n <= static_cast<int64_t>(b.dump_buf.size())) break;
     b.dump_buf.resize(2 * n);
@@ -171,7 +214,7 @@ const CacheBlock* TierStore::find_chain(uint64_t chain_hash) const {
   Backend& b = Backend::get();
   pyg_block x{};
   int32_t found = 0;
-  check(pyg_tier_find(b.ctx, api_slot(slot_), tier_, chain_hash, &x, &found));
+  check(PYG_T(pyg_tier_find)(b.ctx, api_slot(slot_), tier_, chain_hash, &x, &found));
   if (!found) return nullptr;
   found_ = b.block(x);
   return &found_;
@@ -186,20 +229,20 @@ uint64_t TierStore::put(uint64_t chain_hash, int64_t span_start, int64_t span_en
   Backend& b = Backend::get();
   b.bump(slot_, tier_);
   uint64_t id = 0;
-  check(pyg_tier_put(b.ctx, api_slot(slot_), tier_, chain_hash, span_start, span_end,
+  check(PYG_T(pyg_tier_put)(b.ctx, api_slot(slot_), tier_, chain_hash, span_start, span_end,
                      b.wf(lineage.workflow_id), b.role(lineage.role_id), now, pin_delta, &id));
   return id;
 }
 
 void TierStore::erase(uint64_t block_id) {
   Backend::get().bump(slot_, tier_);
-  check(pyg_tier_erase(Backend::get().ctx, api_slot(slot_), tier_, block_id));
+  check(PYG_T(pyg_tier_erase)(Backend::get().ctx, api_slot(slot_), tier_, block_id));
 }
 
 int64_t TierStore::matched_prefix(const workflow::TokenSeq& tokens,
                                   const std::vector<uint64_t>&) const {
   int64_t m = 0;
-  check(pyg_matched_prefix(Backend::get().ctx, api_slot(slot_), tier_, tokens.data(),
+  check(PYG_T(pyg_matched_prefix)(Backend::get().ctx, api_slot(slot_), tier_, tokens.data(),
                            static_cast<int64_t>(tokens.size()), &m));
   return m;
 }
@@ -210,7 +253,7 @@ CacheHierarchy::CacheHierarchy(int64_t l1_capacity, int64_t l2_capacity)
   Backend& b = Backend::get();
   if (slot_ >= b.max_slots)
     throw std::runtime_error("libpyg_b200 adapter: raise PYG_ENGINE_MAX_REPLICAS");
-  check(pyg_set_capacity(b.ctx, slot_, l1_capacity, l2_capacity));
+  check(PYG_T(pyg_set_capacity)(b.ctx, slot_, l1_capacity, l2_capacity));
   b.bump(slot_, 0);
   b.bump(slot_, 1);
 }
@@ -223,7 +266,7 @@ CacheHierarchy::Match CacheHierarchy::lookup(const workflow::TokenSeq& prompt,
     if (!(v.valid && v.epoch == b.epoch && slot_ < v.n_slots && v.tokens == prompt)) {
       v.n_slots = b.next_slot;
       v.m.resize(3 * static_cast<size_t>(v.n_slots));
-      check(pyg_lookup_all(b.ctx, prompt.data(), static_cast<int64_t>(prompt.size()), 0,
+      check(PYG_T(pyg_lookup_all)(b.ctx, prompt.data(), static_cast<int64_t>(prompt.size()), 0,
                            v.n_slots, v.m.data()));
       v.tokens = prompt;
       v.epoch = b.epoch;
@@ -232,7 +275,7 @@ CacheHierarchy::Match CacheHierarchy::lookup(const workflow::TokenSeq& prompt,
     return {v.m[3 * slot_], v.m[3 * slot_ + 1], 0};
   }
   int64_t m[3];
-  check(pyg_lookup(b.ctx, slot_, prompt.data(), static_cast<int64_t>(prompt.size()), 1, m));
+  check(PYG_T(pyg_lookup)(b.ctx, slot_, prompt.data(), static_cast<int64_t>(prompt.size()), 1, m));
   return {m[0], m[1], m[2]};
 }
 
@@ -240,24 +283,24 @@ void CacheHierarchy::insert_chain(Tier t, const workflow::TokenSeq& tokens, int6
                                   const Lineage& lineage, double now, int pin_delta) {
   Backend& b = Backend::get();
   b.bump(slot_, t == Tier::L1 ? 0 : 1);  // tier(L3) aliases L2
-  check(pyg_insert_chain(b.ctx, slot_, static_cast<int32_t>(t), tokens.data(),
+  check(PYG_T(pyg_insert_chain)(b.ctx, slot_, static_cast<int32_t>(t), tokens.data(),
                          static_cast<int64_t>(tokens.size()), upto, b.wf(lineage.workflow_id),
                          b.role(lineage.role_id), now, pin_delta));
 }
 
 void CacheHierarchy::unpin_chain(const workflow::TokenSeq& tokens, int64_t upto) {
   Backend::get().bump(slot_, 0);
-  check(pyg_unpin_chain(Backend::get().ctx, slot_, tokens.data(),
+  check(PYG_T(pyg_unpin_chain)(Backend::get().ctx, slot_, tokens.data(),
                         static_cast<int64_t>(tokens.size()), upto));
 }
 
 void CacheHierarchy::add_decode_tokens(int64_t n) {
-  check(pyg_add_decode_tokens(Backend::get().ctx, slot_, n));
+  check(PYG_T(pyg_add_decode_tokens)(Backend::get().ctx, slot_, n));
 }
 
 int64_t CacheHierarchy::l1_occupancy() const {
   int64_t o = 0;
-  check(pyg_l1_occupancy(Backend::get().ctx, slot_, &o));
+  check(PYG_T(pyg_l1_occupancy)(Backend::get().ctx, slot_, &o));
   return o;
 }
 
@@ -270,13 +313,13 @@ std::set<std::string> future_nodes(const workflow::PathCursor& position) {
 
 void FutureRegistry::update(const std::string& workflow_id, std::set<std::string> roles) {
   Backend& b = Backend::get();
-  check(pyg_registry_update(b.ctx, b.wf(workflow_id), b.mask(roles)));
+  check(PYG_T(pyg_registry_update)(b.ctx, b.wf(workflow_id), b.mask(roles)));
   futures_[workflow_id] = std::move(roles);
 }
 
 void FutureRegistry::drop(const std::string& workflow_id) {
   Backend& b = Backend::get();
-  check(pyg_registry_drop(b.ctx, b.wf(workflow_id)));
+  check(PYG_T(pyg_registry_drop)(b.ctx, b.wf(workflow_id)));
   futures_.erase(workflow_id);
 }
 
@@ -373,7 +416,7 @@ EvictionResult evict_for_space(CacheHierarchy& cache, Tier tier, int64_t needed,
   static std::vector<uint64_t> ids(1 << 20);
   int64_t n = 0, ft = 0;
   int32_t ok = 0;
-  check(pyg_evict_for_space(b.ctx, cache.tier(Tier::L1).slot(), static_cast<int32_t>(tier), needed,
+  check(PYG_T(pyg_evict_for_space)(b.ctx, cache.tier(Tier::L1).slot(), static_cast<int32_t>(tier), needed,
                             speculative, ids.data(), static_cast<int64_t>(ids.size()), &n, &ft,
                             &ok));
   if (n > static_cast<int64_t>(ids.size()))
@@ -419,7 +462,7 @@ RoutingDecision route(const std::vector<NodeView>& nodes, const Reservation& req
   const pyg_reservation q{req.prompt_len, req.upper, req.alpha, req.tokens_generated};
   if (asg.empty()) asg.push_back({0, 0, 0.0, 0});  // never read: off[n] == 0
   pyg_decision d{};
-  check(pyg_route(b.ctx, n, rid.data(), kv.data(), off.data(), asg.data(), staged.data(), &q, eps,
+  check(PYG_T(pyg_route)(b.ctx, n, rid.data(), kv.data(), off.data(), asg.data(), staged.data(), &q, eps,
                   &d));
   RoutingDecision out;
   if (d.target >= 0) out.target = d.target;
@@ -471,14 +514,14 @@ std::vector<size_t> form_batch(const std::vector<QueueItem>& pool, int64_t activ
   auto* d_order = reinterpret_cast<int32_t*>(p + 32 + n * sizeof(pyg_queue_item));
   auto* d_n = d_order + n;
   const auto* d_hdr = reinterpret_cast<const int64_t*>(p);
-  check(pyg_set_stream(b.ctx, nullptr));
-  check(pyg_form_batch_dev(b.ctx, 1, d_hdr, reinterpret_cast<const pyg_queue_item*>(p + 32),
+  check(PYG_T(pyg_set_stream)(b.ctx, nullptr));
+  check(PYG_T(pyg_form_batch_dev)(b.ctx, 1, d_hdr, reinterpret_cast<const pyg_queue_item*>(p + 32),
                            d_hdr + 2, d_hdr + 3, now, aging_rate, d_order, d_n));
   int32_t na = 0;
   std::vector<int32_t> ord(n);
   cudaMemcpy(&na, d_n, 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(ord.data(), d_order, n * 4, cudaMemcpyDeviceToHost);
-  check(pyg_check_device_error(b.ctx));
+  check(PYG_T(pyg_check_device_error)(b.ctx));
   return std::vector<size_t>(ord.begin(), ord.begin() + na);
 }
 
@@ -495,8 +538,8 @@ size_t select_preemption_victim(const std::vector<QueueItem>& active, double now
   cudaMemcpy(p, hdr, 16, cudaMemcpyHostToDevice);
   cudaMemcpy(p + 16, items.data(), n * sizeof(pyg_queue_item), cudaMemcpyHostToDevice);
   auto* d_v = reinterpret_cast<int32_t*>(p + 16 + n * sizeof(pyg_queue_item));
-  check(pyg_set_stream(b.ctx, nullptr));
-  check(pyg_preemption_victim_dev(b.ctx, 1, reinterpret_cast<const int64_t*>(p),
+  check(PYG_T(pyg_set_stream)(b.ctx, nullptr));
+  check(PYG_T(pyg_preemption_victim_dev)(b.ctx, 1, reinterpret_cast<const int64_t*>(p),
                                   reinterpret_cast<const pyg_queue_item*>(p + 16), now, aging_rate,
                                   d_v));
   int32_t v = 0;
@@ -515,7 +558,7 @@ std::optional<int> route_least_outstanding(const std::vector<NodeView>& nodes) {
     off[i + 1] = off[i] + static_cast<int64_t>(nodes[i].assigned.size());
   }
   int32_t t = -1;
-  check(pyg_route_least_outstanding(b.ctx, n, rid.data(), off.data(), &t));
+  check(PYG_T(pyg_route_least_outstanding)(b.ctx, n, rid.data(), off.data(), &t));
   if (t < 0) return std::nullopt;
   return t;
 }
