@@ -113,6 +113,19 @@ int pyg_tier_put(pyg_ctx* ctx, int32_t replica, int32_t tier, uint64_t chain_has
                  int32_t pin_delta, uint64_t* out_id);
 /* TierStore::erase (hierarchy.cpp:68-82) */
 int pyg_tier_erase(pyg_ctx* ctx, int32_t replica, int32_t tier, uint64_t block_id);
+/* One block of a pyg_tier_put_many list (TierStore::put arguments, hierarchy.cpp:44-66). */
+typedef struct {
+  uint64_t chain_hash;
+  int64_t span_start, span_end;
+  int32_t workflow, role;
+} pyg_put_item;
+/* TierStore::erase / put of a whole list, in list order, stream-ordered (no host sync; the
+   host arrays may be reused when the call returns).  put_many returns no ids: for callers
+   that do not use them (apply_completion's L3 writes, manager.cpp:44-58). */
+int pyg_tier_erase_many(pyg_ctx* ctx, int32_t replica, int32_t tier, const uint64_t* ids,
+                        int64_t n);
+int pyg_tier_put_many(pyg_ctx* ctx, int32_t replica, int32_t tier, const pyg_put_item* items,
+                      int64_t n, double now, int32_t pin_delta);
 /* TierStore::find_chain (hierarchy.cpp:32-42) */
 int pyg_tier_find(pyg_ctx* ctx, int32_t replica, int32_t tier, uint64_t chain_hash,
                   pyg_block* out, int32_t* found);

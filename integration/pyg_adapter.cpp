@@ -96,6 +96,13 @@ struct Backend {
   size_t tkey(int32_t slot, int32_t tier) const {
     return tier == 2 || slot < 0 ? 2 * static_cast<size_t>(max_slots) : 2 * static_cast<size_t>(slot) + tier;
   }
+  // host mirrors, exact by construction: a tier's occupancy as read after its last change
+  // (re-read once the tier's epoch moves), capacities (fixed), decode tokens per slot (every
+  // change goes through add_decode_tokens; pushed to the device lazily, before the device
+  // next reads it -- an eviction on that slot)
+  std::vector<int64_t> occ, cap, decode, decode_pending;
+  std::vector<uint64_t> occ_ep;
+  std::vector<char> cap_ok;
   void bump() { ++epoch; }
   void bump(int32_t slot, int32_t tier) {
     ++epoch;
@@ -120,6 +127,35 @@ struct Backend {
                    0, zero.data(), zero.data(), 4096};
     check(PYG_T(pyg_create)(&cfg, &ctx));
     tier_epoch.assign(2 * static_cast<size_t>(max_slots) + 1, 0);
+    occ.assign(tier_epoch.size(), 0);
+    cap.assign(tier_epoch.size(), 0);
+    occ_ep.assign(tier_epoch.size(), ~0ULL);
+    cap_ok.assign(tier_epoch.size(), 0);
+    decode.assign(max_slots, 0);
+    decode_pending.assign(max_slots, 0);
+  }
+  void stats(int32_t slot, int32_t tier) {
+    const size_t k = tkey(slot, tier);
+    if (occ_ep[k] == tier_epoch[k] && cap_ok[k]) return;
+    int64_t o, c, n;
+    check(PYG_T(pyg_tier_stats)(ctx, slot < 0 ? 0 : slot, tier, &o, &c, &n));
+    occ[k] = o;
+    cap[k] = c;
+    occ_ep[k] = tier_epoch[k];
+    cap_ok[k] = 1;
+  }
+  int64_t occupancy(int32_t slot, int32_t tier) {
+    stats(slot, tier);
+    return occ[tkey(slot, tier)];
+  }
+  int64_t capacity(int32_t slot, int32_t tier) {
+    stats(slot, tier);
+    return cap[tkey(slot, tier)];
+  }
+  void flush_decode(int32_t slot) {
+    if (decode_pending[slot] == 0) return;
+    check(PYG_T(pyg_add_decode_tokens)(ctx, slot, decode_pending[slot]));
+    decode_pending[slot] = 0;
   }
 
   int32_t wf(const std::string& s) {
@@ -179,17 +215,9 @@ std::vector<uint64_t> chain_boundary_hashes(const workflow::TokenSeq& tokens) {
 // ------------------------------------------------------------------ TierStore
 TierStore::TierStore(int64_t) : slot_(-1), tier_(2) {}
 
-int64_t TierStore::capacity() const {
-  int64_t occ, cap, n;
-  check(PYG_T(pyg_tier_stats)(Backend::get().ctx, api_slot(slot_), tier_, &occ, &cap, &n));
-  return cap;
-}
+int64_t TierStore::capacity() const { return Backend::get().capacity(slot_, tier_); }
 
-int64_t TierStore::occupancy() const {
-  int64_t occ, cap, n;
-  check(PYG_T(pyg_tier_stats)(Backend::get().ctx, api_slot(slot_), tier_, &occ, &cap, &n));
-  return occ;
-}
+int64_t TierStore::occupancy() const { return Backend::get().occupancy(slot_, tier_); }
 
 const std::map<uint64_t, CacheBlock>& TierStore::blocks() const {
   Backend& b = Backend::get();
@@ -295,16 +323,18 @@ void CacheHierarchy::unpin_chain(const workflow::TokenSeq& tokens, int64_t upto)
 }
 
 void CacheHierarchy::add_decode_tokens(int64_t n) {
-  check(PYG_T(pyg_add_decode_tokens)(Backend::get().ctx, slot_, n));
+  Backend& b = Backend::get();
+  b.decode[slot_] += n;  // hierarchy.hpp:111; reaches the device before its next eviction
+  b.decode_pending[slot_] += n;
 }
 
+// hierarchy.hpp:114: blocks + in-flight decode tokens
 int64_t CacheHierarchy::l1_occupancy() const {
-  int64_t o = 0;
-  check(PYG_T(pyg_l1_occupancy)(Backend::get().ctx, slot_, &o));
-  return o;
+  Backend& b = Backend::get();
+  return b.occupancy(slot_, 0) + b.decode[slot_];
 }
 
-int64_t CacheHierarchy::decode_tokens() const { return l1_occupancy() - l1_.occupancy(); }
+int64_t CacheHierarchy::decode_tokens() const { return Backend::get().decode[slot_]; }
 
 // ------------------------------------------------------------------- manager
 std::set<std::string> future_nodes(const workflow::PathCursor& position) {
@@ -346,10 +376,15 @@ std::vector<CompletionAction> on_request_complete(const workflow::RequestEnvelop
 }
 
 // manager.cpp:44-58: one dump per tier, then device erases / L3 puts in action order
+// manager.cpp:44-58: the erases (per tier) and the L3 writes go to the device as two ordered
+// lists -- they touch different tiers, so only the order within each list matters
 void apply_completion(const std::vector<CompletionAction>& actions, CacheHierarchy& cache,
                       SharedL3& l3, double now) {
+  Backend& b = Backend::get();
   std::map<uint64_t, CacheBlock> view[2];
   bool have[2] = {false, false};
+  std::vector<uint64_t> frees[2];
+  std::vector<pyg_put_item> puts;
   for (const auto& a : actions) {
     const int k = a.tier == Tier::L1 ? 0 : 1;
     if (!have[k]) {
@@ -359,14 +394,27 @@ void apply_completion(const std::vector<CompletionAction>& actions, CacheHierarc
     auto it = view[k].find(a.block_id);
     if (it == view[k].end()) continue;
     if (a.kind == CompletionAction::Kind::Free) {
-      cache.tier(a.tier).erase(a.block_id);
+      frees[k].push_back(a.block_id);
       view[k].erase(it);
     } else {
       const CacheBlock& blk = it->second;
-      l3.store().put(blk.chain_hash, blk.span_start, blk.span_end, blk.lineage, now, 0,
-                     l3.id_counter());
+      puts.push_back({blk.chain_hash, blk.span_start, blk.span_end, b.wf(blk.lineage.workflow_id),
+                      b.role(blk.lineage.role_id)});
     }
   }
+  const int32_t slot = cache.tier(Tier::L1).slot();
+  for (int k = 0; k < 2; ++k) {
+    if (frees[k].empty()) continue;
+    b.bump(slot, k);
+    check(PYG_T(pyg_tier_erase_many)(b.ctx, slot, k, frees[k].data(),
+                                     static_cast<int64_t>(frees[k].size())));
+  }
+  if (!puts.empty()) {
+    b.bump(-1, 2);
+    check(PYG_T(pyg_tier_put_many)(b.ctx, 0, 2, puts.data(), static_cast<int64_t>(puts.size()),
+                                   now, 0));
+  }
+  (void)l3;
 }
 
 // manager.cpp:60-100 with device lookups
@@ -412,7 +460,17 @@ std::vector<StageAction> on_prefetch_requested(const workflow::RequestEnvelope& 
 EvictionResult evict_for_space(CacheHierarchy& cache, Tier tier, int64_t needed,
                                const FutureRegistry&, bool speculative) {
   Backend& b = Backend::get();
-  b.bump(cache.tier(Tier::L1).slot(), tier == Tier::L1 ? 0 : 1);  // tier(L3) aliases L2
+  const int32_t slot = cache.tier(Tier::L1).slot();
+  const int32_t tt = tier == Tier::L1 ? 0 : 1;  // tier(L3) aliases L2
+  // manager.cpp:106-111 on the host mirrors: no excess, nothing to do
+  const int64_t base = tt == 0 ? cache.l1_occupancy() : b.occupancy(slot, 1);
+  if (base + needed - b.capacity(slot, tt) <= 0) {
+    EvictionResult r;
+    r.satisfied = true;
+    return r;
+  }
+  b.flush_decode(slot);
+  b.bump(slot, tt);
   static std::vector<uint64_t> ids(1 << 20);
   int64_t n = 0, ft = 0;
   int32_t ok = 0;

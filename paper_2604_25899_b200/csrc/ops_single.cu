@@ -75,6 +75,48 @@ __global__ void k_erase_id(CtxDev c, int ti, uint64_t id) {
   }
 }
 
+// TierStore::erase of a list of ids, in order (one thread: each is a binary search)
+__global__ void k_erase_ids(CtxDev c, int ti, const uint64_t* ids, int64_t n) {
+  TierDev* tp = c.tiers + ti;
+  const TierDev t = *tp;
+  int64_t occ = 0, cnt = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    const uint64_t id = ids[k];
+    int64_t lo = 0, hi = t.log_len - 1;
+    while (lo <= hi) {
+      const int64_t mid = (lo + hi) / 2;
+      const uint64_t v = t.log[mid].id;
+      if (v == id) {
+        if (t.log[mid].flags & kAlive) {
+          occ += erase_at(t, mid);
+          cnt += 1;
+        }
+        break;
+      }
+      if (v < id)
+        lo = mid + 1;
+      else
+        hi = mid - 1;
+    }
+  }
+  tp->occupancy -= occ;
+  tp->n_alive -= cnt;
+}
+
+struct PutListGet {
+  const pyg_put_item* items;
+  __device__ PutItem operator()(int64_t i) const {
+    const pyg_put_item x = items[i];
+    return PutItem{x.chain_hash, 0, x.span_start, x.span_end, x.workflow, x.role, 1};
+  }
+};
+
+// TierStore::put of a list of blocks, in order (one warp, warp_put_ordered)
+__global__ void k_put_list(CtxDev c, int ti, const pyg_put_item* items, int64_t n, double now,
+                           int32_t pin) {
+  warp_put_ordered(c, c.tiers + ti, n, PutListGet{items}, now, pin);
+}
+
 __global__ void k_find(CtxDev c, int ti, uint64_t hash, pyg_block* out, int32_t* found) {
   const TierDev t = c.tiers[ti];
   const int64_t li = idx_find(t, hash);
@@ -490,7 +532,50 @@ int pyg_tier_erase(pyg_ctx* c, int32_t replica, int32_t tier, uint64_t id) {
   if (rc) return rc;
   k_erase_id<<<1, 1, 0, c->stream>>>(c->hd, ti, id);
   PYG_LAUNCHED(c);
-  PYG_CUDA(cudaStreamSynchronize(c->stream));
+  return PYG_OK;  // stream-ordered: nothing to return, later calls see the erase
+}
+
+int pyg_tier_erase_many(pyg_ctx* c, int32_t replica, int32_t tier, const uint64_t* ids,
+                        int64_t n) {
+  PYG_ON_DEVICE(c);
+  if (c) dir_touch(c);
+  int ti;
+  int rc = tier_index(c, replica, tier, false, &ti);
+  if (rc) return rc;
+  if (n < 0 || (n && !ids)) return PYG_EINVAL;
+  if (!n) return PYG_OK;
+  void* sp;
+  if ((rc = aux(c, static_cast<size_t>(n) * 8 + 64, &sp))) return rc;
+  // pageable source: the copy is staged before the call returns, the host list may go
+  PYG_CUDA(cudaMemcpyAsync(sp, ids, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice,
+                           c->stream));
+  k_erase_ids<<<1, 1, 0, c->stream>>>(c->hd, ti, static_cast<const uint64_t*>(sp), n);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_tier_put_many(pyg_ctx* c, int32_t replica, int32_t tier, const pyg_put_item* items,
+                      int64_t n, double now, int32_t pin) {
+  PYG_ON_DEVICE(c);
+  if (c) dir_touch(c);
+  int ti;
+  int rc = tier_index(c, replica, tier, false, &ti);
+  if (rc) return rc;
+  if (n < 0 || (n && !items)) return PYG_EINVAL;
+  if (!n) return PYG_OK;
+  for (int64_t k = 0; k < n; ++k)
+    if (items[k].span_end < items[k].span_start) {
+      set_error("span_end < span_start");
+      return PYG_EINVAL;
+    }
+  if ((rc = ensure_capacity(c, ti, n))) return rc;
+  void* sp;
+  if ((rc = aux(c, static_cast<size_t>(n) * sizeof(pyg_put_item) + 64, &sp))) return rc;
+  PYG_CUDA(cudaMemcpyAsync(sp, items, static_cast<size_t>(n) * sizeof(pyg_put_item),
+                           cudaMemcpyHostToDevice, c->stream));
+  k_put_list<<<1, 32, 0, c->stream>>>(c->hd, ti, static_cast<const pyg_put_item*>(sp), n, now,
+                                      pin);
+  PYG_LAUNCHED(c);
   return PYG_OK;
 }
 
