@@ -77,8 +77,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
-    ap.add_argument("--split-min", type=int, default=8192,
-                    help="K1: prompts of >= this many tokens are split tasks (0 = never)")
+    ap.add_argument("--split-min", type=int, default=-1,
+                    help="K1: prompts of >= this many tokens are split tasks (0 = never, "
+                         "-1 = from the batch's token count)")
     ap.add_argument("--free-sms", type=int, default=8,
                     help="K1 of step k+1 overlaps step k on a second stream, its grid capped at "
                          "(SMs - free_sms); -1 = no overlap (serial step)")

@@ -209,10 +209,11 @@ int pyg_hash_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_
    whose K1 overlaps another ctx's step on a second stream leaves SMs free for the step's
    latency-bound kernels (route, admission) this way. */
 int pyg_set_hash_ctas(pyg_ctx* ctx, int32_t n_ctas);
-/* K1 hashes prompts of >= min_tokens tokens (default 8192; 0 = never) as split tasks: one
-   warp per prompt, 512 tokens at a time, through the low-byte decomposition of FNV-1a
-   (k_hash.cu) -- the same hashes, without the long-prompt tail of one lane per request.
-   Requires B % 16 == 0 (otherwise ignored). */
+/* K1 hashes prompts of >= min_tokens tokens as split tasks: one warp per prompt, 512 tokens
+   at a time, through the low-byte decomposition of FNV-1a (k_hash.cu) -- the same hashes,
+   without the long-prompt tail of one lane per request.  0 = never; -1 (default) = a
+   threshold from the batch's token count (1,024 .. 16,384 tokens).  Requires B % 16 == 0
+   (otherwise ignored). */
 int pyg_set_hash_split(pyg_ctx* ctx, int64_t min_tokens);
 
 /* K2: staged matrix.  For request r and its j-th candidate replica cand[cand_off[g_r]+j]

@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(32) k_hash_seq(const uint64_t* __restrict__ to
 }
 
 __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val,
-                           int64_t split_min, int* n_split) {
+                           int64_t split_min, int* n_split, unsigned long long* total) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = r < R ? tok_off[r + 1] - tok_off[r] : 0;
   if (r < R) {
@@ -484,11 +484,39 @@ __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t
     key[r] = static_cast<uint16_t>(L > 65535 ? 65535 : L);
     val[r] = r;
   }
-  // split tasks: the n_split requests of >= split_min tokens.  They lead the descending
-  // length order up to key ties at the threshold, which only decide which of two equally
-  // long requests is split -- either way exact.
-  const unsigned m = __ballot_sync(kFull, r < R && split_min > 0 && n >= split_min);
-  if (m && (threadIdx.x & 31) == 0) atomicAdd(n_split, __popc(m));
+  // fixed threshold: count the split requests here; adaptive (split_min < 0): sum the tokens
+  // for k_split_count
+  if (split_min > 0) {
+    const unsigned m = __ballot_sync(kFull, r < R && n >= split_min);
+    if (m && (threadIdx.x & 31) == 0) atomicAdd(n_split, __popc(m));
+  } else if (split_min < 0) {
+    unsigned long long v = static_cast<unsigned long long>(n);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+  }
+}
+
+// Adaptive split threshold: the longest one-lane task costs ~119 cycles per token
+// (~63 ns), the whole batch ~tokens / 250 Gtok/s on one B200; prompts longer than half of
+// that span (>= 1,024 tokens, <= 16,384) become split tasks, which hash a prompt ~10x
+// faster at ~2.3x the instructions -- a short batch is no longer as slow as its longest
+// prompt, a large one keeps most of its tokens on the cheaper path.  The split requests are
+// the first n_split of the descending order (binary search of the sorted keys).
+__global__ void k_split_count(const uint16_t* sorted_keys, int R, const unsigned long long* total,
+                              int* n_split) {
+  if (threadIdx.x) return;
+  const double bulk_s = static_cast<double>(*total) / 250e9;
+  int64_t T = static_cast<int64_t>(bulk_s / 63e-9 / 2.0);
+  T = T < 1024 ? 1024 : (T > 16384 ? 16384 : T);
+  const uint16_t kmin = static_cast<uint16_t>((T + 3) >> 2);
+  int lo = 0, hi = R;  // first index whose key < kmin
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sorted_keys[mid] >= kmin) lo = mid + 1;
+    else hi = mid;
+  }
+  *n_split = lo;
 }
 
 __global__ void k_nblocks(const int64_t* tok_off, int R, int B, int64_t* nb) {
@@ -592,15 +620,21 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   auto* v_out = reinterpret_cast<int32_t*>(p + 2 * kb + vb);
   void* d_tmp = p + 2 * kb + 2 * vb;
   auto* ctr0 = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
-  PYG_CUDA(cudaMemsetAsync(ctr0, 0, 8, c->stream));  // [0] task counter, [1] split requests
+  auto* tot = reinterpret_cast<unsigned long long*>(ctr0 + 2);
+  // [0] task counter, [1] split requests, [2..3] total tokens
+  PYG_CUDA(cudaMemsetAsync(ctr0, 0, 16, c->stream));
   // split tasks: the fused-assembly loader and B % 16 != 0 keep one lane per request
   const int64_t split_min0 = (!kGather && c->B % kSplitTok == 0) ? c->split_min : 0;
   k_len_keys<<<(R + 255) / 256, 256, 0, c->stream>>>(d_tok_off, R, k_in, v_in, split_min0,
-                                                     ctr0 + 1);
+                                                     ctr0 + 1, tot);
   PYG_LAUNCHED(c);
   PYG_CUDA(cub::DeviceRadixSort::SortPairsDescending(d_tmp, tmp, k_in, k_out, v_in, v_out, R, 0,
                                                      16, c->stream));
   PYG_LAUNCHED(c);
+  if (split_min0 < 0) {
+    k_split_count<<<1, 32, 0, c->stream>>>(k_out, R, tot, ctr0 + 1);
+    PYG_LAUNCHED(c);
+  }
   PYG_CUDA(pyg_host::device_setup(c->device));
   const int per_block = kWarps * 32;
   const int n_sm = pyg_host::sm_count(c->device);
@@ -654,8 +688,8 @@ int pyg_assemble_hash_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
 
 int pyg_set_hash_split(pyg_ctx* c, int64_t min_tokens) {
   PYG_ON_DEVICE(c);
-  if (!c || min_tokens < 0) return PYG_EINVAL;
-  c->split_min = (min_tokens + 3) & ~int64_t{3};
+  if (!c || min_tokens < -1) return PYG_EINVAL;
+  c->split_min = min_tokens < 0 ? -1 : (min_tokens + 3) & ~int64_t{3};
   return PYG_OK;
 }
 

@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="1000,16000,125000")
-    ap.add_argument("--splits", default="8192,4096,0")
+    ap.add_argument("--splits", default="-1,8192,4096,0")
     a = ap.parse_args()
     from paper_2604_25899_b200 import Context
     from paper_2604_25899_b200 import batch as PB
