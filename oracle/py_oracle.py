@@ -314,6 +314,8 @@ class Reference(_Backend):
         s("pref_burst", i64, vp, i32, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp,
           vp, vp, i32, dbl, dbl, i32, i32, vp, vp, vp, vp)
         s("pref_release", None, vp, vp, vp, i32, vp, vp)
+        s("pref_assemble", i32, C.c_char_p, i32, C.c_char_p, vp, vp, vp, vp, i32, vp, i64, vp,
+          vp)
 
     def fnv1a_u64(self, v, h=1469598103934665603):
         return self.lib.pref_fnv1a_u64(v, h)
@@ -503,6 +505,27 @@ class Reference(_Backend):
                               _p(np.ascontiguousarray(tok_off, np.int64)), R,
                               _p(np.ascontiguousarray(rep, np.int32)),
                               _p(np.ascontiguousarray(admitted, np.int32)))
+
+    def assemble(self, text: str, exchanges: dict, prefix=False):
+        """pref_assemble: (rc, tokens, complete) of assemble_prompt / assemble_resolvable_prefix
+        (prompt.cpp:128-164) over a MapPromptHistory; rc 1 = nullopt, -1 = parse error."""
+        ids = list(exchanges)
+        req = [np.asarray(exchanges[k][0], np.uint64) for k in ids]
+        resp = [np.asarray(exchanges[k][1], np.uint64) for k in ids]
+        ro = np.zeros(len(ids) + 1, np.int64)
+        np.cumsum([len(x) for x in req], out=ro[1:])
+        so = np.zeros(len(ids) + 1, np.int64)
+        np.cumsum([len(x) for x in resp], out=so[1:])
+        rt = np.concatenate(req + [np.zeros(1, np.uint64)])
+        st = np.concatenate(resp + [np.zeros(1, np.uint64)])
+        cap = int(ro[-1] + so[-1]) + 64 * (len(text) + 1)
+        out = np.zeros(cap, np.uint64)
+        n = C.c_int64()
+        comp = C.c_int32()
+        rc = self.lib.pref_assemble(text.encode(), len(ids), "\n".join(ids).encode(), _p(ro),
+                                    _p(rt), _p(so), _p(st), int(bool(prefix)), _p(out), cap,
+                                    C.byref(n), C.byref(comp))
+        return rc, (out[:n.value].copy() if rc == 0 else None), bool(comp.value)
 
     def future_mask(self, expr, history):
         m = C.c_uint64()

@@ -31,6 +31,7 @@
 #include "pythia/sched/worker.hpp"
 #include "pythia/workflow/path_analysis.hpp"
 #include "pythia/workflow/path_expr.hpp"
+#include "pythia/workflow/prompt.hpp"
 
 using namespace pythia;
 using cache::CacheHierarchy;
@@ -572,6 +573,49 @@ void pref_release(void** caches, const uint64_t* tokens, const int64_t* tok_off,
     workflow::TokenSeq seq(tokens + tok_off[r], tokens + tok_off[r + 1]);
     static_cast<CacheHierarchy*>(caches[rep[r]])->unpin_chain(seq, static_cast<int64_t>(seq.size()));
   }
+}
+
+// assemble_prompt / assemble_resolvable_prefix (prompt.cpp:128-164) of a template in the
+// reference's placeholder text form (parse_prompt_template, prompt.cpp:75-101) over a
+// MapPromptHistory of n_ex exchanges (ids '\n'-separated; request / response token CSRs).
+// prefix != 0: the resolvable prefix.  Returns 0 and the tokens (*n_out, up to cap written),
+// 1 when assemble_prompt returns nullopt, -1 on a template parse error.
+int pref_assemble(const char* text, int32_t n_ex, const char* ids, const int64_t* req_off,
+                  const uint64_t* req_tok, const int64_t* resp_off, const uint64_t* resp_tok,
+                  int32_t prefix, uint64_t* out, int64_t cap, int64_t* n_out,
+                  int32_t* complete) {
+  workflow::PromptTemplate t;
+  try {
+    t = workflow::parse_prompt_template(text);
+  } catch (const std::exception&) {
+    return -1;
+  }
+  workflow::MapPromptHistory h;
+  std::string all(ids);
+  size_t pos = 0;
+  for (int32_t k = 0; k < n_ex; ++k) {
+    const size_t nl = all.find('\n', pos);
+    const std::string id = all.substr(pos, nl == std::string::npos ? std::string::npos : nl - pos);
+    pos = nl == std::string::npos ? all.size() : nl + 1;
+    workflow::Exchange ex;
+    ex.request.assign(req_tok + req_off[k], req_tok + req_off[k + 1]);
+    ex.response.assign(resp_tok + resp_off[k], resp_tok + resp_off[k + 1]);
+    h.entries[id] = std::move(ex);
+  }
+  workflow::TokenSeq seq;
+  if (prefix) {
+    auto r = workflow::assemble_resolvable_prefix(t, h);
+    seq = std::move(r.tokens);
+    if (complete) *complete = r.complete ? 1 : 0;
+  } else {
+    auto r = workflow::assemble_prompt(t, h);
+    if (!r) return 1;
+    seq = std::move(*r);
+    if (complete) *complete = 1;
+  }
+  *n_out = static_cast<int64_t>(seq.size());
+  if (out) std::memcpy(out, seq.data(), std::min<int64_t>(cap, *n_out) * sizeof(uint64_t));
+  return 0;
 }
 
 // ---- path analysis over a flattened tree (preorder node arrays, the layout of
