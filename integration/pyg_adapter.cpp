@@ -124,7 +124,7 @@ struct Backend {
     const char* d = std::getenv("PYG_ENGINE_DEVICE");
     std::vector<int64_t> zero(max_slots, 0);
     pyg_config cfg{static_cast<int32_t>(pythia::cache::kBlockTokens), max_slots, d ? std::atoi(d) : 0,
-                   0, zero.data(), zero.data(), 4096};
+                   0, zero.data(), zero.data(), 256};  // tiers grow on demand
     check(PYG_T(pyg_create)(&cfg, &ctx));
     tier_epoch.assign(2 * static_cast<size_t>(max_slots) + 1, 0);
     occ.assign(tier_epoch.size(), 0);
@@ -479,6 +479,12 @@ EvictionResult evict_for_space(CacheHierarchy& cache, Tier tier, int64_t needed,
                             &ok));
   if (n > static_cast<int64_t>(ids.size()))
     throw std::runtime_error("libpyg_b200 adapter: eviction list longer than 2^20 blocks");
+  // the mirror follows without a device read: the tier lost exactly the freed tokens
+  const size_t k = b.tkey(slot, tt);
+  if (b.occ_ep[k] == b.tier_epoch[k] - 1) {
+    b.occ[k] -= ft;
+    b.occ_ep[k] = b.tier_epoch[k];
+  }
   EvictionResult r;
   r.freed.assign(ids.begin(), ids.begin() + n);
   r.freed_tokens = ft;
