@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     if (room) {
       ChainGetB gget{hs, L, c.B, a.wf[r], a.role[r]};
       // blocks the insert touches get pinned: no longer eviction candidates
-      uint32_t* klo = reinterpret_cast<uint32_t*>(smem + kSmemSortCap * 8);
+      uint32_t* klo = ec.klo;
       const bool cached = ec.valid != 0;
       const int64_t nc = ec.ncand;
       auto drop = [&](int64_t li) {

@@ -861,6 +861,8 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
 struct EvCache {
   int64_t ncand;
   int32_t valid;
+  uint64_t* khi;  // the cached keys: shared memory, or the tier scratch beyond kSmemSortCap
+  uint32_t* klo;
 };
 constexpr uint32_t kRemoved = 0x7fu << 24;
 
@@ -885,8 +887,6 @@ __device__ inline EvictOut block_evict_admit(const CtxDev& c, TierDev* tp, int64
   if (excess <= 0) return res;
   const TierDev t = *tp;
   const int lane = threadIdx.x & 31;
-  uint64_t* khi = reinterpret_cast<uint64_t*>(smem_keys);
-  uint32_t* klo = reinterpret_cast<uint32_t*>(smem_keys + kSmemSortCap * 8);
   if (!ec->valid) {
     const int64_t n = t.log_len;
     const WarpSeg ls = warp_seg(n);
@@ -897,10 +897,15 @@ __device__ inline EvictOut block_evict_admit(const CtxDev& c, TierDev* tp, int64
     }
     int64_t ncand;
     const int64_t wbase = warp_seg_prefix(wc, swp, &ncand);
-    if (ncand > kSmemSortCap || n >= (1 << 24) || c.B >= 127) {
+    if (n >= (1 << 24) || c.B >= 127) {
       res = block_evict_sorted(c, tp, excess, speculative, nullptr, 0, smem_keys, sm);
       goto stats;
     }
+    // keys in shared memory, or (a large L1: config 3's 8.8k-block tiers) in the tier scratch
+    uint64_t* khi = ncand <= kSmemSortCap ? reinterpret_cast<uint64_t*>(smem_keys) : t.scratch;
+    uint32_t* klo = ncand <= kSmemSortCap
+                        ? reinterpret_cast<uint32_t*>(smem_keys + kSmemSortCap * 8)
+                        : reinterpret_cast<uint32_t*>(t.scratch + 2 * t.log_cap);
     int64_t wpos = wbase;
     for (int64_t base = ls.lo; base < ls.hi; base += 32) {
       const int64_t i = base + lane;
@@ -934,11 +939,15 @@ __device__ inline EvictOut block_evict_admit(const CtxDev& c, TierDev* tp, int64
     if (threadIdx.x == 0) {
       ec->ncand = ncand;
       ec->valid = 1;
+      ec->khi = khi;
+      ec->klo = klo;
     }
     __syncthreads();
   }
   {
     const int64_t ncand = ec->ncand;
+    uint64_t* khi = ec->khi;
+    uint32_t* klo = ec->klo;
     const WarpSeg cs = warp_seg(ncand);
     int64_t rem = excess, nfreed = 0, ftok = 0;
     uint32_t pc = 0;

@@ -475,8 +475,30 @@ __global__ void __launch_bounds__(32) k_hash_seq(const uint64_t* __restrict__ to
   }
 }
 
+// Length histogram of the adaptive split threshold: 4 bins per octave from 512 tokens
+// (bin 0 = shorter), tokens and request counts per bin.
+constexpr int kHistBins = 40;
+__device__ __forceinline__ int len_bin(int64_t n) {
+  if (n < 512) return 0;
+  const double b = 4.0 * log2(static_cast<double>(n) / 512.0);
+  const int k = 1 + static_cast<int>(b);
+  return k < kHistBins ? k : kHistBins - 1;
+}
+__device__ __forceinline__ double bin_lo(int k) { return k == 0 ? 0.0 : 512.0 * exp2((k - 1) / 4.0); }
+
+struct SplitHist {
+  unsigned long long tok[kHistBins];
+  unsigned long long cnt[kHistBins];
+  unsigned long long max_len;
+};
+
 __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val,
-                           int64_t split_min, int* n_split, unsigned long long* total) {
+                           int64_t split_min, int* n_split, SplitHist* hist) {
+  __shared__ unsigned long long s_tok[kHistBins], s_cnt[kHistBins];
+  const bool adaptive = split_min < 0;
+  if (adaptive)
+    for (int k = threadIdx.x; k < kHistBins; k += blockDim.x) s_tok[k] = s_cnt[k] = 0;
+  __syncthreads();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = r < R ? tok_off[r + 1] - tok_off[r] : 0;
   if (r < R) {
@@ -484,32 +506,59 @@ __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t
     key[r] = static_cast<uint16_t>(L > 65535 ? 65535 : L);
     val[r] = r;
   }
-  // fixed threshold: count the split requests here; adaptive (split_min < 0): sum the tokens
-  // for k_split_count
-  if (split_min > 0) {
+  if (split_min > 0) {  // fixed threshold: count the split requests here
     const unsigned m = __ballot_sync(kFull, r < R && n >= split_min);
     if (m && (threadIdx.x & 31) == 0) atomicAdd(n_split, __popc(m));
-  } else if (split_min < 0) {
-    unsigned long long v = static_cast<unsigned long long>(n);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+  } else if (adaptive) {
+    if (r < R) {
+      const int k = len_bin(n);
+      atomicAdd(s_tok + k, static_cast<unsigned long long>(n));
+      atomicAdd(s_cnt + k, 1ULL);
+      atomicMax(&hist->max_len, static_cast<unsigned long long>(n));
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHistBins; k += blockDim.x)
+      if (s_cnt[k]) {
+        atomicAdd(hist->tok + k, s_tok[k]);
+        atomicAdd(hist->cnt + k, s_cnt[k]);
+      }
   }
 }
 
-// Adaptive split threshold: the longest one-lane task costs ~119 cycles per token
-// (~63 ns), the whole batch ~tokens / 250 Gtok/s on one B200; prompts longer than half of
-// that span (>= 1,024 tokens, <= 16,384) become split tasks, which hash a prompt ~10x
-// faster at ~2.3x the instructions -- a short batch is no longer as slow as its longest
-// prompt, a large one keeps most of its tokens on the cheaper path.  The split requests are
+// Adaptive split threshold: choose the length from which prompts become split tasks by a
+// makespan model of K1 on one B200 -- the longest one-lane task (~63 ns per token: ~119
+// cycles), the longest split task (~6 ns per token), the work (~250 Gtok/s one lane per
+// request; split tokens cost ~2.4x) -- over "no split" and the histogram's bin edges from
+// 512 tokens up.  Many long prompts keep one lane each (their chains overlap, config 3); a
+// few long ones in a large batch, or any in a small batch, are split.  The split requests are
 // the first n_split of the descending order (binary search of the sorted keys).
-__global__ void k_split_count(const uint16_t* sorted_keys, int R, const unsigned long long* total,
+__global__ void k_split_count(const uint16_t* sorted_keys, int R, const SplitHist* hist,
                               int* n_split) {
   if (threadIdx.x) return;
-  const double bulk_s = static_cast<double>(*total) / 250e9;
-  int64_t T = static_cast<int64_t>(bulk_s / 63e-9 / 2.0);
-  T = T < 1024 ? 1024 : (T > 16384 ? 16384 : T);
-  const uint16_t kmin = static_cast<uint16_t>((T + 3) >> 2);
+  const double c_lane = 63e-9, c_split = 6e-9, rate = 250e9, extra = 1.4;
+  double total = 0;
+  for (int k = 0; k < kHistBins; ++k) total += static_cast<double>(hist->tok[k]);
+  const double lmax = static_cast<double>(hist->max_len);
+  double best = fmax(lmax * c_lane, total / rate);  // no split
+  double best_T = 1e30;
+  double above = 0;                                  // tokens of bins >= k
+  for (int k = kHistBins - 1; k >= 1; --k) {
+    above += static_cast<double>(hist->tok[k]);
+    if (!hist->cnt[k] && above == 0) continue;
+    const double T = bin_lo(k);
+    const double cost = fmax(fmax(T * c_lane, lmax * c_split), (total + extra * above) / rate);
+    if (cost < best) {
+      best = cost;
+      best_T = T;
+    }
+  }
+  if (best_T >= 1e29) {
+    *n_split = 0;
+    return;
+  }
+  const int64_t Tk = static_cast<int64_t>(best_T);
+  const int64_t kq = (Tk + 3) >> 2;
+  const uint16_t kmin = static_cast<uint16_t>(kq > 65535 ? 65535 : kq);
   int lo = 0, hi = R;  // first index whose key < kmin
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
@@ -611,7 +660,7 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   const size_t kb = (static_cast<size_t>(R) * 2 + 255) & ~size_t{255};
   const size_t vb = (static_cast<size_t>(R) * 4 + 255) & ~size_t{255};
   void* sp;
-  int rc = scratch(c, 2 * kb + 2 * vb + tmp + 768, &sp);
+  int rc = scratch(c, 2 * kb + 2 * vb + tmp + 768 + sizeof(SplitHist), &sp);
   if (rc) return rc;
   char* p = static_cast<char*>(sp);
   auto* k_in = reinterpret_cast<uint16_t*>(p);
@@ -620,19 +669,19 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   auto* v_out = reinterpret_cast<int32_t*>(p + 2 * kb + vb);
   void* d_tmp = p + 2 * kb + 2 * vb;
   auto* ctr0 = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
-  auto* tot = reinterpret_cast<unsigned long long*>(ctr0 + 2);
-  // [0] task counter, [1] split requests, [2..3] total tokens
-  PYG_CUDA(cudaMemsetAsync(ctr0, 0, 16, c->stream));
+  auto* hist = reinterpret_cast<SplitHist*>(ctr0 + 4);
+  // [0] task counter, [1] split requests, then the length histogram
+  PYG_CUDA(cudaMemsetAsync(ctr0, 0, 16 + sizeof(SplitHist), c->stream));
   // split tasks: the fused-assembly loader and B % 16 != 0 keep one lane per request
   const int64_t split_min0 = (!kGather && c->B % kSplitTok == 0) ? c->split_min : 0;
   k_len_keys<<<(R + 255) / 256, 256, 0, c->stream>>>(d_tok_off, R, k_in, v_in, split_min0,
-                                                     ctr0 + 1, tot);
+                                                     ctr0 + 1, hist);
   PYG_LAUNCHED(c);
   PYG_CUDA(cub::DeviceRadixSort::SortPairsDescending(d_tmp, tmp, k_in, k_out, v_in, v_out, R, 0,
                                                      16, c->stream));
   PYG_LAUNCHED(c);
   if (split_min0 < 0) {
-    k_split_count<<<1, 32, 0, c->stream>>>(k_out, R, tot, ctr0 + 1);
+    k_split_count<<<1, 32, 0, c->stream>>>(k_out, R, hist, ctr0 + 1);
     PYG_LAUNCHED(c);
   }
   PYG_CUDA(pyg_host::device_setup(c->device));
