@@ -526,16 +526,16 @@ __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t
 }
 
 // Adaptive split threshold: choose the length from which prompts become split tasks by a
-// makespan model of K1 on one B200 -- the longest one-lane task (~63 ns per token: ~119
-// cycles), the longest split task (~6 ns per token), the work (~250 Gtok/s one lane per
-// request; split tokens cost ~2.4x) -- over "no split" and the histogram's bin edges from
-// 512 tokens up.  Many long prompts keep one lane each (their chains overlap, config 3); a
+// makespan model of K1 on one B200 -- the longest one-lane task, the longest split task, the
+// work (constants below) -- over "no split" and the histogram's bin edges from 512 tokens up.  Many long prompts keep one lane each (their chains overlap, config 3); a
 // few long ones in a large batch, or any in a small batch, are split.  The split requests are
 // the first n_split of the descending order (binary search of the sorted keys).
 __global__ void k_split_count(const uint16_t* sorted_keys, int R, const SplitHist* hist,
                               int* n_split) {
   if (threadIdx.x) return;
-  const double c_lane = 63e-9, c_split = 6e-9, rate = 250e9, extra = 1.4;
+  // measured on B200 (tools/k1_sweep.py): a one-lane chain in a loaded SM ~120 ns per token,
+  // a split task ~8 ns per token, ~250 Gtok/s one lane per request, split tokens ~2.8x
+  const double c_lane = 120e-9, c_split = 8e-9, rate = 250e9, extra = 1.8;
   double total = 0;
   for (int k = 0; k < kHistBins; ++k) total += static_cast<double>(hist->tok[k]);
   const double lmax = static_cast<double>(hist->max_len);

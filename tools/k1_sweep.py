@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="1000,16000,125000")
     ap.add_argument("--splits", default="-1,8192,4096,0")
+    ap.add_argument("--workload", default="bursty")
     a = ap.parse_args()
     from paper_2604_25899_b200 import Context
     from paper_2604_25899_b200 import batch as PB
@@ -29,7 +30,7 @@ def main():
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
     for R in [int(x) for x in a.sizes.split(",")]:
-        tr = S.make_burst(3, R, 1, dev, "bursty", 8)
+        tr = S.make_burst(3, R, 1, dev, a.workload, 8)
         b = S.upload_burst(tr, 16, dev, 3)
         L = np.diff(tr.tok_off)
         nbytes = 8 * int(L.sum()) + 8 * b.b.n_hashes + 16 * (R + 1)
