@@ -716,14 +716,14 @@ def run_sharded(args):
         e.record(H)
         ev_h[k] = e
 
-    def run(k0, n, hevs=None):
+    def run(k0, n, hevs=None, pevs=None):
         hash_into(k0, hevs[0] if hevs else None)
         for i in range(n):
             k = k0 + i
             Sst.wait_event(ev_h.pop(k))
             if i + 1 < n:
                 hash_into(k + 1, hevs[i + 1] if hevs else None)
-            sh.step(k, 1.0 + k)
+            sh.step(k, 1.0 + k, ev=pevs[i] if pevs is not None else None)
 
     run(0, W_)
     torch.cuda.synchronize(dev)
@@ -738,12 +738,17 @@ def run_sharded(args):
     ET = torch.cuda.Event
     hevs = [(ET(enable_timing=True), ET(enable_timing=True)) for _ in range(K)]
     t0, t1 = ET(enable_timing=True), ET(enable_timing=True)
+    pevs = [dict() for _ in range(K)]
     dist.barrier()
     torch.cuda.synchronize(dev)
     t0.record(Sst)
-    run(W_, K, hevs)
+    run(W_, K, hevs, pevs)
     t1.record(Sst)
     torch.cuda.synchronize(dev)
+    names = ["begin", "start", "staged", "exchange", "route", "pull+admit", "l3_chain", "lists"]
+    phase_ms = {("bookkeeping" if a == "begin" else b): sum(p[a].elapsed_time(p[b]) for p in pevs) / K
+                for a, b in zip(names[:-1], names[1:])}
+    phase_ms.pop("start", None)
     launches = ctx.kernel_launches() + hctx.kernel_launches() - l0
     clk = clocks.stop()
     ctx.check_device_error()
@@ -788,6 +793,7 @@ def run_sharded(args):
                          "frac": hash_gbs / peak, "traffic": None, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": int(hash_bytes),
                          "avg_launch_ms": hash_ms, "max_over_ranks_launch_ms": hash_ms_max},
+            "phase_ms_rank0": phase_ms, "hash_ms_rank0": hash_ms,
             "clocks": clk, "gpu_launches": int(cnt[3].item()), "e2e": None,
             "cpu_baseline": None,
         }
@@ -797,6 +803,9 @@ def run_sharded(args):
 
 
 def main():
+    # NCCL's banner would be a second stdout line next to the JSON line
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "INFO", "TRACE"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -59,15 +59,24 @@ class SteadyShardStep(ShardedStep):
     flags).  route_nodes: this rank's node table (global replica ids, own models'
     candidates only)."""
 
-    def step_steady(self, now, route_nodes, after_gather=None):
+    def step_steady(self, now, route_nodes, after_gather=None, ev=None):
+        """ev: optional dict name -> CUDA event, recorded at the phase ends (experiments)."""
         ctx, plan, b, nodes = self.ctx, self.plan, self.b, self.nodes
         lib = _lib._lib
         W = plan.world
+
+        def mark(name):
+            if ev is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev[name] = e
         PB.bind_current_stream(ctx)
+        mark("start")
         check(lib.pyg_staged_matrix_dev(ctx.h, _ptr(b.tokens), _ptr(b.tok_off), _ptr(b.hash_off),
                                         _ptr(b.hashes), plan.R_local, _ptr(b.group),
                                         nodes.n_groups, _ptr(nodes.cand_off), _ptr(nodes.cand),
                                         nodes.max_cand, _ptr(self.staged)))
+        mark("staged")
         mc = max(nodes.max_cand, 1)
         self.seq += 1
         if self.p2p:
@@ -89,6 +98,7 @@ class SteadyShardStep(ShardedStep):
             check(lib.pyg_shard_unpack_dev(ctx.h, _ptr(g_rows), plan.R_total, mc, self.s16,
                                            _ptr(self.g_res), _ptr(self.g_group),
                                            _ptr(self.g_staged)))
+        mark("exchange")
         if after_gather is not None:
             after_gather()
         # K3 over this rank's models only (other models' requests have no local candidates)
@@ -99,6 +109,7 @@ class SteadyShardStep(ShardedStep):
                                       route_nodes.max_cand, _ptr(self.g_staged), 0.05,
                                       _ptr(self.decisions), _ptr(self.placed_off),
                                       _ptr(self.placed)))
+        mark("route")
         check(lib.pyg_shard_recv_plan_dev(ctx.h, plan.R_total, _ptr(self.decisions),
                                           _ptr(self.peers), W, _ptr(self.req_off_d), self.cap_req,
                                           _ptr(self.recv_gidx), _ptr(self.recv_count),
@@ -116,6 +127,7 @@ class SteadyShardStep(ShardedStep):
                                       _ptr(self.recv_role), self.cap_req, _ptr(self.p_off),
                                       _ptr(self.p_loc), now, 1, _ptr(self.adm), _ptr(self.m3),
                                       _ptr(self.l2_list), self.cap_hash, _ptr(self.counts)))
+        mark("pull+admit")
         me = plan.rank
 
         def resolve():
@@ -140,7 +152,9 @@ class SteadyShardStep(ShardedStep):
                                                               me, 0))
                     resolve()
                 barrier_on_stream(self.dev)
+        mark("l3_chain")
         check(lib.pyg_shard_apply_lists_range_dev(ctx.h, _ptr(self.peers), W, me, me, W, 1))
+        mark("lists")
 
     def release_hold(self, hold_all, h):
         """Unpin this burst's admitted requests of hold h on this rank's replicas."""
@@ -219,14 +233,18 @@ class ShardedSteady:
             _ptr(pl), _ptr(req), _ptr(hold), 2, _ptr(self.route_nodes.asg_off),
             _ptr(self.route_nodes.asg)))
 
-    def step(self, k, now, after_gather=None):
+    def step(self, k, now, after_gather=None, ev=None):
         """Everything of step k after K1 of this rank's burst k."""
         PB.bind_current_stream(self.ctx)
+        if ev is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            ev["begin"] = e
         for h in (1, 2):
             if k - h >= 0:
                 self.steps[k - h].release_hold(self.hold_all[k - h], h)
         self.compose_nodes(k)
         rw, rm, nr, mx = self.reg[k]
         check(_lib._lib.pyg_registry_update_batch_dev(self.ctx.h, nr, _ptr(rw), _ptr(rm), mx))
-        self.steps[k].step_steady(now, self.route_nodes, after_gather)
+        self.steps[k].step_steady(now, self.route_nodes, after_gather, ev)
         return self.steps[k]

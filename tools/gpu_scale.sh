@@ -1,12 +1,13 @@
-# usage: NS="1 2" bash tools/gpu_scale.sh   (bench at each N; one JSON line per N into gpurun_out/scale.jsonl)
-python paper_2604_25899_b200/build.py > gpurun_out/build.log 2>&1 || exit 1
-: > gpurun_out/scale.jsonl
-for n in ${NS:-1 2}; do
-  if [ "$n" = 1 ]; then
-    timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline ${BENCH_ARGS} >> gpurun_out/scale.jsonl 2> gpurun_out/scale_$n.err
-  else
-    timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port $((29600+n)) bench.py --gpus $n --steps 10 --warmup 3 ${BENCH_ARGS} >> gpurun_out/scale.jsonl 2> gpurun_out/scale_$n.err
-  fi
-  echo "N=$n rc=$?"; grep -v Warning gpurun_out/scale_$n.err | grep -iE "error|Traceback" -A3 | head -20
+#!/bin/bash
+# scaling: bench at N = 1, 2, 4 (weak: 125k requests per GPU per step) + world-4 parity
+set -x
+python paper_2604_25899_b200/build.py > gpurun_out/build.log 2>&1
+NG=$(nvidia-smi -L | wc -l)
+timeout 900 python -m pytest -q -m gpu tests/test_gpu_steady_shard.py tests/test_gpu_shard.py 2>&1 | tail -3
+for n in 1 2 4; do
+  [ $n -le $NG ] || continue
+  timeout 900 python bench.py --gpus $n --no-cpu-baseline --no-e2e ${BENCH_ARGS} > gpurun_out/scale_n$n.out 2> gpurun_out/scale_n$n.err
+  python -c "import json;d=json.load(open('gpurun_out/scale_n$n.out'));print($n, d['value']/1e6, d['ms_per_step'], d.get('phase_ms'), d['config']['placed_per_step'])"
 done
-cat gpurun_out/scale.jsonl
+python tools/k1_sweep.py --sizes=1000,16000,125000 --splits=-1 2>&1 | tail -3
+python tools/k1_sweep.py --workload long_context --sizes=12500 --splits=-1 2>&1 | tail -1
