@@ -95,7 +95,8 @@ int64_t pyg_kernel_launches(pyg_ctx* ctx);
 /* Counters since creation / the last reset (synchronizes the ctx stream), out[8]: [0] blocks
    evicted by evict_for_space, [1] their tokens, [2] evictions that had work (excess > 0),
    [3] of those unsatisfied, [4] batched admissions tried, [5] admitted, [6] L3 tokens
-   promoted by batched admission, [7] reserved. */
+   promoted by batched admission, [7] whether the last admission call matched anything in L3
+   (the sharded L3 chain's skip condition). */
 int pyg_stats(pyg_ctx* ctx, int64_t* out, int32_t reset);
 /* (Re)sets a replica's tier capacities -- CacheHierarchy(l1_capacity, l2_capacity)
    (hierarchy.hpp:100) for a replica slot the engine provisions later (engine.cpp:197, 1482). */
@@ -404,6 +405,12 @@ int pyg_shard_unpack_peer_dev(pyg_ctx* ctx, const int64_t* d_rows_of, int32_t wo
                               const int64_t* d_req_off, int32_t n_req_total, int32_t max_cand,
                               int32_t staged16, pyg_reservation* d_req, int32_t* d_group,
                               int32_t* d_staged);
+/* The same, with the staged rows copied only for requests of the groups in own_mask (bit g =
+   group g < 64; 0 = every group): a shard that routes only its own models needs no others. */
+int pyg_shard_unpack_peer_own_dev(pyg_ctx* ctx, const int64_t* d_rows_of, int32_t world,
+                                  const int64_t* d_req_off, int32_t n_req, int32_t max_cand,
+                                  int32_t s16, uint64_t own_mask, pyg_reservation* d_req,
+                                  int32_t* d_group, int32_t* d_staged);
 /* Cross-GPU stream barrier over peer memory (replaces a one-element NCCL all-reduce).
    signal: after a system-scope fence, writes seq into slot `me` of every shard's flag array
    (d_flag_of[k] = shard k's int64 flags[world], mapped here).  wait: blocks this stream until
@@ -427,6 +434,11 @@ int pyg_shard_local_placed_dev(pyg_ctx* ctx, const int32_t* d_placed_off, const 
 int pyg_shard_apply_lists_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world, int32_t me);
 /* The same for a subset: L3 erase lists of peers [l3_lo, l3_hi), and (with_l2) the L2
    directory clears of every peer except me. */
+/* The first half of the L3 chain for rank me: wait for the L3 lists of ranks < me and apply
+   them -- skipped on the device when none of this rank's admissions (the last
+   pyg_admit_shard_dev) matched anything in L3, since erasures can only shrink a match. */
+int pyg_shard_l3_prepare_dev(pyg_ctx* ctx, const pyg_peer* d_peers, const int64_t* d_flags,
+                             int32_t world, int32_t me, int64_t seq);
 int pyg_shard_apply_lists_range_dev(pyg_ctx* ctx, const pyg_peer* d_peers, int32_t world,
                                     int32_t me, int32_t l3_lo, int32_t l3_hi, int32_t with_l2);
 /* Admission results of this shard's own requests, read from their owner shards. */

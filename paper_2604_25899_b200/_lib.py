@@ -127,6 +127,7 @@ _sig("pyg_registry_from_cursors_dev", vp, i32, i32, vp, vp, vp, vp)
 _sig("pyg_ipc_import", vp, vp, i64, vp)
 _sig("pyg_shard_recv_plan_dev", vp, i32, vp, vp, i32, vp, i64, vp, vp, vp, vp, vp, vp)
 _sig("pyg_shard_unpack_peer_dev", vp, vp, i32, vp, i32, i32, i32, vp, vp, vp)
+_sig("pyg_shard_unpack_peer_own_dev", vp, vp, i32, vp, i32, i32, i32, C.c_uint64, vp, vp, vp)
 _sig("pyg_shard_signal_dev", vp, vp, i32, i32, i64)
 _sig("pyg_shard_wait_dev", vp, vp, i32, i64)
 _sig("pyg_shard_pack_dev", vp, vp, vp, vp, i32, i32, i32, vp)
@@ -142,6 +143,7 @@ _sig("pyg_registry_update_batch_dev", vp, i32, vp, vp, i32)
 _sig("pyg_registry_reserve", vp, i32)
 _sig("pyg_shard_apply_lists_dev", vp, vp, i32, i32)
 _sig("pyg_shard_apply_lists_range_dev", vp, vp, i32, i32, i32, i32, i32)
+_sig("pyg_shard_l3_prepare_dev", vp, vp, vp, i32, i32, i64)
 _sig("pyg_shard_results_dev", vp, vp, i32, vp, vp, i64, i32, vp, vp)
 _sig("pyg_lookup_batch_dev", vp, vp, vp, vp, vp, i32, vp, i32, vp)
 _sig("pyg_route_batch_dev", vp, i32, C.POINTER(NodesDev), vp, i32, vp, i32, vp, vp, i32, vp,

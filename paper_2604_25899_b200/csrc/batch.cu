@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
       m[2] = bc[2];
       __syncthreads();
     }
+    if (threadIdx.x == 0 && m[2] > 0 && c.stats) atomicOr(c.stats + 7, 1ULL);
     // evict_for_space(L1, needed): base = l1_occupancy() (manager.cpp:106)
     const int64_t excess = t1p->occupancy + c.decode[rep] + (L - m[0]) - t1p->capacity;
     __syncthreads();
@@ -705,6 +706,7 @@ static int admit_core(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok
   if (rc) return rc;
   PYG_CUDA(cudaMemsetAsync(d_admitted, 0, static_cast<size_t>(R) * 4, c->stream));
   PYG_CUDA(cudaMemsetAsync(d_match3, 0, static_cast<size_t>(R) * 24, c->stream));
+  PYG_CUDA(cudaMemsetAsync(c->hd.stats + 7, 0, 8, c->stream));  // "some admission hit L3"
   auto* cnt = reinterpret_cast<unsigned long long*>(d_counts);
   AdmitArgs a{d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, d_placed_off, d_placed,
               now, speculative, d_admitted, d_match3, rec,

@@ -152,25 +152,42 @@ __global__ void k_unpack(const int32_t* rows, int R, int mc, int s16, pyg_reserv
 
 // Unpack the whole burst's route rows straight from every shard's row buffer over NVLink
 // (rows_of[k] = shard k's rows, mapped in this process): the NCCL all-gather's replacement.
+// One warp per 32 rows: lane l unpacks row r0+l's reservation and group, then the warp
+// copies each row's staged values one candidate per lane (coalesced 128-byte stores).
+// own_mask (groups < 64; 0 = all): the staged row is only read for the requests of groups
+// this shard routes -- the others are never evaluated here.
 __global__ void k_unpack_peer(const int64_t* rows_of, int world, const int64_t* req_off, int R,
-                              int mc, int s16, pyg_reservation* req, int32_t* group,
-                              int32_t* staged) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= R) return;
-  const int k = src_of(req_off, world, r);
+                              int mc, int s16, uint64_t own_mask, pyg_reservation* req,
+                              int32_t* group, int32_t* staged) {
+  const int lane = threadIdx.x & 31;
+  const int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+  if (r0 >= R) return;
   const int wd = 5 + (s16 ? (mc + 1) / 2 : mc);
-  const int32_t* o = reinterpret_cast<const int32_t*>(rows_of[k]) +
-                     static_cast<int64_t>(r - req_off[k]) * wd;
-  const int64_t t = (static_cast<int64_t>(o[1]) << 32) | static_cast<uint32_t>(o[0]);
-  const int64_t ab = (static_cast<int64_t>(o[3]) << 32) | static_cast<uint32_t>(o[2]);
-  req[r] = pyg_reservation{t, 0, __longlong_as_double(ab), 0};
-  group[r] = o[4];
-  int32_t* st = staged + static_cast<int64_t>(r) * mc;
-  if (s16) {
-    for (int j = 0; j < mc; ++j)
-      st[j] = static_cast<int32_t>((static_cast<uint32_t>(o[5 + j / 2]) >> (16 * (j & 1))) & 0xffffu);
-  } else {
-    for (int j = 0; j < mc; ++j) st[j] = o[5 + j];
+  const int r = r0 + lane;
+  const int32_t* o = nullptr;
+  bool own = false;
+  if (r < R) {
+    const int k = src_of(req_off, world, r);
+    o = reinterpret_cast<const int32_t*>(rows_of[k]) + static_cast<int64_t>(r - req_off[k]) * wd;
+    const int64_t t = (static_cast<int64_t>(o[1]) << 32) | static_cast<uint32_t>(o[0]);
+    const int64_t ab = (static_cast<int64_t>(o[3]) << 32) | static_cast<uint32_t>(o[2]);
+    req[r] = pyg_reservation{t, 0, __longlong_as_double(ab), 0};
+    const int g = o[4];
+    group[r] = g;
+    own = own_mask == 0 || g < 0 || g >= 64 || ((own_mask >> g) & 1ULL);
+  }
+  unsigned todo = __ballot_sync(kFull, own);
+  while (todo) {
+    const int l = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int32_t* src = reinterpret_cast<const int32_t*>(
+        __shfl_sync(kFull, reinterpret_cast<unsigned long long>(o), l));
+    int32_t* st = staged + static_cast<int64_t>(r0 + l) * mc;
+    for (int j = lane; j < mc; j += 32) {
+      st[j] = s16 ? static_cast<int32_t>((static_cast<uint32_t>(src[5 + j / 2]) >> (16 * (j & 1))) &
+                                         0xffffu)
+                  : src[5 + j];
+    }
   }
 }
 
@@ -188,7 +205,9 @@ __global__ void k_signal(const int64_t* flag_of, int world, int me, int64_t seq)
   }
 }
 
-__global__ void k_wait(const int64_t* flags, int world, int64_t seq, int32_t* err) {
+__global__ void k_wait(const int64_t* flags, int world, int64_t seq, int32_t* err,
+                       const unsigned long long* cond) {
+  if (cond && *cond == 0) return;  // nothing depends on the peers' data this time
   const int k = threadIdx.x;
   if (k < world) {
     uint64_t t0;
@@ -258,7 +277,8 @@ __global__ void k_local_placed(const int32_t* placed_off, const int32_t* placed,
 }
 
 __global__ void k_apply_lists(CtxDev c, const pyg_peer* peers, int world, int me, int l3_lo,
-                              int l3_hi, int with_l2) {
+                              int l3_hi, int with_l2, const unsigned long long* cond) {
+  if (cond && *cond == 0) return;
   TierDev* tp = c.tiers + 2 * c.n_rep;
   for (int k = 0; k < world; ++k) {
     const pyg_peer& p = peers[k];
@@ -464,11 +484,20 @@ int pyg_shard_unpack_dev(pyg_ctx* c, const int32_t* d_rows, int32_t R, int32_t m
 int pyg_shard_unpack_peer_dev(pyg_ctx* c, const int64_t* d_rows_of, int32_t world,
                               const int64_t* d_req_off, int32_t R, int32_t mc, int32_t s16,
                               pyg_reservation* d_req, int32_t* d_group, int32_t* d_staged) {
+  return pyg_shard_unpack_peer_own_dev(c, d_rows_of, world, d_req_off, R, mc, s16, 0, d_req,
+                                       d_group, d_staged);
+}
+
+int pyg_shard_unpack_peer_own_dev(pyg_ctx* c, const int64_t* d_rows_of, int32_t world,
+                                  const int64_t* d_req_off, int32_t R, int32_t mc, int32_t s16,
+                                  uint64_t own_mask, pyg_reservation* d_req, int32_t* d_group,
+                                  int32_t* d_staged) {
   PYG_ON_DEVICE(c);
   if (!c || R < 0 || mc < 0 || world < 1) return PYG_EINVAL;
   if (!R) return PYG_OK;
-  k_unpack_peer<<<(R + 255) / 256, 256, 0, c->stream>>>(d_rows_of, world, d_req_off, R, mc, s16,
-                                                        d_req, d_group, d_staged);
+  const int warps = (R + 31) / 32;
+  k_unpack_peer<<<(warps + 7) / 8, 256, 0, c->stream>>>(d_rows_of, world, d_req_off, R, mc, s16,
+                                                        own_mask, d_req, d_group, d_staged);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -485,7 +514,8 @@ int pyg_shard_signal_dev(pyg_ctx* c, const int64_t* d_flag_of, int32_t world, in
 int pyg_shard_wait_dev(pyg_ctx* c, const int64_t* d_flags, int32_t world, int64_t seq) {
   PYG_ON_DEVICE(c);
   if (!c || world < 1 || world > 1024) return PYG_EINVAL;
-  k_wait<<<1, 32 * ((world + 31) / 32), 0, c->stream>>>(d_flags, world, seq, c->hd.error);
+  k_wait<<<1, 32 * ((world + 31) / 32), 0, c->stream>>>(d_flags, world, seq, c->hd.error,
+                                                         nullptr);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -518,7 +548,7 @@ int pyg_shard_local_placed_dev(pyg_ctx* c, const int32_t* d_placed_off, const in
 int pyg_shard_apply_lists_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t world, int32_t me) {
   PYG_ON_DEVICE(c);
   if (!c || world < 1) return PYG_EINVAL;
-  k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, 0, world, 1);
+  k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, 0, world, 1, nullptr);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -528,7 +558,21 @@ int pyg_shard_apply_lists_range_dev(pyg_ctx* c, const pyg_peer* d_peers, int32_t
   PYG_ON_DEVICE(c);
   if (!c || world < 1 || l3_lo < 0 || l3_hi > world) return PYG_EINVAL;
   if (l3_lo >= l3_hi && !with_l2) return PYG_OK;
-  k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, l3_lo, l3_hi, with_l2);
+  k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, l3_lo, l3_hi, with_l2,
+                                            nullptr);
+  PYG_LAUNCHED(c);
+  return PYG_OK;
+}
+
+int pyg_shard_l3_prepare_dev(pyg_ctx* c, const pyg_peer* d_peers, const int64_t* d_flags,
+                             int32_t world, int32_t me, int64_t seq) {
+  PYG_ON_DEVICE(c);
+  if (!c || world < 1 || me < 0 || me >= world) return PYG_EINVAL;
+  if (me == 0) return PYG_OK;
+  const unsigned long long* cond = c->hd.stats + 7;  // k_admit: an admission matched in L3
+  k_wait<<<1, 32 * ((me + 31) / 32), 0, c->stream>>>(d_flags, me, seq, c->hd.error, cond);
+  PYG_LAUNCHED(c);
+  k_apply_lists<<<148, 256, 0, c->stream>>>(c->hd, d_peers, world, me, 0, me, 0, cond);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

@@ -85,10 +85,10 @@ class SteadyShardStep(ShardedStep):
                                          plan.R_local, mc, self.s16, _ptr(self.rows_buf[par])))
             check(lib.pyg_shard_signal_dev(ctx.h, _ptr(self.flag_of[0]), W, plan.rank, self.seq))
             check(lib.pyg_shard_wait_dev(ctx.h, _ptr(self.flags), W, self.seq))
-            check(lib.pyg_shard_unpack_peer_dev(ctx.h, _ptr(self.rows_of[par]), W,
-                                                _ptr(self.req_off_d), plan.R_total, mc, self.s16,
-                                                _ptr(self.g_res), _ptr(self.g_group),
-                                                _ptr(self.g_staged)))
+            check(lib.pyg_shard_unpack_peer_own_dev(ctx.h, _ptr(self.rows_of[par]), W,
+                                                    _ptr(self.req_off_d), plan.R_total, mc,
+                                                    self.s16, self.own_mask, _ptr(self.g_res),
+                                                    _ptr(self.g_group), _ptr(self.g_staged)))
         else:
             from .shard import allgather_var
             check(lib.pyg_shard_pack_dev(ctx.h, _ptr(b.res), _ptr(b.group), _ptr(self.staged),
@@ -137,10 +137,11 @@ class SteadyShardStep(ShardedStep):
                                                _ptr(self.adm), _ptr(self.m3), _ptr(self.l3_list),
                                                self.cap_hash, self.cap_hash, _ptr(self.counts)))
         if self.p2p:
-            if me > 0:
-                check(lib.pyg_shard_wait_dev(ctx.h, _ptr(self.flags[W:]), me, self.seq))
-                check(lib.pyg_shard_apply_lists_range_dev(ctx.h, _ptr(self.peers), W, me, 0, me,
-                                                          0))
+            # the lower ranks' L3 lists matter only if an admission here matched in L3: the
+            # wait + apply run on the device only then (a rank without L3 matches publishes
+            # its empty list at once, so the chain serializes only the ranks that need it)
+            check(lib.pyg_shard_l3_prepare_dev(ctx.h, _ptr(self.peers), _ptr(self.flags[W:]), W,
+                                               me, self.seq))
             resolve()
             check(lib.pyg_shard_signal_dev(ctx.h, _ptr(self.flag_of[1]), W, me, self.seq))
             check(lib.pyg_shard_wait_dev(ctx.h, _ptr(self.flags[W:]), W, self.seq))
@@ -153,7 +154,8 @@ class SteadyShardStep(ShardedStep):
                     resolve()
                 barrier_on_stream(self.dev)
         mark("l3_chain")
-        check(lib.pyg_shard_apply_lists_range_dev(ctx.h, _ptr(self.peers), W, me, me, W, 1))
+        # every rank's L3 erasures (re-applying the lower ranks' is a no-op) + the L2 clears
+        check(lib.pyg_shard_apply_lists_range_dev(ctx.h, _ptr(self.peers), W, me, 0, W, 1))
         mark("lists")
 
     def release_hold(self, hold_all, h):
@@ -202,6 +204,12 @@ class ShardedSteady:
         self.bursts = bursts
         self.steps = [SteadyShardStep(ctx, self.plan, b.b, self.nodes, device, kv_loc, tt)
                       for b in bursts]
+        own_mask = 0
+        if max(self.own, default=0) < 64:
+            for g in self.own:
+                own_mask |= 1 << g
+        for st in self.steps:
+            st.own_mask = own_mask if own_mask else 0
         # per burst: hold of every global request, and the registry pairs of the whole burst
         self.hold_all, self.reg = [], []
         for k, b in enumerate(bursts):
