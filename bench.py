@@ -80,6 +80,10 @@ def parse():
     ap.add_argument("--split-min", type=int, default=-1,
                     help="K1: prompts of >= this many tokens are split tasks (0 = never, "
                          "-1 = from the batch's token count)")
+    ap.add_argument("--k1-after", default="staged", choices=["start", "staged"],
+                    help="K1 of burst k+1 starts with step k (start) or once step k's K2 is "
+                         "done (staged: K2 runs alone, K1 overlaps the latency-bound K3 / "
+                         "admission)")
     ap.add_argument("--free-sms", type=int, default=8,
                     help="K1 of step k+1 overlaps step k on a second stream, its grid capped at "
                          "(SMs - free_sms); -1 = no overlap (serial step)")
@@ -360,11 +364,16 @@ class Arm:
     def run(self, k0, n, evs=None, hevs=None):
         """steps k0 .. k0+n-1; K1 of the first burst inside this call."""
         self.hash_into(k0, hevs[0] if hevs else None)
+        after_staged = self.args.k1_after == "staged"
         for i in range(n):
             k = k0 + i
             self.S_stream.wait_event(self.ev_h.pop(k))
+            nxt = None
             if i + 1 < n:
-                self.hash_into(k + 1, hevs[i + 1] if hevs else None)
+                nxt = (lambda kk=k + 1, ii=i + 1: self.hash_into(kk, hevs[ii] if hevs else None))
+                if not after_staged:
+                    nxt()
+                    nxt = None
             e = evs[i] if evs else None
             if e:
                 e[0].record(self.S_stream)
@@ -372,7 +381,7 @@ class Arm:
             self.st.complete(self.bursts, k)
             self.st.compose_nodes(self.bursts[k - 1] if k >= 1 else None, k)
             self.st.registry(self.bursts[k])
-            self.st.route_admit(self.bursts[k], k, 1.0 + k, e[1:] if e else None)
+            self.st.route_admit(self.bursts[k], k, 1.0 + k, e[1:] if e else None, nxt)
 
 
 def run_ours(args):
@@ -471,7 +480,8 @@ def run_ours(args):
                         "larger than the 126 MB L2" % (arm.bursts[-1].b.n_tokens * 8 / 1e9),
             "parallelism": "one GPU holds every replica",
             "k1_overlap": (f"K1 of burst k+1 on a second stream (grid = SMs - {args.free_sms}) "
-                           "during step k; each step's own K1 is inside the timed region")
+                           f"from step k's {'K2 end' if args.k1_after == 'staged' else 'start'}; "
+                           "each step's own K1 is inside the timed region")
             if arm.overlap else "none (serial)"},
         "roofline": {"bound": "hbm", "kernel": "k_hash_staged (K1, chain_boundary_hashes)",
                      "achieved": hash_gbs, "peak": peak, "unit": "GB/s", "frac": hash_gbs / peak,
@@ -721,9 +731,13 @@ def run_sharded(args):
         for i in range(n):
             k = k0 + i
             Sst.wait_event(ev_h.pop(k))
+            nxt = None
             if i + 1 < n:
-                hash_into(k + 1, hevs[i + 1] if hevs else None)
-            sh.step(k, 1.0 + k, ev=pevs[i] if pevs is not None else None)
+                nxt = (lambda kk=k + 1, ii=i + 1: hash_into(kk, hevs[ii] if hevs else None))
+                if args.k1_after != "staged":
+                    nxt()
+                    nxt = None
+            sh.step(k, 1.0 + k, ev=pevs[i] if pevs is not None else None, after_staged=nxt)
 
     run(0, W_)
     torch.cuda.synchronize(dev)

@@ -186,13 +186,16 @@ class Steady:
         check(_lib._lib.pyg_registry_update_batch_dev(self.ctx.h, burst.n_reg, _ptr(burst.reg_wf),
                                                       _ptr(burst.reg_mask), burst.max_wf))
 
-    def route_admit(self, burst: Burst, k, now, events=None):
+    def route_admit(self, burst: Burst, k, now, events=None, after_staged=None):
         """K2 -> K3 -> K4/K5 of burst k (its hashes are ready).  events: optional list of 4
-        CUDA events recorded before K2, K3, admission and after it."""
+        CUDA events recorded before K2, K3, admission and after it; after_staged() is called
+        once K2 is enqueued (the bench starts the next burst's K1 there)."""
         o = self.out(k)
         rec = (lambda i: events[i].record()) if events else (lambda i: None)
         rec(0)
         PB.staged_matrix(self.ctx, burst.b, self.nodes, o)
+        if after_staged is not None:
+            after_staged()
         rec(1)
         PB.route_batch(self.ctx, burst.b, self.nodes, o, PB.SEQ_COMMIT)
         rec(2)

@@ -59,7 +59,7 @@ class SteadyShardStep(ShardedStep):
     flags).  route_nodes: this rank's node table (global replica ids, own models'
     candidates only)."""
 
-    def step_steady(self, now, route_nodes, after_gather=None, ev=None):
+    def step_steady(self, now, route_nodes, after_gather=None, ev=None, after_staged=None):
         """ev: optional dict name -> CUDA event, recorded at the phase ends (experiments)."""
         ctx, plan, b, nodes = self.ctx, self.plan, self.b, self.nodes
         lib = _lib._lib
@@ -76,6 +76,8 @@ class SteadyShardStep(ShardedStep):
                                         _ptr(b.hashes), plan.R_local, _ptr(b.group),
                                         nodes.n_groups, _ptr(nodes.cand_off), _ptr(nodes.cand),
                                         nodes.max_cand, _ptr(self.staged)))
+        if after_staged is not None:
+            after_staged()
         mark("staged")
         mc = max(nodes.max_cand, 1)
         self.seq += 1
@@ -241,7 +243,7 @@ class ShardedSteady:
             _ptr(pl), _ptr(req), _ptr(hold), 2, _ptr(self.route_nodes.asg_off),
             _ptr(self.route_nodes.asg)))
 
-    def step(self, k, now, after_gather=None, ev=None):
+    def step(self, k, now, after_gather=None, ev=None, after_staged=None):
         """Everything of step k after K1 of this rank's burst k."""
         PB.bind_current_stream(self.ctx)
         if ev is not None:
@@ -254,5 +256,5 @@ class ShardedSteady:
         self.compose_nodes(k)
         rw, rm, nr, mx = self.reg[k]
         check(_lib._lib.pyg_registry_update_batch_dev(self.ctx.h, nr, _ptr(rw), _ptr(rm), mx))
-        self.steps[k].step_steady(now, self.route_nodes, after_gather, ev)
+        self.steps[k].step_steady(now, self.route_nodes, after_gather, ev, after_staged)
         return self.steps[k]

@@ -1,6 +1,10 @@
-# overlap variants: where K1 of step k+1 starts, and the free-SM count
+#!/bin/bash
+set -x
 python paper_2604_25899_b200/build.py > gpurun_out/build.log 2>&1
-for a in staged start; do for f in 0 8 16; do
-  timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --k1-after $a --free-sms $f > gpurun_out/ka_${a}_$f.json 2>/dev/null
-  python -c "import json;d=json.load(open('gpurun_out/ka_${a}_$f.json'));print('$a', $f, round(d['value']/1e6,1), round(d['ms_per_step'],3), {k:round(v,3) for k,v in d['phase_ms'].items()})"
-done; done
+NG=$(nvidia-smi -L | wc -l)
+for ka in staged start; do
+for n in 1 $NG; do
+  timeout 900 python bench.py --gpus $n --no-cpu-baseline --no-e2e --k1-after $ka > gpurun_out/ka_${ka}_n$n.out 2> gpurun_out/ka_${ka}_n$n.err
+  python -c "import json;d=json.loads(open('gpurun_out/ka_${ka}_n$n.out').read().strip().splitlines()[-1]);print('$ka', $n, d['value']/1e6, d['ms_per_step'], d.get('phase_ms') or d.get('phase_ms_rank0'))"
+done
+done
