@@ -311,10 +311,17 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   const int n_split = (!kGather && n_split_p) ? *n_split_p : 0;
   const int ntasks = n_split + (R - n_split + 31) / 32;
   // persistent: each warp pulls tasks, longest first, until none are left
-  for (;;) {
+  // persistent (next_task != null): warps pull tasks from a counter until none are left;
+  // otherwise one task per warp (a CTA per 8 tasks, in the longest-first order), so CTAs
+  // retire continually and a higher-priority stream's kernels get SMs between them
+  for (int it = 0;; ++it) {
   int task = 0;
-  if (lane == 0) task = atomicAdd(next_task, 1);
-  task = __shfl_sync(kFull, task, 0);
+  if (next_task) {
+    if (lane == 0) task = atomicAdd(next_task, 1);
+    task = __shfl_sync(kFull, task, 0);
+  } else {
+    task = it == 0 ? static_cast<int>(blockIdx.x) * kWarps + warp : ntasks;
+  }
   if (task >= ntasks) break;
   if (task < n_split) {
     const int r = order[task];
@@ -689,9 +696,13 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   const int n_sm = pyg_host::sm_count(c->device);
   const int cap = c->hash_ctas > 0 ? std::min(c->hash_ctas, n_sm) : n_sm;
   const int tasks_max = (R + 31) / 32 + (split_min0 ? R : 0);
-  const int grid = std::max(1, std::min((tasks_max + kWarps - 1) / kWarps, cap));  // 1 CTA/SM
+  const bool persistent = c->hash_persistent != 0;
+  const int grid = persistent
+                       ? std::max(1, std::min((tasks_max + kWarps - 1) / kWarps, cap))  // 1/SM
+                       : std::max(1, (tasks_max + kWarps - 1) / kWarps);
   k_hash_staged<kGather><<<grid, per_block, kSmemBytes, c->stream>>>(
-      d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, ctr0, g, ctr0 + 1);
+      d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, persistent ? ctr0 : nullptr, g,
+      ctr0 + 1);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -739,6 +750,13 @@ int pyg_set_hash_split(pyg_ctx* c, int64_t min_tokens) {
   PYG_ON_DEVICE(c);
   if (!c || min_tokens < -1) return PYG_EINVAL;
   c->split_min = min_tokens < 0 ? -1 : (min_tokens + 3) & ~int64_t{3};
+  return PYG_OK;
+}
+
+int pyg_set_hash_persistent(pyg_ctx* c, int32_t persistent) {
+  PYG_ON_DEVICE(c);
+  if (!c) return PYG_EINVAL;
+  c->hash_persistent = persistent ? 1 : 0;
   return PYG_OK;
 }
 
