@@ -84,7 +84,7 @@ def parse():
                     help="K1 of burst k+1 starts with step k (start) or once step k's K2 is "
                          "done (staged: K2 runs alone, K1 overlaps the latency-bound K3 / "
                          "admission)")
-    ap.add_argument("--k1-grid", default="persistent", choices=["persistent", "tasks"],
+    ap.add_argument("--k1-grid", default="persistent", choices=["persistent", "tasks", "tasks1"],
                     help="K1 grid: persistent CTAs, or one task per warp (CTAs retire so the "
                          "step's kernels interleave)")
     ap.add_argument("--free-sms", type=int, default=8,
@@ -345,7 +345,7 @@ class Arm:
             n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
             self.hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
         self.hctx.set_hash_split(args.split_min)
-        self.hctx.set_hash_persistent(args.k1_grid == "persistent")
+        self.hctx.set_hash_grid(args.k1_grid)
         self.ev_h = {}
         torch.cuda.synchronize(dev)
         self.ctx.check_device_error()
@@ -717,7 +717,7 @@ def run_sharded(args):
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
     hctx.set_hash_split(args.split_min)
-    hctx.set_hash_persistent(args.k1_grid == "persistent")
+    hctx.set_hash_grid(args.k1_grid)
     ev_h = {}
 
     def hash_into(k, hev=None):

@@ -210,9 +210,11 @@ int pyg_hash_batch_dev(pyg_ctx* ctx, const uint64_t* d_tokens, const int64_t* d_
    whose K1 overlaps another ctx's step on a second stream leaves SMs free for the step's
    latency-bound kernels (route, admission) this way. */
 int pyg_set_hash_ctas(pyg_ctx* ctx, int32_t n_ctas);
-/* K1 grid: persistent (1, default: one CTA per SM pulling tasks) or one task per warp (0:
-   CTAs retire as their 8 tasks finish, so kernels of a higher-priority stream interleave). */
-int pyg_set_hash_persistent(pyg_ctx* ctx, int32_t persistent);
+/* K1 grid: 1 (default) persistent, one CTA per SM pulling tasks; 0 one task per warp (CTAs
+   retire as their 8 tasks finish, so kernels of a higher-priority stream interleave); 2 as 0
+   with at most one K1 CTA per SM (shared memory padded), the rest of each SM left to the
+   step's kernels. */
+int pyg_set_hash_grid(pyg_ctx* ctx, int32_t mode);
 /* K1 hashes prompts of >= min_tokens tokens as split tasks: one warp per prompt, 512 tokens
    at a time, through the low-byte decomposition of FNV-1a (k_hash.cu) -- the same hashes,
    without the long-prompt tail of one lane per request.  0 = never; -1 (default) = a

@@ -137,7 +137,7 @@ _sig("pyg_shard_local_placed_dev", vp, vp, vp, vp, vp, vp, vp)
 _sig("pyg_stats", vp, vp, i32)
 _sig("pyg_lookup_all", vp, vp, i64, i32, i32, vp)
 _sig("pyg_set_hash_split", vp, i64)
-_sig("pyg_set_hash_persistent", vp, i32)
+_sig("pyg_set_hash_grid", vp, i32)
 _sig("pyg_nodes_compose_dev", vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp)
 _sig("pyg_release_hold_dev", vp, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp)
 _sig("pyg_registry_update_batch_dev", vp, i32, vp, vp, i32)
@@ -237,8 +237,10 @@ class Context:
     def registry_reserve(self, max_wf: int):
         check(_lib.pyg_registry_reserve(self.h, int(max_wf)))
 
-    def set_hash_persistent(self, persistent: bool):
-        check(_lib.pyg_set_hash_persistent(self.h, int(bool(persistent))))
+    def set_hash_grid(self, mode: str):
+        """K1 grid: "persistent" (default), "tasks" (one task per warp), "tasks1" (one task
+        per warp, at most one K1 CTA per SM)."""
+        check(_lib.pyg_set_hash_grid(self.h, {"tasks": 0, "persistent": 1, "tasks1": 2}[mode]))
 
     def set_hash_split(self, min_tokens: int):
         check(_lib.pyg_set_hash_split(self.h, int(min_tokens)))

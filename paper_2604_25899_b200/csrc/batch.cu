@@ -130,7 +130,31 @@ struct AdmitArgs {
   DirRecord* l2_out;
   int64_t l2_cap;
   unsigned long long* l2_count;
+  // replicas are taken from a queue, most placements first (k_admit_order)
+  const int32_t* rep_order;
+  int32_t* rep_next;
+  int32_t n_rep;
 };
+
+// Queue order of k_admit: replicas by descending placement count (a counting sort on one
+// CTA), so the CTAs of a grid smaller than the replica count -- or sharing the SMs with K1
+// of the next burst -- pull the longest admission sequences first and finish together.
+__global__ void __launch_bounds__(1024) k_admit_order(const int32_t* placed_off, int32_t n_rep,
+                                                      int32_t* order, int32_t* next) {
+  __shared__ int32_t hist[1024];
+  __shared__ int64_t sm[33];
+  hist[threadIdx.x] = 0;
+  __syncthreads();
+  auto bucket = [&](int r) { return 1023 - min(placed_off[r + 1] - placed_off[r], 1023); };
+  for (int r = threadIdx.x; r < n_rep; r += blockDim.x) atomicAdd(&hist[bucket(r)], 1);
+  __syncthreads();
+  int64_t tot;
+  const int64_t pre = block_exscan(hist[threadIdx.x], sm, &tot);
+  hist[threadIdx.x] = static_cast<int32_t>(pre);
+  __syncthreads();
+  for (int r = threadIdx.x; r < n_rep; r += blockDim.x) order[atomicAdd(&hist[bucket(r)], 1)] = r;
+  if (threadIdx.x == 0) *next = 0;
+}
 
 struct ChainGetB {
   const uint64_t* hashes;
@@ -164,9 +188,17 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
   __shared__ int64_t bc[4];
   __shared__ uint32_t sdup[1024];
   __shared__ EvCache ec;
-  const int rep = blockIdx.x;
-  if (threadIdx.x == 0) ec.valid = 0;
+  __shared__ int32_t s_rep;
+  for (;;) {
+  if (threadIdx.x == 0) {
+    const int32_t q = atomicAdd(a.rep_next, 1);
+    s_rep = q < a.n_rep ? a.rep_order[q] : -1;
+    ec.valid = 0;
+  }
   __syncthreads();
+  const int rep = s_rep;
+  __syncthreads();  // s_rep is rewritten by the next iteration only after every thread read it
+  if (rep < 0) break;
   TierDev* t1p = c.tiers + 2 * rep;
   TierDev* t2p = c.tiers + 2 * rep + 1;
   const TierDev& t3 = c.tiers[2 * c.n_rep];
@@ -285,6 +317,7 @@ __global__ void __launch_bounds__(512, 2) k_admit(CtxDev c, AdmitArgs a) {
     }
     __syncthreads();
   }
+  }  // replica queue
 }
 
 // ------------------------------------------------ ordered L3 (engine order)
@@ -680,9 +713,12 @@ int pyg_lookup_batch_dev(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_
 }
 
 // scratch layout of one admission call: L3Rec[R] | ctl[32] (kept until the L3 stage ran)
+// [R] L3 records | 256 B of control words (ctl[60] = k_admit's replica queue head) |
+// [n_rep] replica queue order
 static int admit_scratch(pyg_ctx* c, int32_t R, L3Rec** rec, int32_t** ctl) {
   void* sp;
-  int rc = scratch(c, static_cast<size_t>(R) * sizeof(L3Rec) + 256, &sp);
+  int rc = scratch(c, static_cast<size_t>(R) * sizeof(L3Rec) + 256 +
+                          static_cast<size_t>(c->n_rep) * 4, &sp);
   if (rc) return rc;
   *rec = static_cast<L3Rec*>(sp);
   *ctl = reinterpret_cast<int32_t*>(static_cast<char*>(sp) + static_cast<size_t>(R) * sizeof(L3Rec));
@@ -708,12 +744,18 @@ static int admit_core(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok
   PYG_CUDA(cudaMemsetAsync(d_match3, 0, static_cast<size_t>(R) * 24, c->stream));
   PYG_CUDA(cudaMemsetAsync(c->hd.stats + 7, 0, 8, c->stream));  // "some admission hit L3"
   auto* cnt = reinterpret_cast<unsigned long long*>(d_counts);
+  int32_t* order = ctl + 64;
+  int32_t* next = ctl + 60;
+  k_admit_order<<<1, 1024, 0, c->stream>>>(d_placed_off, c->n_rep, order, next);
+  PYG_LAUNCHED(c);
   AdmitArgs a{d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, d_placed_off, d_placed,
               now, speculative, d_admitted, d_match3, rec,
-              static_cast<DirRecord*>(l2_out), l2_cap, cnt};
+              static_cast<DirRecord*>(l2_out), l2_cap, cnt, order, next, c->n_rep};
   const size_t smem = kSmemSortCap * 12;
   PYG_CUDA(cudaFuncSetAttribute(k_admit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_admit<<<c->n_rep, 512, smem, c->stream>>>(c->hd, a);
+  // two CTAs per SM when the SMs are free; each pulls replicas until the queue is empty
+  const int grid = std::min(c->n_rep, 2 * pyg_host::sm_count(c->device));
+  k_admit<<<grid, 512, smem, c->stream>>>(c->hd, a);
   c->dir_admits += 1;
   PYG_LAUNCHED(c);
   return PYG_OK;

@@ -43,7 +43,7 @@ struct pyg_ctx {
   int32_t rep_base = 0;      // global index of this ctx's replica 0
   int64_t dir_admits = 0;    // admission calls since the last build (cleared bits accumulate)
   int32_t hash_ctas = 0;     // K1 persistent grid cap (0 = one CTA per SM)
-  int32_t hash_persistent = 1;  // K1: persistent grid (1) or one task per warp (0)
+  int32_t hash_grid = 1;  // K1 grid: 0 one task per warp, 1 persistent, 2 = 0 at 1 CTA/SM
   int64_t split_min = -1;    // K1: prompts of >= split_min tokens are split tasks (0 = never,
                              // -1 = a threshold from the batch's token count, k_split_count)
   void* d_aux = nullptr;     // second on-demand buffer (fused assembly's chunk sources)

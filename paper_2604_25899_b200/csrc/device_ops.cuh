@@ -671,6 +671,81 @@ __device__ __forceinline__ int64_t warp_incl_scan(int64_t v) {
 __device__ __forceinline__ bool evict_candidate(const Block& b) {
   return (b.flags & kAlive) && b.pin <= 0;
 }
+// (pin, flags) of a record in one 8-byte load
+__device__ __forceinline__ bool evict_candidate_pf(const Block* b) {
+  const int2 pf = *reinterpret_cast<const int2*>(&b->pin);
+  return (pf.y & kAlive) && pf.x <= 0;
+}
+
+// Eviction candidates of one warp's log range, in log order.  The scans are bound by the
+// latency of HBM / L2 reads of the 64-byte records, so each lane keeps kScanU records in
+// flight: first the (pin, flags) word of all of them, then the key fields of the candidates.
+constexpr int kScanU = 4;
+constexpr int kGatherU = 2;
+__device__ __forceinline__ int64_t warp_count_candidates(const TierDev& t, int64_t lo,
+                                                         int64_t hi) {
+  const int lane = threadIdx.x & 31;
+  int64_t wc = 0;
+  for (int64_t base = lo; base < hi; base += 32 * kScanU) {
+    bool cand[kScanU];
+#pragma unroll
+    for (int u = 0; u < kScanU; ++u) {
+      const int64_t i = base + 32 * u + lane;
+      cand[u] = i < hi ? evict_candidate_pf(t.log + i) : false;
+    }
+#pragma unroll
+    for (int u = 0; u < kScanU; ++u) wc += __popc(__ballot_sync(kFull, cand[u]));
+  }
+  return wc;
+}
+// Writes the sort keys of the candidates in [lo, hi) from position wpos on:
+// khi = order(last_access), klo = live << 31 | size << 24 | log index.
+__device__ __forceinline__ void warp_gather_candidates(const CtxDev& c, const TierDev& t,
+                                                       int64_t lo, int64_t hi, int64_t wpos,
+                                                       int speculative, uint64_t* khi,
+                                                       uint32_t* klo) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = lo; base < hi; base += 32 * kGatherU) {
+    bool cand[kGatherU];
+#pragma unroll
+    for (int u = 0; u < kGatherU; ++u) {
+      const int64_t i = base + 32 * u + lane;
+      cand[u] = i < hi ? evict_candidate_pf(t.log + i) : false;
+    }
+    double la[kGatherU];
+    int32_t wf[kGatherU], role[kGatherU], sz[kGatherU];
+#pragma unroll
+    for (int u = 0; u < kGatherU; ++u) {
+      la[u] = 0.0;
+      wf[u] = role[u] = sz[u] = 0;
+      if (cand[u]) {
+        const Block& b = t.log[base + 32 * u + lane];
+        la[u] = b.la;
+        wf[u] = b.wf;
+        role[u] = b.role;
+        sz[u] = static_cast<int32_t>(b.e - b.s);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGatherU; ++u) {
+      bool dead = false;
+      if (cand[u] && speculative) {
+        const bool live = wf[u] >= 0 && wf[u] < c.reg_cap && c.reg_present[wf[u]] &&
+                          role[u] >= 0 && role[u] < 64 &&
+                          ((c.reg_mask[wf[u]] >> role[u]) & 1ULL);
+        dead = !live;  // FutureRegistry::lineage_live (manager.cpp:19-23)
+      }
+      const unsigned m = __ballot_sync(kFull, cand[u]);
+      if (cand[u]) {
+        const int64_t pos = wpos + __popc(m & lanemask_lt());
+        khi[pos] = order_double(la[u]);
+        klo[pos] = (dead ? 0u : 0x80000000u) | (static_cast<uint32_t>(sz[u]) << 24) |
+                   static_cast<uint32_t>(base + 32 * u + lane);
+      }
+      wpos += __popc(m);
+    }
+  }
+}
 
 __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t excess, int speculative,
                                 uint64_t* out_ids, int64_t cap, unsigned char* smem_keys,
@@ -683,12 +758,7 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
   const int lane = threadIdx.x & 31;
   // candidates per warp range of the log
   const WarpSeg ls = warp_seg(n);
-  int64_t wc = 0;
-  for (int64_t base = ls.lo; base < ls.hi; base += 32) {
-    const int64_t i = base + lane;
-    const bool cand = i < ls.hi && evict_candidate(t.log[i]);
-    wc += __popc(__ballot_sync(kFull, cand));
-  }
+  const int64_t wc = warp_count_candidates(t, ls.lo, ls.hi);
   int64_t ncand;
   const int64_t wbase = warp_seg_prefix(wc, swp, &ncand);
   int64_t opos = 0, rem = excess, ftok = 0;
@@ -698,36 +768,7 @@ __device__ inline EvictOut block_evict(const CtxDev& c, TierDev* tp, int64_t exc
     uint64_t* khi = reinterpret_cast<uint64_t*>(smem_keys);
     uint32_t* klo = reinterpret_cast<uint32_t*>(smem_keys + kSmemSortCap * 8);
     // gather in log (= id) order: key = order(last_access) | class, size, log index
-    int64_t wpos = wbase;
-    for (int64_t base = ls.lo; base < ls.hi; base += 32) {
-      const int64_t i = base + lane;
-      bool cand = false;
-      uint64_t h = 0;
-      uint32_t l = 0;
-      if (i < ls.hi) {
-        const Block& b = t.log[i];
-        cand = evict_candidate(b);
-        if (cand) {
-          bool dead = false;
-          if (speculative) {
-            const bool live = b.wf >= 0 && b.wf < c.reg_cap && c.reg_present[b.wf] &&
-                              b.role >= 0 && b.role < 64 &&
-                              ((c.reg_mask[b.wf] >> b.role) & 1ULL);
-            dead = !live;  // FutureRegistry::lineage_live (manager.cpp:19-23)
-          }
-          h = order_double(b.la);
-          l = (dead ? 0u : 0x80000000u) | (static_cast<uint32_t>(b.e - b.s) << 24) |
-              static_cast<uint32_t>(i);
-        }
-      }
-      const unsigned m = __ballot_sync(kFull, cand);
-      if (cand) {
-        const int64_t pos = wpos + __popc(m & lanemask_lt());
-        khi[pos] = h;
-        klo[pos] = l;
-      }
-      wpos += __popc(m);
-    }
+    warp_gather_candidates(c, t, ls.lo, ls.hi, wbase, speculative, khi, klo);
     __syncthreads();
     const WarpSeg cs = warp_seg(ncand);
     uint32_t pc = 0;   // groups <= (pc, ph) are taken (none while `first`)
@@ -890,11 +931,7 @@ __device__ inline EvictOut block_evict_admit(const CtxDev& c, TierDev* tp, int64
   if (!ec->valid) {
     const int64_t n = t.log_len;
     const WarpSeg ls = warp_seg(n);
-    int64_t wc = 0;
-    for (int64_t base = ls.lo; base < ls.hi; base += 32) {
-      const int64_t i = base + lane;
-      wc += __popc(__ballot_sync(kFull, i < ls.hi && evict_candidate(t.log[i])));
-    }
+    const int64_t wc = warp_count_candidates(t, ls.lo, ls.hi);
     int64_t ncand;
     const int64_t wbase = warp_seg_prefix(wc, swp, &ncand);
     if (n >= (1 << 24) || c.B >= 127) {
@@ -906,36 +943,7 @@ __device__ inline EvictOut block_evict_admit(const CtxDev& c, TierDev* tp, int64
     uint32_t* klo = ncand <= kSmemSortCap
                         ? reinterpret_cast<uint32_t*>(smem_keys + kSmemSortCap * 8)
                         : reinterpret_cast<uint32_t*>(t.scratch + 2 * t.log_cap);
-    int64_t wpos = wbase;
-    for (int64_t base = ls.lo; base < ls.hi; base += 32) {
-      const int64_t i = base + lane;
-      bool cand = false;
-      uint64_t h = 0;
-      uint32_t l = 0;
-      if (i < ls.hi) {
-        const Block& b = t.log[i];
-        cand = evict_candidate(b);
-        if (cand) {
-          bool dead = false;
-          if (speculative) {
-            const bool live = b.wf >= 0 && b.wf < c.reg_cap && c.reg_present[b.wf] &&
-                              b.role >= 0 && b.role < 64 &&
-                              ((c.reg_mask[b.wf] >> b.role) & 1ULL);
-            dead = !live;  // FutureRegistry::lineage_live (manager.cpp:19-23)
-          }
-          h = order_double(b.la);
-          l = (dead ? 0u : 0x80000000u) | (static_cast<uint32_t>(b.e - b.s) << 24) |
-              static_cast<uint32_t>(i);
-        }
-      }
-      const unsigned m = __ballot_sync(kFull, cand);
-      if (cand) {
-        const int64_t pos = wpos + __popc(m & lanemask_lt());
-        khi[pos] = h;
-        klo[pos] = l;
-      }
-      wpos += __popc(m);
-    }
+    warp_gather_candidates(c, t, ls.lo, ls.hi, wbase, speculative, khi, klo);
     if (threadIdx.x == 0) {
       ec->ncand = ncand;
       ec->valid = 1;

@@ -27,6 +27,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ctx.cuh"
 #include "device_ops.cuh"
@@ -45,7 +46,9 @@ constexpr int kWarps = 8;                       // warps per CTA
 // request l sit at position perm(l) = (l & 1) * 16 + (l >> 1), so the 16 requests a
 // half-warp loads (l = 2t + sub) are 128 contiguous bytes: 8 broadcast LDS.128.
 constexpr int kMetaBytes = 5 * 32 * 8;
-constexpr int kSmemBytes = kWarps * (2 * kStageBytes + kMetaBytes);
+constexpr int smem_bytes(int w) { return w * (2 * kStageBytes + kMetaBytes); }
+// more than half of the SM's 228 KB: one K1 CTA per SM (grid mode 2)
+constexpr int kSmemOneCta = 116 * 1024;
 // packed chunk source: pointer | (valid tokens in the chunk, 0..16) << 59
 constexpr int kVShift = 59;
 constexpr unsigned long long kPtrMask = (1ull << kVShift) - 1;
@@ -293,8 +296,8 @@ __device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_
 //
 // Long prompts (>= the split threshold) are split tasks (split_task above); the rest run
 // one lane per request in 32-request tasks.
-template <bool kGather>
-__global__ void __launch_bounds__(kWarps * 32, 2)
+template <bool kGather, int W>
+__global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1))
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
               uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task, GatherSrc g,
@@ -304,7 +307,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   unsigned char* wbuf = smem + warp * 2 * kStageBytes;
   // fused assembly: wbase[32] destination bases, lsl[4][32] packed chunk sources
   unsigned long long* wbase = reinterpret_cast<unsigned long long*>(
-      smem + kWarps * 2 * kStageBytes + warp * kMetaBytes);
+      smem + W * 2 * kStageBytes + warp * kMetaBytes);
   unsigned long long* lsl = wbase + 32;
   // tasks: [0, n_split) one long request each (split_task, the longest first), then
   // 32-request tasks over the rest of the length-sorted order
@@ -320,7 +323,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
     if (lane == 0) task = atomicAdd(next_task, 1);
     task = __shfl_sync(kFull, task, 0);
   } else {
-    task = it == 0 ? static_cast<int>(blockIdx.x) * kWarps + warp : ntasks;
+    task = it == 0 ? static_cast<int>(blockIdx.x) * W + warp : ntasks;
   }
   if (task >= ntasks) break;
   if (task < n_split) {
@@ -482,16 +485,16 @@ __global__ void __launch_bounds__(32) k_hash_seq(const uint64_t* __restrict__ to
   }
 }
 
-// Length histogram of the adaptive split threshold: 4 bins per octave from 512 tokens
+// Length histogram of the adaptive split threshold: 8 bins per octave from 512 tokens
 // (bin 0 = shorter), tokens and request counts per bin.
-constexpr int kHistBins = 40;
+constexpr int kHistBins = 80;
 __device__ __forceinline__ int len_bin(int64_t n) {
   if (n < 512) return 0;
-  const double b = 4.0 * log2(static_cast<double>(n) / 512.0);
+  const double b = 8.0 * log2(static_cast<double>(n) / 512.0);
   const int k = 1 + static_cast<int>(b);
   return k < kHistBins ? k : kHistBins - 1;
 }
-__device__ __forceinline__ double bin_lo(int k) { return k == 0 ? 0.0 : 512.0 * exp2((k - 1) / 4.0); }
+__device__ __forceinline__ double bin_lo(int k) { return k == 0 ? 0.0 : 512.0 * exp2((k - 1) / 8.0); }
 
 struct SplitHist {
   unsigned long long tok[kHistBins];
@@ -501,10 +504,12 @@ struct SplitHist {
 
 __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val,
                            int64_t split_min, int* n_split, SplitHist* hist) {
-  __shared__ unsigned long long s_tok[kHistBins], s_cnt[kHistBins];
+  __shared__ unsigned long long s_tok[kHistBins], s_cnt[kHistBins], s_max;
   const bool adaptive = split_min < 0;
-  if (adaptive)
+  if (adaptive) {
     for (int k = threadIdx.x; k < kHistBins; k += blockDim.x) s_tok[k] = s_cnt[k] = 0;
+    if (threadIdx.x == 0) s_max = 0;
+  }
   __syncthreads();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = r < R ? tok_off[r + 1] - tok_off[r] : 0;
@@ -521,9 +526,13 @@ __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t
       const int k = len_bin(n);
       atomicAdd(s_tok + k, static_cast<unsigned long long>(n));
       atomicAdd(s_cnt + k, 1ULL);
-      atomicMax(&hist->max_len, static_cast<unsigned long long>(n));
     }
+    // one global atomic per CTA (all requests on one address would serialise in L2)
+    const unsigned long long wmax =
+        __reduce_max_sync(kFull, static_cast<unsigned>(n));  // n < 2^32 tokens
+    if ((threadIdx.x & 31) == 0 && wmax) atomicMax(&s_max, wmax);
     __syncthreads();
+    if (threadIdx.x == 0 && s_max) atomicMax(&hist->max_len, s_max);
     for (int k = threadIdx.x; k < kHistBins; k += blockDim.x)
       if (s_cnt[k]) {
         atomicAdd(hist->tok + k, s_tok[k]);
@@ -540,9 +549,10 @@ __global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t
 __global__ void k_split_count(const uint16_t* sorted_keys, int R, const SplitHist* hist,
                               int* n_split) {
   if (threadIdx.x) return;
-  // measured on B200 (tools/k1_sweep.py): a one-lane chain in a loaded SM ~120 ns per token,
-  // a split task ~8 ns per token, ~250 Gtok/s one lane per request, split tokens ~2.8x
-  const double c_lane = 120e-9, c_split = 8e-9, rate = 250e9, extra = 1.8;
+  // measured on B200 (tools/k1_sweep.py, config-4 burst of 125k requests at thresholds
+  // 4k..16k): a one-lane chain in a loaded SM ~90 ns per token, a split task ~8 ns per
+  // token, ~280 Gtok/s one lane per request, a split token costs 2.8 lane tokens
+  const double c_lane = 90e-9, c_split = 8e-9, rate = 280e9, extra = 1.8;
   double total = 0;
   for (int k = 0; k < kHistBins; ++k) total += static_cast<double>(hist->tok[k]);
   const double lmax = static_cast<double>(hist->max_len);
@@ -619,11 +629,17 @@ cudaError_t device_setup(int dev) {
   if (done[dev]) return cudaSuccess;
   cudaError_t e = cudaSetDevice(dev);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_hash_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kSmemBytes);
+  e = cudaFuncSetAttribute(k_hash_staged<false, kWarps>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOneCta);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_hash_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kSmemBytes);
+  e = cudaFuncSetAttribute(k_hash_staged<true, kWarps>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOneCta);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_hash_staged<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem_bytes(16));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_hash_staged<false, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem_bytes(12));
   if (e != cudaSuccess) return e;
   uint64_t pw[kSplitTok + 1];
   uint64_t q = 1;
@@ -692,17 +708,32 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
     PYG_LAUNCHED(c);
   }
   PYG_CUDA(pyg_host::device_setup(c->device));
-  const int per_block = kWarps * 32;
   const int n_sm = pyg_host::sm_count(c->device);
   const int cap = c->hash_ctas > 0 ? std::min(c->hash_ctas, n_sm) : n_sm;
   const int tasks_max = (R + 31) / 32 + (split_min0 ? R : 0);
-  const bool persistent = c->hash_persistent != 0;
-  const int grid = persistent
-                       ? std::max(1, std::min((tasks_max + kWarps - 1) / kWarps, cap))  // 1/SM
-                       : std::max(1, (tasks_max + kWarps - 1) / kWarps);
-  k_hash_staged<kGather><<<grid, per_block, kSmemBytes, c->stream>>>(
-      d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, persistent ? ctr0 : nullptr, g,
-      ctr0 + 1);
+  const bool persistent = c->hash_grid == 1;
+  // experiment knob: warps per K1 CTA (8, 12, 16) on the CSR path
+  static const int env_w = [] {
+    const char* e = getenv("PYG_K1_WARPS");
+    return e ? atoi(e) : kWarps;
+  }();
+  const int W = kGather ? kWarps : env_w;
+  const int grid = persistent ? std::max(1, std::min((tasks_max + W - 1) / W, cap))  // 1/SM
+                              : std::max(1, (tasks_max + W - 1) / W);
+  // grid mode 2: shared memory padded so that one K1 CTA fits per SM (the rest of the SM
+  // stays free for the step's kernels); the launch sizes are set in device_setup
+  const int pad = c->hash_grid == 2 && W == kWarps ? kSmemOneCta : 0;
+  int* next = persistent ? ctr0 : nullptr;
+  if (W == 16)
+    k_hash_staged<kGather, 16><<<grid, 16 * 32, smem_bytes(16), c->stream>>>(
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1);
+  else if (W == 12)
+    k_hash_staged<kGather, 12><<<grid, 12 * 32, smem_bytes(12), c->stream>>>(
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1);
+  else
+    k_hash_staged<kGather, kWarps><<<grid, kWarps * 32, std::max(pad, smem_bytes(kWarps)),
+                                     c->stream>>>(
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -753,10 +784,10 @@ int pyg_set_hash_split(pyg_ctx* c, int64_t min_tokens) {
   return PYG_OK;
 }
 
-int pyg_set_hash_persistent(pyg_ctx* c, int32_t persistent) {
+int pyg_set_hash_grid(pyg_ctx* c, int32_t mode) {
   PYG_ON_DEVICE(c);
-  if (!c) return PYG_EINVAL;
-  c->hash_persistent = persistent ? 1 : 0;
+  if (!c || mode < 0 || mode > 2) return PYG_EINVAL;
+  c->hash_grid = mode;
   return PYG_OK;
 }
 

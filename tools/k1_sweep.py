@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--sizes", default="1000,16000,125000")
     ap.add_argument("--splits", default="-1,8192,4096,0")
     ap.add_argument("--workload", default="bursty")
+    ap.add_argument("--grids", default="persistent,tasks")
     a = ap.parse_args()
     from paper_2604_25899_b200 import Context
     from paper_2604_25899_b200 import batch as PB
@@ -34,8 +35,9 @@ def main():
         b = S.upload_burst(tr, 16, dev, 3)
         L = np.diff(tr.tok_off)
         nbytes = 8 * int(L.sum()) + 8 * b.b.n_hashes + 16 * (R + 1)
-        for sm in [int(x) for x in a.splits.split(",")]:
+        for sm, grid in [(int(x), gm) for x in a.splits.split(",") for gm in a.grids.split(",")]:
             ctx = Context(0, [], [], 16, device=0)
+            ctx.set_hash_grid(grid)
             ctx.set_stream(ctypes.c_void_p(s.cuda_stream))
             ctx.set_hash_split(sm)
             ts = []
@@ -48,7 +50,7 @@ def main():
                 if i >= 2:
                     ts.append(e0.elapsed_time(e1))
             ms = float(np.median(ts))
-            print(json.dumps({"R": R, "split_min": sm, "ms": ms, "tokens": int(L.sum()),
+            print(json.dumps({"R": R, "split_min": sm, "grid": grid, "ms": ms, "tokens": int(L.sum()),
                               "max_len": int(L.max()), "gbs": nbytes / ms / 1e6}), flush=True)
             ctx.close()
 
