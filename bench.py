@@ -87,6 +87,9 @@ def parse():
     ap.add_argument("--k1-grid", default="persistent", choices=["persistent", "tasks", "tasks1"],
                     help="K1 grid: persistent CTAs, or one task per warp (CTAs retire so the "
                          "step's kernels interleave)")
+    ap.add_argument("--k1-gate", default="off", choices=["on", "off"],
+                    help="K1 of the next burst pauses while the step's admission runs "
+                         "(pyg_set_hash_gate)")
     ap.add_argument("--free-sms", type=int, default=8,
                     help="K1 of step k+1 overlaps step k on a second stream, its grid capped at "
                          "(SMs - free_sms); -1 = no overlap (serial step)")
@@ -346,6 +349,8 @@ class Arm:
             self.hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
         self.hctx.set_hash_split(args.split_min)
         self.hctx.set_hash_grid(args.k1_grid)
+        if self.overlap and args.k1_gate == "on":
+            self.hctx.set_hash_gate(self.ctx)
         self.ev_h = {}
         torch.cuda.synchronize(dev)
         self.ctx.check_device_error()
@@ -484,7 +489,9 @@ def run_ours(args):
                         "larger than the 126 MB L2" % (arm.bursts[-1].b.n_tokens * 8 / 1e9),
             "parallelism": "one GPU holds every replica",
             "k1_overlap": (f"K1 of burst k+1 on a second stream (grid = SMs - {args.free_sms}) "
-                           f"from step k's {'K2 end' if args.k1_after == 'staged' else 'start'}; "
+                           f"from step k's {'K2 end' if args.k1_after == 'staged' else 'start'}, "
+                           f"grid {args.k1_grid}"
+                           f"{', paused while the admission runs' if args.k1_gate == 'on' else ''}; "
                            "each step's own K1 is inside the timed region")
             if arm.overlap else "none (serial)"},
         "roofline": {"bound": "hbm", "kernel": "k_hash_staged (K1, chain_boundary_hashes)",
@@ -718,6 +725,8 @@ def run_sharded(args):
     hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
     hctx.set_hash_split(args.split_min)
     hctx.set_hash_grid(args.k1_grid)
+    if args.k1_gate == "on":
+        hctx.set_hash_gate(ctx)
     ev_h = {}
 
     def hash_into(k, hev=None):

@@ -215,6 +215,12 @@ int pyg_set_hash_ctas(pyg_ctx* ctx, int32_t n_ctas);
    with at most one K1 CTA per SM (shared memory padded), the rest of each SM left to the
    step's kernels. */
 int pyg_set_hash_grid(pyg_ctx* ctx, int32_t mode);
+/* Admission gate: K1 launches of hash_ctx pause (warps sleep between 16-token chunks) while
+   step_ctx runs an admission (pyg_admit_batch_dev / pyg_admit_shard_dev), so the
+   latency-bound admission gets its SMs' issue slots; step_ctx = NULL removes the gate.
+   Same device; honoured with K1 grid modes 1 and 2 (room for admission CTAs beside the
+   paused K1 CTAs).  step_ctx must outlive hash_ctx's K1 launches. */
+int pyg_set_hash_gate(pyg_ctx* hash_ctx, pyg_ctx* step_ctx);
 /* K1 hashes prompts of >= min_tokens tokens as split tasks: one warp per prompt, 512 tokens
    at a time, through the low-byte decomposition of FNV-1a (k_hash.cu) -- the same hashes,
    without the long-prompt tail of one lane per request.  0 = never; -1 (default) = a

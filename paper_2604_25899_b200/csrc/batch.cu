@@ -136,11 +136,15 @@ struct AdmitArgs {
   int32_t n_rep;
 };
 
+__global__ void k_gate_open(int32_t* gate) { atomicExch(gate, 0); }
+
 // Queue order of k_admit: replicas by descending placement count (a counting sort on one
 // CTA), so the CTAs of a grid smaller than the replica count -- or sharing the SMs with K1
 // of the next burst -- pull the longest admission sequences first and finish together.
 __global__ void __launch_bounds__(1024) k_admit_order(const int32_t* placed_off, int32_t n_rep,
-                                                      int32_t* order, int32_t* next) {
+                                                      int32_t* order, int32_t* next,
+                                                      int32_t* gate) {
+  if (gate && threadIdx.x == 0) atomicExch(gate, 1);  // K1 of another ctx pauses (set_hash_gate)
   __shared__ int32_t hist[1024];
   __shared__ int64_t sm[33];
   hist[threadIdx.x] = 0;
@@ -746,16 +750,24 @@ static int admit_core(pyg_ctx* c, const uint64_t* d_tokens, const int64_t* d_tok
   auto* cnt = reinterpret_cast<unsigned long long*>(d_counts);
   int32_t* order = ctl + 64;
   int32_t* next = ctl + 60;
-  k_admit_order<<<1, 1024, 0, c->stream>>>(d_placed_off, c->n_rep, order, next);
+  k_admit_order<<<1, 1024, 0, c->stream>>>(d_placed_off, c->n_rep, order, next, c->d_gate);
   PYG_LAUNCHED(c);
   AdmitArgs a{d_tokens, d_tok_off, d_hash_off, d_hashes, d_wf, d_role, d_placed_off, d_placed,
               now, speculative, d_admitted, d_match3, rec,
               static_cast<DirRecord*>(l2_out), l2_cap, cnt, order, next, c->n_rep};
   const size_t smem = kSmemSortCap * 12;
   PYG_CUDA(cudaFuncSetAttribute(k_admit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // gated K1 (pyg_set_hash_gate): all shared, room for a paused K1 CTA beside it
+  if (c->d_gate)
+    PYG_CUDA(cudaFuncSetAttribute(k_admit, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
   // two CTAs per SM when the SMs are free; each pulls replicas until the queue is empty
   const int grid = std::min(c->n_rep, 2 * pyg_host::sm_count(c->device));
   k_admit<<<grid, 512, smem, c->stream>>>(c->hd, a);
+  if (c->d_gate) {
+    PYG_LAUNCHED(c);
+    k_gate_open<<<1, 1, 0, c->stream>>>(c->d_gate);
+  }
   c->dir_admits += 1;
   PYG_LAUNCHED(c);
   return PYG_OK;

@@ -283,6 +283,7 @@ void pyg_destroy(pyg_ctx* c) {
   cudaFree(c->d_scratch);
   cudaFree(c->d_aux);
   cudaFree(c->d_claim);
+  cudaFree(c->d_gate);
   cudaFree(c->memo);
   cudaFree(c->d_list);
   cudaFree(c->dir_mem);

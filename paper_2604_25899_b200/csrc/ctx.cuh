@@ -44,6 +44,10 @@ struct pyg_ctx {
   int64_t dir_admits = 0;    // admission calls since the last build (cleared bits accumulate)
   int32_t hash_ctas = 0;     // K1 persistent grid cap (0 = one CTA per SM)
   int32_t hash_grid = 1;  // K1 grid: 0 one task per warp, 1 persistent, 2 = 0 at 1 CTA/SM
+  // admission gate: d_gate (this ctx's admissions hold it at 1 while they run); hash_gate =
+  // another ctx's d_gate that this ctx's K1 pauses on (pyg_set_hash_gate)
+  int32_t* d_gate = nullptr;
+  const int32_t* hash_gate = nullptr;
   int64_t split_min = -1;    // K1: prompts of >= split_min tokens are split tasks (0 = never,
                              // -1 = a threshold from the batch's token count, k_split_count)
   void* d_aux = nullptr;     // second on-demand buffer (fused assembly's chunk sources)

@@ -59,6 +59,17 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
                "r"(src_bytes));
 }
+// admission gate (pyg_set_hash_gate): K1 warps read it once per chunk and, when it is set,
+// sleep until the step's admission has finished (the latency-bound admission then runs
+// without K1 warps competing for its SMs' issue slots)
+__device__ __forceinline__ int gate_load(const int32_t* g) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(g));
+  return v;
+}
+__device__ __forceinline__ void gate_wait(const int32_t* g) {
+  while (gate_load(g)) __nanosleep(1000);
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
@@ -183,7 +194,8 @@ __device__ __forceinline__ uint32_t lo8_step(uint32_t x, uint32_t w, int bi) {
 // One split task: request of n tokens at src, boundary hashes to out (B % 16 == 0).
 // wbuf: this warp's 2 staging buffers (rows of kRowBytes, row l = segment l).
 __device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_t n, int B,
-                           uint64_t* __restrict__ out, unsigned char* wbuf) {
+                           uint64_t* __restrict__ out, unsigned char* wbuf,
+                           const int32_t* gate = nullptr) {
   const int lane = threadIdx.x & 31;
   const int nsc = static_cast<int>((n + kSuper - 1) / kSuper);
   auto issue = [&](int sc) {
@@ -200,6 +212,7 @@ __device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_
   uint64_t H0 = kFnvOffset;  // hash at the super-chunk start (warp-uniform)
   issue(0);
   for (int sc = 0; sc < nsc; ++sc) {
+    const int gz = gate ? gate_load(gate) : 0;
     if (sc + 1 < nsc)
       issue(sc + 1);
     else
@@ -286,6 +299,7 @@ __device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_
     const int64_t nv = min(static_cast<int64_t>(kSuper), n - static_cast<int64_t>(sc) * kSuper);
     H0 = __shfl_sync(kFull, hend, static_cast<int>((nv - 1) / kSplitTok));
     __syncwarp();
+    if (gz) gate_wait(gate);
   }
 }
 
@@ -301,7 +315,7 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1))
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
               uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task, GatherSrc g,
-              const int* __restrict__ n_split_p) {
+              const int* __restrict__ n_split_p, const int32_t* gate) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbuf = smem + warp * 2 * kStageBytes;
@@ -329,7 +343,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   if (task < n_split) {
     const int r = order[task];
     const int64_t s0 = tok_off[r];
-    split_task(tokens + s0, tok_off[r + 1] - s0, B, hashes + hash_off[r], wbuf);
+    split_task(tokens + s0, tok_off[r + 1] - s0, B, hashes + hash_off[r], wbuf, gate);
     continue;
   }
   const int idx = n_split + (task - n_split) * 32 + lane;
@@ -432,6 +446,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   int64_t k = 0;
   issue(0);
   for (int c = 0; c < maxch; ++c) {
+    const int gz = gate ? gate_load(gate) : 0;
     if (c + 1 < maxch)
       issue(c + 1);
     else
@@ -463,6 +478,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
       }
     }
     __syncwarp();
+    if (gz) gate_wait(gate);
   }
   }  // task loop
 }
@@ -724,16 +740,19 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   // stays free for the step's kernels); the launch sizes are set in device_setup
   const int pad = c->hash_grid == 2 && W == kWarps ? kSmemOneCta : 0;
   int* next = persistent ? ctr0 : nullptr;
+  // the admission gate needs room for admission CTAs beside the paused K1 CTAs: honoured
+  // with the persistent grid (<= one CTA per SM of 148) and grid mode 2 (one per SM) only
+  const int32_t* gate = c->hash_grid != 0 ? c->hash_gate : nullptr;
   if (W == 16)
     k_hash_staged<kGather, 16><<<grid, 16 * 32, smem_bytes(16), c->stream>>>(
-        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1);
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate);
   else if (W == 12)
     k_hash_staged<kGather, 12><<<grid, 12 * 32, smem_bytes(12), c->stream>>>(
-        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1);
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate);
   else
     k_hash_staged<kGather, kWarps><<<grid, kWarps * 32, std::max(pad, smem_bytes(kWarps)),
                                      c->stream>>>(
-        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1);
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -775,6 +794,31 @@ int pyg_assemble_hash_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
   PYG_LAUNCHED(c);
   return hash_launch<true>(c, d_pool, d_tok_off, R, d_hash_off, d_hashes,
                            GatherSrc{tab, d_tokens});
+}
+
+int pyg_set_hash_gate(pyg_ctx* c, pyg_ctx* step) {
+  PYG_ON_DEVICE(c);
+  if (!c) return PYG_EINVAL;
+  if (!step) {
+    c->hash_gate = nullptr;
+    return PYG_OK;
+  }
+  if (step->device != c->device) return PYG_EINVAL;
+  if (!step->d_gate) {
+    PYG_CUDA(cudaMalloc(&step->d_gate, sizeof(int32_t)));
+    PYG_CUDA(cudaMemset(step->d_gate, 0, sizeof(int32_t)));
+  }
+  PYG_CUDA(pyg_host::device_setup(c->device));
+  // the whole 228 KB as shared memory on the SMs K1 runs on: an SM's L1/shared split is
+  // fixed while CTAs are resident, and with the split the driver picks for K1 alone (~100 KB)
+  // the admission CTAs (~103 KB) could not start beside a paused K1 CTA (k_admit asks for
+  // the same when its ctx has a gate)
+  for (const void* f : {reinterpret_cast<const void*>(k_hash_staged<false, kWarps>),
+                        reinterpret_cast<const void*>(k_hash_staged<true, kWarps>)})
+    PYG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+  c->hash_gate = step->d_gate;
+  return PYG_OK;
 }
 
 int pyg_set_hash_split(pyg_ctx* c, int64_t min_tokens) {

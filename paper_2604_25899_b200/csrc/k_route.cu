@@ -302,7 +302,10 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
     for (int j = lane; j < nc; j += 32) s_ba[j] = bound_loop(A.nodes, A.ns, s_node[j], astar);
     __syncwarp();
   }
+  // class maxima F0 / Fa of the free capacity over the bound-feasible nodes, and the node
+  // holding it when it is unique (u0 / ua, else -1)
   int64_t F0 = INT64_MIN, Fa = INT64_MIN;
+  int u0 = -1, ua = -1;
   auto refresh = [&]() {
     int64_t f0 = INT64_MIN, fa = INT64_MIN;
     for (int j = lane; j < nc; j += 32) {
@@ -311,6 +314,19 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
     }
     F0 = redux_max_i64(f0);
     Fa = redux_max_i64(fa);
+    int n0 = 0, na = 0, w0 = -1, wa = -1;
+    for (int jb = 0; jb < nc; jb += 32) {
+      const int j = jb + lane;
+      const unsigned m0 = __ballot_sync(kFull, j < nc && !(s_b0[j] > A.eps) && s_free[j] == F0);
+      const unsigned ma = __ballot_sync(
+          kFull, have_star && j < nc && !(s_ba[j] > A.eps) && s_free[j] == Fa);
+      if (m0 && w0 < 0) w0 = jb + __ffs(m0) - 1;
+      if (ma && wa < 0) wa = jb + __ffs(ma) - 1;
+      n0 += __popc(m0);
+      na += __popc(ma);
+    }
+    u0 = n0 == 1 ? w0 : -1;
+    ua = na == 1 ? wa : -1;
   };
   refresh();
   auto bound_of = [&](int j, int cls, double al) -> double {
@@ -401,113 +417,125 @@ __global__ void __launch_bounds__(32) k_route_seq(SeqArgs A) {
         if (u == uu) cl = __shfl_sync(kFull, cl4[u], owner);
       // classes 0 / 1 are bit-identical to +0.0 / a*; only "other" alphas are fetched
       const double a = cl == 0 ? 0.0 : (cl == 1 ? astar : A.req[first].alpha);
-      // the staged row is read where it is needed (one L2 line per evaluated request);
-      // staging every visited chunk's rows in shared memory cost more than it saved once
-      // groups interleave (probe: tools/route_probe.py)
-      int32_t own_v = 0;
-      // the next request of this group in the chunk (narrow groups) / the next one that
-      // could fit under the current state (wide groups: a mispredicted row costs a full
-      // L2 round trip there)
-      int nx = INT32_MAX;
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int r = base + lane * kPer + u;
-        if (!mine[u] || r <= first) continue;
-        const int cls = cl4[u];
-        if (nc <= 32 || (cls == 0 ? t[u] <= F0 : (cls == 1 ? t[u] <= Fa : true))) nx = min(nx, r);
-      }
-      nx = __reduce_min_sync(kFull, nx);
-      if (nc <= 32) {
-        // load the next request's value now: its evaluation (usually the next one) then
-        // finds its staged value in a register instead of waiting on L2
-        own_v = (first == pre_r)
-                    ? pre_v
-                    : (lane < nc ? A.staged[static_cast<int64_t>(first) * A.max_cand + lane] : 0);
-        pre_r = nx;
-        if (nx != INT32_MAX && lane < nc) pre_v = A.staged[static_cast<int64_t>(nx) * A.max_cand + lane];
-      } else {
-        // wide groups: the row was prefetched into s_stg[wide_buf] if `first` is the
-        // request predicted last time, else it is loaded now (8 loads in flight per lane)
-        asm volatile("cp.async.wait_all;\n" ::);
-        __syncwarp();
-        if (first != wide_pre) {
-          const int32_t* row = A.staged + static_cast<int64_t>(first) * A.max_cand;
-          for (int jb = 0; jb < nc; jb += 256) {
-            int32_t v[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = jb + lane + 32 * i;
-              v[i] = j < nc ? row[j] : 0;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = jb + lane + 32 * i;
-              if (j < nc) s_stg[wide_buf][j] = v[i];
-            }
-          }
-        }
-        __syncwarp();
-        // prefetch the next request's row into the other buffer (read one evaluation ago)
-        wide_pre = nx;
-        if (nx != INT32_MAX) {
-          const int32_t* row = A.staged + static_cast<int64_t>(nx) * A.max_cand;
-          int32_t* dst = s_stg[wide_buf ^ 1];
-          for (int j = lane; j < nc; j += 32) {
-            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + j));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(row + j));
-          }
-          asm volatile("cp.async.commit_group;\n" ::);
-        }
-      }
-      const int32_t* stg = s_stg[wide_buf];
-      if (nc > 32) wide_buf ^= 1;  // the prefetched row becomes current next time
-      auto staged_of = [&](int j) -> int32_t {
-        if (nc > 32) return stg[j];
-        return j == lane ? own_v : A.staged[static_cast<int64_t>(first) * A.max_cand + j];
-      };
-      // full sched::route over the group's candidates (router.cpp:24-43): the
-      // reference's strict lexicographic running max on (headroom, staged, -replica_id) in
-      // input order == argmax of (h, s, -id, -pos); tiebreak <=> first position with
-      // headroom H precedes the first with (H, S)
+      // classes 0 / 1 whose maximum is held by ONE bound-feasible node: that node alone has
+      // the largest headroom, so it wins whatever the staged values and p1 == p2 (no
+      // tiebreak) -- no staged row, no reductions
+      const int uniq = cl == 0 ? u0 : (cl == 1 ? ua : -1);
       RouteAcc best{0, 0, 0, -1};
-      // classes 0 / 1: headroom order is free-capacity order (tt is fixed per request),
-      // so the winners are the bound-feasible nodes whose free capacity equals F0 / Fa
-      // (the class maxima refresh() keeps); only that tie set is scanned for staged / id.
-      // "Other" alphas need bound_loop per node: full scan.
-      const bool by_max = cl < 2;
-      const int64_t F = cl == 0 ? F0 : Fa;
-      for (int j = lane; j < nc; j += 32) {
-        const int64_t fr = s_free[j];
-        if (by_max ? (fr != F || tt > fr) : tt > fr) continue;
-        if (bound_of(j, cl, a) > A.eps) continue;
-        RouteAcc x{fr - tt, staged_of(j), s_rid[j], j};
-        if (acc_better(x, best)) best = x;
-      }
-      const int64_t H = redux_max_i64(best.pos >= 0 ? best.h : INT64_MIN);
-      if (H != INT64_MIN) {
-        const bool onH = best.pos >= 0 && best.h == H;
-        const int64_t S = redux_max_i64(onH ? best.s : INT64_MIN);
-        const bool onS = onH && best.s == S;
-        const int32_t ID = __reduce_min_sync(kFull, onS ? best.id : INT32_MAX);
-        const int32_t POS = __reduce_min_sync(kFull, onS && best.id == ID ? best.pos : INT32_MAX);
-        best = RouteAcc{H, S, ID, POS};
+      int tb = 0;
+      if (uniq >= 0) {
+        best = RouteAcc{(cl == 0 ? F0 : Fa) - tt, 0, s_rid[uniq], uniq};
       } else {
-        best.pos = -1;
-      }
-      if (best.pos >= 0) {
-        int32_t p1 = 0x7fffffff, p2 = 0x7fffffff;
+        // the staged row is read where it is needed (one L2 line per evaluated request);
+        // staging every visited chunk's rows in shared memory cost more than it saved once
+        // groups interleave (probe: tools/route_probe.py)
+        int32_t own_v = 0;
+        // the next request of this group in the chunk (narrow groups) / the next one that
+        // could fit under the current state (wide groups: a mispredicted row costs a full
+        // L2 round trip there)
+        int nx = INT32_MAX;
+  #pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int r = base + lane * kPer + u;
+          if (!mine[u] || r <= first) continue;
+          const int cls = cl4[u];
+          if (nc <= 32 || (cls == 0 ? t[u] <= F0 : (cls == 1 ? t[u] <= Fa : true))) nx = min(nx, r);
+        }
+        nx = __reduce_min_sync(kFull, nx);
+        if (nc <= 32) {
+          // load the next request's value now: its evaluation (usually the next one) then
+          // finds its staged value in a register instead of waiting on L2
+          own_v = (first == pre_r)
+                      ? pre_v
+                      : (lane < nc ? A.staged[static_cast<int64_t>(first) * A.max_cand + lane] : 0);
+          pre_r = nx;
+          if (nx != INT32_MAX && lane < nc) pre_v = A.staged[static_cast<int64_t>(nx) * A.max_cand + lane];
+        } else {
+          // wide groups: the row was prefetched into s_stg[wide_buf] if `first` is the
+          // request predicted last time, else it is loaded now (8 loads in flight per lane)
+          asm volatile("cp.async.wait_all;\n" ::);
+          __syncwarp();
+          if (first != wide_pre) {
+            const int32_t* row = A.staged + static_cast<int64_t>(first) * A.max_cand;
+            for (int jb = 0; jb < nc; jb += 256) {
+              int32_t v[8];
+  #pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int j = jb + lane + 32 * i;
+                v[i] = j < nc ? row[j] : 0;
+              }
+  #pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int j = jb + lane + 32 * i;
+                if (j < nc) s_stg[wide_buf][j] = v[i];
+              }
+            }
+          }
+          __syncwarp();
+          // prefetch the next request's row into the other buffer (read one evaluation ago)
+          wide_pre = nx;
+          if (nx != INT32_MAX) {
+            const int32_t* row = A.staged + static_cast<int64_t>(nx) * A.max_cand;
+            int32_t* dst = s_stg[wide_buf ^ 1];
+            for (int j = lane; j < nc; j += 32) {
+              const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + j));
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(row + j));
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+          }
+        }
+        const int32_t* stg = s_stg[wide_buf];
+        if (nc > 32) wide_buf ^= 1;  // the prefetched row becomes current next time
+        auto staged_of = [&](int j) -> int32_t {
+          if (nc > 32) return stg[j];
+          return j == lane ? own_v : A.staged[static_cast<int64_t>(first) * A.max_cand + j];
+        };
+        // full sched::route over the group's candidates (router.cpp:24-43): the
+        // reference's strict lexicographic running max on (headroom, staged, -replica_id) in
+        // input order == argmax of (h, s, -id, -pos); tiebreak <=> first position with
+        // headroom H precedes the first with (H, S)
+        // classes 0 / 1: headroom order is free-capacity order (tt is fixed per request),
+        // so the winners are the bound-feasible nodes whose free capacity equals F0 / Fa
+        // (the class maxima refresh() keeps); only that tie set is scanned for staged / id.
+        // "Other" alphas need bound_loop per node: full scan.
+        const bool by_max = cl < 2;
+        const int64_t F = cl == 0 ? F0 : Fa;
         for (int j = lane; j < nc; j += 32) {
           const int64_t fr = s_free[j];
-          if (tt > fr || fr - tt != best.h) continue;
+          if (by_max ? (fr != F || tt > fr) : tt > fr) continue;
           if (bound_of(j, cl, a) > A.eps) continue;
-          p1 = min(p1, j);
-          if (staged_of(j) == best.s) p2 = min(p2, j);
+          RouteAcc x{fr - tt, staged_of(j), s_rid[j], j};
+          if (acc_better(x, best)) best = x;
         }
-        p1 = __reduce_min_sync(kFull, p1);
-        p2 = __reduce_min_sync(kFull, p2);
+        const int64_t H = redux_max_i64(best.pos >= 0 ? best.h : INT64_MIN);
+        if (H != INT64_MIN) {
+          const bool onH = best.pos >= 0 && best.h == H;
+          const int64_t S = redux_max_i64(onH ? best.s : INT64_MIN);
+          const bool onS = onH && best.s == S;
+          const int32_t ID = __reduce_min_sync(kFull, onS ? best.id : INT32_MAX);
+          const int32_t POS = __reduce_min_sync(kFull, onS && best.id == ID ? best.pos : INT32_MAX);
+          best = RouteAcc{H, S, ID, POS};
+        } else {
+          best.pos = -1;
+        }
+        if (best.pos >= 0) {
+          int32_t p1 = 0x7fffffff, p2 = 0x7fffffff;
+          for (int j = lane; j < nc; j += 32) {
+            const int64_t fr = s_free[j];
+            if (tt > fr || fr - tt != best.h) continue;
+            if (bound_of(j, cl, a) > A.eps) continue;
+            p1 = min(p1, j);
+            if (staged_of(j) == best.s) p2 = min(p2, j);
+          }
+          p1 = __reduce_min_sync(kFull, p1);
+          p2 = __reduce_min_sync(kFull, p2);
+          tb = p1 < p2 ? 1 : 0;
+        }
+      }
+      if (best.pos >= 0) {
         const int w = best.pos;
         if (lane == 0) {
-          A.out[first] = pyg_decision{best.id, p1 < p2 ? 1 : 0, best.h, bound_of(w, cl, a)};
+          A.out[first] = pyg_decision{best.id, tb, best.h, bound_of(w, cl, a)};
           const int n = s_node[w];
           A.t_idx[first] = n;
           A.glist[lbase + nplaced] = first;
