@@ -23,11 +23,9 @@
 // config-2 length mix (tools/k1/k1_variants.cu).
 #include <cuda_runtime.h>
 
-#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "ctx.cuh"
 #include "device_ops.cuh"
@@ -470,10 +468,22 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
         }
       } else {
         const int p1 = rem < kChunk ? static_cast<int>(rem) : kChunk;
-        for (int p = 0; p < p1; ++p) {
-          h = fnv_token(h, *reinterpret_cast<const uint64_t*>(row + 8 * p));
-          const int64_t j = static_cast<int64_t>(c) * kChunk + p;  // position in the request
-          if ((j + 1) % B == 0 || j + 1 == n) out[k++] = h;  // hierarchy.cpp:26
+        if (fast) {
+          // the request's last, partial chunk: block boundaries (multiples of B, a multiple
+          // of 16, from the chunk-aligned request start) fall only on full chunks, so the
+          // one emit is the last token's (hierarchy.cpp:26)
+          for (int p = 0; p < p1; ++p)
+            h = fnv_token(h, *reinterpret_cast<const uint64_t*>(row + 8 * p));
+          out[k++] = h;
+        } else {
+          // B % 16 != 0: per token; `left` counts down to the next boundary
+          int64_t j = static_cast<int64_t>(c) * kChunk;  // position in the request
+          int left = B - static_cast<int>(j % B);
+          for (int p = 0; p < p1; ++p, ++j) {
+            h = fnv_token(h, *reinterpret_cast<const uint64_t*>(row + 8 * p));
+            if (--left == 0 || j + 1 == n) out[k++] = h;  // hierarchy.cpp:26
+            if (left == 0) left = B;
+          }
         }
       }
     }
@@ -501,104 +511,168 @@ __global__ void __launch_bounds__(32) k_hash_seq(const uint64_t* __restrict__ to
   }
 }
 
-// Length histogram of the adaptive split threshold: 8 bins per octave from 512 tokens
-// (bin 0 = shorter), tokens and request counts per bin.
+// ------------------------------------------------------------- K1 task order
+// K1 hashes requests longest first (split tasks, then 32-request tasks of near-equal
+// lengths so the lanes of a warp finish together).  The order is a counting sort, descending
+// over ORDER BUCKETS of the length: 32 per octave from 512 tokens (2.2% wide), 32-token-wide
+// below; with a fixed split threshold the split requests get buckets of their own above all
+// others.  Three kernels, no library sort: histogram (k_len_hist), bucket cursors and the
+// split threshold (k_order_plan, one CTA), scatter (k_order_fill).
+//
+// The adaptive split threshold uses a coarser histogram derived from the order buckets: 8
+// bins per octave from 512 tokens (bin 0 = shorter), requests and (estimated) tokens per
+// bin; split bin k covers order buckets 32 + 4 (k - 1) .. 32 + 4 k - 1, so "bin >= k" is a
+// suffix of the order.
 constexpr int kHistBins = 80;
-__device__ __forceinline__ int len_bin(int64_t n) {
-  if (n < 512) return 0;
-  const double b = 8.0 * log2(static_cast<double>(n) / 512.0);
-  const int k = 1 + static_cast<int>(b);
-  return k < kHistBins ? k : kHistBins - 1;
+constexpr int kOrdPerOct = 32;
+constexpr int kOrd = 32 + kOrdPerOct * 15;  // lengths below 512 * 2^15 tokens; longer share the top
+constexpr int kOrdAll = 2 * kOrd;           // + the split buckets of a fixed threshold
+static_assert(kOrdAll <= 1024, "k_order_plan scans the buckets with one CTA");
+__device__ __forceinline__ int ord_of(int64_t n) {
+  if (n < 512) return static_cast<int>(n >> 4);
+  const int o = static_cast<int>(kOrdPerOct * log2(static_cast<double>(n) / 512.0));
+  return min(32 + o, kOrd - 1);
+}
+__device__ __forceinline__ int bin_of_ord(int ob) {
+  return ob < 32 ? 0 : min(1 + ((ob - 32) >> 2), kHistBins - 1);
 }
 __device__ __forceinline__ double bin_lo(int k) { return k == 0 ? 0.0 : 512.0 * exp2((k - 1) / 8.0); }
 
-struct SplitHist {
-  unsigned long long tok[kHistBins];
-  unsigned long long cnt[kHistBins];
+constexpr int kFillThreads = 1024;  // requests per CTA of k_len_hist / k_order_fill
+
+struct OrderPlan {
   unsigned long long max_len;
+  unsigned int ord[kOrdAll];          // requests per order bucket, then the bucket cursors
 };
 
-__global__ void k_len_keys(const int64_t* tok_off, int R, uint16_t* key, int32_t* val,
-                           int64_t split_min, int* n_split, SplitHist* hist) {
-  __shared__ unsigned long long s_tok[kHistBins], s_cnt[kHistBins], s_max;
-  const bool adaptive = split_min < 0;
-  if (adaptive) {
-    for (int k = threadIdx.x; k < kHistBins; k += blockDim.x) s_tok[k] = s_cnt[k] = 0;
-    if (threadIdx.x == 0) s_max = 0;
-  }
+__device__ __forceinline__ int bucket_of(int64_t n, int64_t split_min) {
+  return ord_of(n) + (split_min > 0 && n >= split_min ? kOrd : 0);
+}
+
+__global__ void __launch_bounds__(kFillThreads) k_len_hist(const int64_t* tok_off, int R,
+                                                           int64_t split_min, int* n_split,
+                                                           OrderPlan* plan) {
+  __shared__ unsigned int s_ord[kOrdAll];
+  __shared__ unsigned long long s_max;
+  for (int k = threadIdx.x; k < kOrdAll; k += blockDim.x) s_ord[k] = 0;
+  if (threadIdx.x == 0) s_max = 0;
   __syncthreads();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = r < R ? tok_off[r + 1] - tok_off[r] : 0;
-  if (r < R) {
-    const int64_t L = (n + 3) >> 2;
-    key[r] = static_cast<uint16_t>(L > 65535 ? 65535 : L);
-    val[r] = r;
-  }
+  const bool sp = split_min > 0 && n >= split_min;
+  if (r < R) atomicAdd(s_ord + ord_of(n) + (sp ? kOrd : 0), 1u);
   if (split_min > 0) {  // fixed threshold: count the split requests here
-    const unsigned m = __ballot_sync(kFull, r < R && n >= split_min);
+    const unsigned m = __ballot_sync(kFull, sp);
     if (m && (threadIdx.x & 31) == 0) atomicAdd(n_split, __popc(m));
-  } else if (adaptive) {
-    if (r < R) {
-      const int k = len_bin(n);
-      atomicAdd(s_tok + k, static_cast<unsigned long long>(n));
-      atomicAdd(s_cnt + k, 1ULL);
-    }
-    // one global atomic per CTA (all requests on one address would serialise in L2)
-    const unsigned long long wmax =
-        __reduce_max_sync(kFull, static_cast<unsigned>(n));  // n < 2^32 tokens
-    if ((threadIdx.x & 31) == 0 && wmax) atomicMax(&s_max, wmax);
-    __syncthreads();
-    if (threadIdx.x == 0 && s_max) atomicMax(&hist->max_len, s_max);
-    for (int k = threadIdx.x; k < kHistBins; k += blockDim.x)
-      if (s_cnt[k]) {
-        atomicAdd(hist->tok + k, s_tok[k]);
-        atomicAdd(hist->cnt + k, s_cnt[k]);
-      }
   }
+  // one global atomic per CTA and bucket (all requests on one address would serialise in L2)
+  const unsigned wmax = __reduce_max_sync(kFull, static_cast<unsigned>(n));  // n < 2^32
+  if ((threadIdx.x & 31) == 0 && wmax) atomicMax(&s_max, static_cast<unsigned long long>(wmax));
+  __syncthreads();
+  for (int k = threadIdx.x; k < kOrdAll; k += blockDim.x)
+    if (s_ord[k]) atomicAdd(plan->ord + k, s_ord[k]);
+  if (threadIdx.x == 0 && s_max) atomicMax(&plan->max_len, s_max);
 }
 
-// Adaptive split threshold: choose the length from which prompts become split tasks by a
-// makespan model of K1 on one B200 -- the longest one-lane task, the longest split task, the
-// work (constants below) -- over "no split" and the histogram's bin edges from 512 tokens up.  Many long prompts keep one lane each (their chains overlap, config 3); a
-// few long ones in a large batch, or any in a small batch, are split.  The split requests are
-// the first n_split of the descending order (binary search of the sorted keys).
-__global__ void k_split_count(const uint16_t* sorted_keys, int R, const SplitHist* hist,
-                              int* n_split) {
-  if (threadIdx.x) return;
-  // measured on B200 (tools/k1_sweep.py, config-4 burst of 125k requests at thresholds
-  // 4k..16k): a one-lane chain in a loaded SM ~90 ns per token, a split task ~8 ns per
-  // token, ~280 Gtok/s one lane per request, a split token costs 2.8 lane tokens
-  const double c_lane = 90e-9, c_split = 8e-9, rate = 280e9, extra = 1.8;
-  double total = 0;
-  for (int k = 0; k < kHistBins; ++k) total += static_cast<double>(hist->tok[k]);
-  const double lmax = static_cast<double>(hist->max_len);
-  double best = fmax(lmax * c_lane, total / rate);  // no split
-  double best_T = 1e30;
-  double above = 0;                                  // tokens of bins >= k
-  for (int k = kHistBins - 1; k >= 1; --k) {
-    above += static_cast<double>(hist->tok[k]);
-    if (!hist->cnt[k] && above == 0) continue;
-    const double T = bin_lo(k);
-    const double cost = fmax(fmax(T * c_lane, lmax * c_split), (total + extra * above) / rate);
-    if (cost < best) {
-      best = cost;
-      best_T = T;
+// One CTA of 1024 threads: (adaptive) the split threshold -- a makespan model of K1 on one
+// B200 over "no split" and every bin edge from 512 tokens up: the longest one-lane task, the
+// longest split task, the work (constants below); many long prompts keep one lane each
+// (their chains overlap, config 3), a few long ones in a large batch, or any in a small
+// batch, are split -- then the bucket cursors: exclusive scan of the counts in descending
+// bucket order.
+__global__ void __launch_bounds__(1024) k_order_plan(OrderPlan* plan, int adaptive, int* n_split) {
+  __shared__ int64_t sm[33];
+  __shared__ double s_cost[32];
+  __shared__ int s_k[32];
+  __shared__ unsigned long long s_tok[kHistBins], s_cnt[kHistBins];
+  const int t = threadIdx.x;
+  if (adaptive) {
+    // the split model's histogram from the order buckets: requests per bin exact, tokens
+    // as count x the bucket's mid length (buckets are 2.2% wide: the model's inputs to ~1%)
+    if (t < kHistBins) s_tok[t] = s_cnt[t] = 0;
+    __syncthreads();
+    if (t < kOrd && plan->ord[t]) {
+      const double mid = t < 32 ? 16.0 * t + 8.0 : 512.0 * exp2((t - 32 + 0.5) / kOrdPerOct);
+      const int k = bin_of_ord(t);
+      atomicAdd(s_cnt + k, static_cast<unsigned long long>(plan->ord[t]));
+      atomicAdd(s_tok + k, static_cast<unsigned long long>(mid * plan->ord[t]));
+    }
+    __syncthreads();
+    // measured on B200 (tools/k1_sweep.py, config-4 burst of 125k requests at thresholds
+    // 4k..16k): a one-lane chain in a loaded SM ~90 ns per token, a split task ~8 ns per
+    // token, ~280 Gtok/s one lane per request, a split token costs 2.8 lane tokens
+    const double c_lane = 90e-9, c_split = 8e-9, rate = 280e9, extra = 1.8;
+    // tokens of bins >= k (k = t): inclusive scan of the bins in descending order
+    const int kd = kHistBins - 1 - t;  // thread t holds bin kHistBins - 1 - t
+    const int64_t tk = t < kHistBins ? static_cast<int64_t>(s_tok[kd]) : 0;
+    int64_t tot;
+    const int64_t above = block_exscan(tk, sm, &tot) + tk;  // tokens in bins >= kd
+    const double total = static_cast<double>(tot);
+    const double lmax = static_cast<double>(plan->max_len);
+    double cost = 1e300;
+    int kk = -1;
+    if (t < kHistBins && kd >= 1 && (s_cnt[kd] || above)) {
+      const double T = bin_lo(kd);
+      cost = fmax(fmax(T * c_lane, lmax * c_split), (total + extra * above) / rate);
+      kk = kd;
+    }
+    // minimum cost, ties to the larger threshold (the model's scan from the top)
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oc = __shfl_xor_sync(kFull, cost, o);
+      const int ok = __shfl_xor_sync(kFull, kk, o);
+      if (oc < cost || (oc == cost && ok > kk)) {
+        cost = oc;
+        kk = ok;
+      }
+    }
+    if ((t & 31) == 0) {
+      s_cost[t >> 5] = cost;
+      s_k[t >> 5] = kk;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double best = fmax(lmax * c_lane, total / rate);  // no split
+      int bk = -1;
+      for (int w = 0; w < 32; ++w)
+        if (s_k[w] >= 0 && (s_cost[w] < best || (s_cost[w] == best && bk >= 0 && s_k[w] > bk))) {
+          best = s_cost[w];
+          bk = s_k[w];
+        }
+      unsigned long long ns = 0;
+      if (bk >= 1)
+        for (int k = bk; k < kHistBins; ++k) ns += s_cnt[k];
+      *n_split = static_cast<int>(ns);
     }
   }
-  if (best_T >= 1e29) {
-    *n_split = 0;
-    return;
+  // cursors: bucket b starts after every request of the buckets above it
+  const int b = kOrdAll - 1 - t;
+  const int64_t v = b >= 0 ? plan->ord[b] : 0;
+  int64_t all;
+  const int64_t ex = block_exscan(v, sm, &all);
+  if (b >= 0) plan->ord[b] = static_cast<unsigned int>(ex);
+}
+
+// order[pos] = r: each CTA ranks its requests per bucket in shared memory and reserves its
+// range of every bucket it touches with ONE global atomic (the lengths crowd into a few
+// dozen buckets: per-warp atomics serialise in L2)
+__global__ void __launch_bounds__(kFillThreads) k_order_fill(const int64_t* tok_off, int R,
+                                                             int64_t split_min, OrderPlan* plan,
+                                                             int32_t* order) {
+  __shared__ unsigned int s_cnt[kOrdAll];
+  for (int k = threadIdx.x; k < kOrdAll; k += blockDim.x) s_cnt[k] = 0;
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  int bk = -1;
+  unsigned rk = 0;
+  if (r < R) {
+    bk = bucket_of(tok_off[r + 1] - tok_off[r], split_min);
+    rk = atomicAdd(s_cnt + bk, 1u);
   }
-  const int64_t Tk = static_cast<int64_t>(best_T);
-  const int64_t kq = (Tk + 3) >> 2;
-  const uint16_t kmin = static_cast<uint16_t>(kq > 65535 ? 65535 : kq);
-  int lo = 0, hi = R;  // first index whose key < kmin
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (sorted_keys[mid] >= kmin) lo = mid + 1;
-    else hi = mid;
-  }
-  *n_split = lo;
+  __syncthreads();
+  for (int k = threadIdx.x; k < kOrdAll; k += blockDim.x)
+    if (s_cnt[k]) s_cnt[k] = atomicAdd(plan->ord + k, s_cnt[k]);
+  __syncthreads();
+  if (bk >= 0) order[s_cnt[bk] + rk] = r;
 }
 
 __global__ void k_nblocks(const int64_t* tok_off, int R, int B, int64_t* nb) {
@@ -651,12 +725,6 @@ cudaError_t device_setup(int dev) {
   e = cudaFuncSetAttribute(k_hash_staged<true, kWarps>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOneCta);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_hash_staged<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_bytes(16));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_hash_staged<false, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_bytes(12));
-  if (e != cudaSuccess) return e;
   uint64_t pw[kSplitTok + 1];
   uint64_t q = 1;
   for (int t = 0; t <= kSplitTok; ++t) {
@@ -688,52 +756,35 @@ int hash_seq_launch(pyg_ctx* c, const uint64_t* d_tok, int64_t n, uint64_t* d_ha
 }
 }  // namespace pyg_host
 
-// length sort (descending, for warp balance) + the persistent K1 launch
+// task order (descending length, for warp balance) + the K1 launch
 template <bool kGather>
 static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_off, int32_t R,
                        const int64_t* d_hash_off, uint64_t* d_hashes, GatherSrc g) {
-  size_t tmp = 0;
-  PYG_CUDA(cub::DeviceRadixSort::SortPairsDescending(
-      nullptr, tmp, static_cast<uint16_t*>(nullptr), static_cast<uint16_t*>(nullptr),
-      static_cast<int32_t*>(nullptr), static_cast<int32_t*>(nullptr), R, 0, 16, c->stream));
-  const size_t kb = (static_cast<size_t>(R) * 2 + 255) & ~size_t{255};
   const size_t vb = (static_cast<size_t>(R) * 4 + 255) & ~size_t{255};
   void* sp;
-  int rc = scratch(c, 2 * kb + 2 * vb + tmp + 768 + sizeof(SplitHist), &sp);
+  int rc = scratch(c, vb + 256 + sizeof(OrderPlan), &sp);
   if (rc) return rc;
   char* p = static_cast<char*>(sp);
-  auto* k_in = reinterpret_cast<uint16_t*>(p);
-  auto* k_out = reinterpret_cast<uint16_t*>(p + kb);
-  auto* v_in = reinterpret_cast<int32_t*>(p + 2 * kb);
-  auto* v_out = reinterpret_cast<int32_t*>(p + 2 * kb + vb);
-  void* d_tmp = p + 2 * kb + 2 * vb;
-  auto* ctr0 = reinterpret_cast<int*>(p + 2 * kb + 2 * vb + ((tmp + 255) & ~size_t{255}));
-  auto* hist = reinterpret_cast<SplitHist*>(ctr0 + 4);
-  // [0] task counter, [1] split requests, then the length histogram
-  PYG_CUDA(cudaMemsetAsync(ctr0, 0, 16 + sizeof(SplitHist), c->stream));
+  auto* v_out = reinterpret_cast<int32_t*>(p);
+  auto* ctr0 = reinterpret_cast<int*>(p + vb);
+  auto* plan = reinterpret_cast<OrderPlan*>(p + vb + 256);
+  // [0] task counter, [1] split requests; the order plan
+  PYG_CUDA(cudaMemsetAsync(ctr0, 0, 256 + sizeof(OrderPlan), c->stream));
   // split tasks: the fused-assembly loader and B % 16 != 0 keep one lane per request
   const int64_t split_min0 = (!kGather && c->B % kSplitTok == 0) ? c->split_min : 0;
-  k_len_keys<<<(R + 255) / 256, 256, 0, c->stream>>>(d_tok_off, R, k_in, v_in, split_min0,
-                                                     ctr0 + 1, hist);
+  const int nb = (R + kFillThreads - 1) / kFillThreads;
+  k_len_hist<<<nb, kFillThreads, 0, c->stream>>>(d_tok_off, R, split_min0, ctr0 + 1, plan);
   PYG_LAUNCHED(c);
-  PYG_CUDA(cub::DeviceRadixSort::SortPairsDescending(d_tmp, tmp, k_in, k_out, v_in, v_out, R, 0,
-                                                     16, c->stream));
+  k_order_plan<<<1, 1024, 0, c->stream>>>(plan, split_min0 < 0 ? 1 : 0, ctr0 + 1);
   PYG_LAUNCHED(c);
-  if (split_min0 < 0) {
-    k_split_count<<<1, 32, 0, c->stream>>>(k_out, R, hist, ctr0 + 1);
-    PYG_LAUNCHED(c);
-  }
+  k_order_fill<<<nb, kFillThreads, 0, c->stream>>>(d_tok_off, R, split_min0, plan, v_out);
+  PYG_LAUNCHED(c);
   PYG_CUDA(pyg_host::device_setup(c->device));
   const int n_sm = pyg_host::sm_count(c->device);
   const int cap = c->hash_ctas > 0 ? std::min(c->hash_ctas, n_sm) : n_sm;
   const int tasks_max = (R + 31) / 32 + (split_min0 ? R : 0);
   const bool persistent = c->hash_grid == 1;
-  // experiment knob: warps per K1 CTA (8, 12, 16) on the CSR path
-  static const int env_w = [] {
-    const char* e = getenv("PYG_K1_WARPS");
-    return e ? atoi(e) : kWarps;
-  }();
-  const int W = kGather ? kWarps : env_w;
+  constexpr int W = kWarps;
   const int grid = persistent ? std::max(1, std::min((tasks_max + W - 1) / W, cap))  // 1/SM
                               : std::max(1, (tasks_max + W - 1) / W);
   // grid mode 2: shared memory padded so that one K1 CTA fits per SM (the rest of the SM
@@ -743,16 +794,9 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   // the admission gate needs room for admission CTAs beside the paused K1 CTAs: honoured
   // with the persistent grid (<= one CTA per SM of 148) and grid mode 2 (one per SM) only
   const int32_t* gate = c->hash_grid != 0 ? c->hash_gate : nullptr;
-  if (W == 16)
-    k_hash_staged<kGather, 16><<<grid, 16 * 32, smem_bytes(16), c->stream>>>(
-        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate);
-  else if (W == 12)
-    k_hash_staged<kGather, 12><<<grid, 12 * 32, smem_bytes(12), c->stream>>>(
-        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate);
-  else
-    k_hash_staged<kGather, kWarps><<<grid, kWarps * 32, std::max(pad, smem_bytes(kWarps)),
-                                     c->stream>>>(
-        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate);
+  k_hash_staged<kGather, kWarps><<<grid, kWarps * 32, std::max(pad, smem_bytes(kWarps)),
+                                   c->stream>>>(d_src, d_tok_off, R, v_out, d_hash_off, d_hashes,
+                                                c->B, next, g, ctr0 + 1, gate);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
