@@ -681,6 +681,100 @@ def run_check(args, dev):
     print(json.dumps(report))
 
 
+def run_e2e_sharded(args, sh, bursts, k_first, E, ws, rank, dev, Sst, H, hctx):
+    """E more sharded steps through the public API from pinned host buffers, on every rank:
+    its burst's tokens, offsets, request metadata and the burst's registry pairs go
+    host->device (copy stream, one burst ahead), hash offsets + K1 and the sharded step run,
+    its requests' decisions / admissions / lookups come back.  Wall clock per rank between
+    barriers, max over ranks; value = all ranks' requests / that time."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    from paper_2604_25899_b200 import _lib
+    from paper_2604_25899_b200 import batch as PB
+    R = args.requests
+    r0, r1 = int(sh.plan.req_off[rank]), int(sh.plan.req_off[rank + 1])
+    host, dst = [], []
+    for i in range(E):
+        b = bursts[k_first + i]
+        rw, rm, _, _ = sh.reg[k_first + i]
+        dv = {"tokens": b.b.tokens[:b.b.n_tokens], "tok_off": b.b.tok_off, "res": b.b.res,
+              "group": b.b.group, "wf": b.b.wf, "role": b.b.role, "reg_wf": rw, "reg_mask": rm}
+        dst.append(dv)
+        host.append({k: v.cpu().pin_memory() for k, v in dv.items()})
+    res_h = [[torch.empty((r1 - r0, 3), dtype=torch.int64).pin_memory(),
+              torch.empty(R, dtype=torch.int32).pin_memory(),
+              torch.empty((R, 3), dtype=torch.int64).pin_memory()] for _ in range(2)]
+    h2d_bytes = sum(int(v.numel() * v.element_size()) for v in host[0].values())
+    d2h_bytes = sum(int(t.numel() * t.element_size()) for t in res_h[0])
+    cp = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+    up = {}
+
+    def upload(i):
+        with torch.cuda.stream(cp):
+            for key, v in host[i].items():
+                dst[i][key].copy_(v, non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(cp)
+            up[i] = e
+
+    def k1(i):
+        b = bursts[k_first + i]
+        H.wait_event(up.pop(i))
+        _lib.check(_lib._lib.pyg_hash_offsets_dev(hctx.h, ctypes.c_void_p(b.b.tok_off.data_ptr()),
+                                                  b.R, ctypes.c_void_p(b.b.hash_off.data_ptr()),
+                                                  None))
+        PB.hash_batch(hctx, b.b)
+        e = torch.cuda.Event()
+        e.record(H)
+        return e
+
+    fetched = [None, None]
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t0 = time.perf_counter()
+    upload(0)
+    if E > 1:
+        upload(1)
+    eh = k1(0)
+    for i in range(E):
+        k = k_first + i
+        Sst.wait_event(eh)
+        stp = sh.step(k, 1.0 + k)
+        es = torch.cuda.Event()
+        es.record(Sst)
+        if i + 1 < E:          # K1 of the next burst overlaps this step
+            eh = k1(i + 1)
+        if i + 2 < E:
+            upload(i + 2)
+        s_ = i % 2
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(es)
+            if fetched[s_] is not None:
+                fetched[s_].synchronize()
+            res_h[s_][0].copy_(stp.decisions[r0:r1], non_blocking=True)
+            res_h[s_][1].copy_(stp.out_adm[:R], non_blocking=True)
+            res_h[s_][2].copy_(stp.out_m3[:R], non_blocking=True)
+            ef = torch.cuda.Event()
+            ef.record(d2h)
+            fetched[s_] = ef
+    torch.cuda.synchronize(dev)
+    el = time.perf_counter() - t0
+    sh.ctx.check_device_error()
+    t = torch.tensor([el], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    el = float(t[0].item())
+    return {"value": R * ws * E / el, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes * ws,
+            "d2h_bytes_per_step": d2h_bytes * ws, "ms_per_step": 1000.0 * el / E, "steps": E,
+            "via": ("public API from pinned host buffers on every rank: per step each GPU's "
+                    "burst (tokens, offsets, request metadata, registry pairs) is copied "
+                    "host->device (copy stream, one burst ahead), hash offsets + K1 + the "
+                    "sharded step run, its requests' decisions / admissions / lookups are "
+                    "copied back; wall clock between barriers, max over ranks; byte counts "
+                    "summed over the GPUs")}
+
+
 def run_sharded(args):
     """N > 1 (one process per GPU): the cluster's replicas split by model over the GPUs
     (steady_shard.py), every rank brings its own burst of args.requests per step (weak
@@ -709,8 +803,9 @@ def run_sharded(args):
     n_fill = S.apply_warm_fill_gpu(ctx, warm, loc_off, placed[off[lo]:off[hi]], args.block, dev)
     S.apply_ops_gpu(ctx, warm, ops, rep_base=lo)
     del warm
+    E = 0 if (args.no_e2e or args.profile) else args.e2e_steps
     bursts = []
-    for k in range(W_ + K):
+    for k in range(W_ + K + E):
         tr = S.make_burst(k * ws + rank, args.requests, args.seed, dev, args.workload,
                           args.models)
         bursts.append(S.upload_burst(tr, args.block, dev, k * ws + rank))
@@ -782,6 +877,7 @@ def run_sharded(args):
     ctx.check_device_error()
     st = ctx.counters(reset=True)
     ms = t0.elapsed_time(t1)
+    e2e = run_e2e_sharded(args, sh, bursts, W_ + K, E, ws, rank, dev, Sst, H, hctx) if E else None
     hash_ms = sum(a.elapsed_time(b) for a, b in hevs) / K
     t = torch.tensor([ms, hash_ms], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -822,7 +918,7 @@ def run_sharded(args):
                          "algorithmic_bytes_per_launch": int(hash_bytes),
                          "avg_launch_ms": hash_ms, "max_over_ranks_launch_ms": hash_ms_max},
             "phase_ms_rank0": phase_ms, "hash_ms_rank0": hash_ms,
-            "clocks": clk, "gpu_launches": int(cnt[3].item()), "e2e": None,
+            "clocks": clk, "gpu_launches": int(cnt[3].item()), "e2e": e2e,
             "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
