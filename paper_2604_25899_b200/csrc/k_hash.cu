@@ -784,12 +784,11 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   const int cap = c->hash_ctas > 0 ? std::min(c->hash_ctas, n_sm) : n_sm;
   const int tasks_max = (R + 31) / 32 + (split_min0 ? R : 0);
   const bool persistent = c->hash_grid == 1;
-  constexpr int W = kWarps;
-  const int grid = persistent ? std::max(1, std::min((tasks_max + W - 1) / W, cap))  // 1/SM
-                              : std::max(1, (tasks_max + W - 1) / W);
+  const int per = (tasks_max + kWarps - 1) / kWarps;  // CTAs of one task per warp
+  const int grid = persistent ? std::max(1, std::min(per, cap)) : std::max(1, per);  // 1/SM
   // grid mode 2: shared memory padded so that one K1 CTA fits per SM (the rest of the SM
-  // stays free for the step's kernels); the launch sizes are set in device_setup
-  const int pad = c->hash_grid == 2 && W == kWarps ? kSmemOneCta : 0;
+  // stays free for the step's kernels; device_setup allows the padded size)
+  const int pad = c->hash_grid == 2 ? kSmemOneCta : 0;
   int* next = persistent ? ctr0 : nullptr;
   // the admission gate needs room for admission CTAs beside the paused K1 CTAs: honoured
   // with the persistent grid (<= one CTA per SM of 148) and grid mode 2 (one per SM) only
