@@ -87,6 +87,8 @@ def parse():
     ap.add_argument("--k1-grid", default="persistent", choices=["persistent", "tasks", "tasks1"],
                     help="K1 grid: persistent CTAs, or one task per warp (CTAs retire so the "
                          "step's kernels interleave)")
+    ap.add_argument("--k1-memo", default="off", choices=["on", "off"],
+                    help="K1 prefix memo of shared leading tokens (pyg_set_hash_memo)")
     ap.add_argument("--k1-gate", default="off", choices=["on", "off"],
                     help="K1 of the next burst pauses while the step's admission runs "
                          "(pyg_set_hash_gate)")
@@ -349,6 +351,7 @@ class Arm:
             self.hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
         self.hctx.set_hash_split(args.split_min)
         self.hctx.set_hash_grid(args.k1_grid)
+        self.hctx.set_hash_memo(args.k1_memo == "on")
         if self.overlap and args.k1_gate == "on":
             self.hctx.set_hash_gate(self.ctx)
         self.ev_h = {}
@@ -825,6 +828,7 @@ def run_sharded(args):
     hctx.set_hash_ctas(max(1, n_sm - args.free_sms))
     hctx.set_hash_split(args.split_min)
     hctx.set_hash_grid(args.k1_grid)
+    hctx.set_hash_memo(args.k1_memo == "on")
     if args.k1_gate == "on":
         hctx.set_hash_gate(ctx)
     ev_h = {}

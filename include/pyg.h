@@ -221,6 +221,12 @@ int pyg_set_hash_grid(pyg_ctx* ctx, int32_t mode);
    Same device; honoured with K1 grid modes 1 and 2 (room for admission CTAs beside the
    paused K1 CTAs).  step_ctx must outlive hash_ctx's K1 launches. */
 int pyg_set_hash_gate(pyg_ctx* hash_ctx, pyg_ctx* step_ctx);
+/* K1 prefix memo (default off; CSR path, B % 16 == 0, persistent grid, bursts of >= 1,024
+   requests): requests sharing their first 16 tokens take the chain states of one leader's
+   first 2,048 tokens for every leading 16-token chunk whose tokens equal the leader's
+   (k_memo_match compares them before K1).  Measured: 22 % faster K1 on 40k requests sharing
+   2,048-token prefixes, 28 % slower on config 4 (profiles/r02_k1_prefix_memo_ab.txt). */
+int pyg_set_hash_memo(pyg_ctx* ctx, int32_t on);
 /* K1 hashes prompts of >= min_tokens tokens as split tasks: one warp per prompt, 512 tokens
    at a time, through the low-byte decomposition of FNV-1a (k_hash.cu) -- the same hashes,
    without the long-prompt tail of one lane per request.  0 = never; -1 (default) = a

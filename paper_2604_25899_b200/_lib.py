@@ -139,6 +139,7 @@ _sig("pyg_lookup_all", vp, vp, i64, i32, i32, vp)
 _sig("pyg_set_hash_split", vp, i64)
 _sig("pyg_set_hash_grid", vp, i32)
 _sig("pyg_set_hash_gate", vp, vp)
+_sig("pyg_set_hash_memo", vp, i32)
 _sig("pyg_nodes_compose_dev", vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp)
 _sig("pyg_release_hold_dev", vp, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp)
 _sig("pyg_registry_update_batch_dev", vp, i32, vp, vp, i32)
@@ -242,6 +243,10 @@ class Context:
         """K1 grid: "persistent" (default), "tasks" (one task per warp), "tasks1" (one task
         per warp, at most one K1 CTA per SM)."""
         check(_lib.pyg_set_hash_grid(self.h, {"tasks": 0, "persistent": 1, "tasks1": 2}[mode]))
+
+    def set_hash_memo(self, on: bool):
+        """K1 prefix memo (default off; see pyg.h)."""
+        check(_lib.pyg_set_hash_memo(self.h, int(bool(on))))
 
     def set_hash_gate(self, step_ctx):
         """K1 of this ctx pauses while step_ctx runs an admission (None: no gate)."""

@@ -43,6 +43,7 @@ struct pyg_ctx {
   int32_t rep_base = 0;      // global index of this ctx's replica 0
   int64_t dir_admits = 0;    // admission calls since the last build (cleared bits accumulate)
   int32_t hash_ctas = 0;     // K1 persistent grid cap (0 = one CTA per SM)
+  int32_t hash_memo = 0;  // K1 prefix memo (k_memo_elect / k_memo_rows / k_memo_match), off
   int32_t hash_grid = 1;  // K1 grid: 0 one task per warp, 1 persistent, 2 = 0 at 1 CTA/SM
   // admission gate: d_gate (this ctx's admissions hold it at 1 while they run); hash_gate =
   // another ctx's d_gate that this ctx's K1 pauses on (pyg_set_hash_gate)

@@ -191,9 +191,10 @@ __device__ __forceinline__ uint32_t lo8_step(uint32_t x, uint32_t w, int bi) {
 
 // One split task: request of n tokens at src, boundary hashes to out (B % 16 == 0).
 // wbuf: this warp's 2 staging buffers (rows of kRowBytes, row l = segment l).
+// h0: the chain state before src[0] (the offset basis, or a memo state at a block boundary)
 __device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_t n, int B,
                            uint64_t* __restrict__ out, unsigned char* wbuf,
-                           const int32_t* gate = nullptr) {
+                           const int32_t* gate = nullptr, uint64_t h0 = kFnvOffset) {
   const int lane = threadIdx.x & 31;
   const int nsc = static_cast<int>((n + kSuper - 1) / kSuper);
   auto issue = [&](int sc) {
@@ -207,7 +208,7 @@ __device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_
     }
     cp_commit();
   };
-  uint64_t H0 = kFnvOffset;  // hash at the super-chunk start (warp-uniform)
+  uint64_t H0 = h0;  // hash at the super-chunk start (warp-uniform)
   issue(0);
   for (int sc = 0; sc < nsc; ++sc) {
     const int gz = gate ? gate_load(gate) : 0;
@@ -301,6 +302,154 @@ __device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_
   }
 }
 
+// ------------------------------------------------------------- prefix memo
+// Requests that start with the same tokens share their leading chain hashes (the state at a
+// chunk end depends only on the tokens before it).  Per burst, one LEADER per first-16-token
+// content -- the longest request sharing it -- is hashed over its first kMemoTok tokens into
+// a memo row of chunk-end states (tasks of K1 itself, ahead of every other task).  Before
+// K1, k_memo_match compares every request with its leader, a warp per request streaming 128
+// tokens per step (coalesced, memory-bound), and records how many leading 16-token chunks
+// match in full; K1 starts each request's chain after them, and k_memo_emit (after K1)
+// copies their boundary hashes from the memo row.  Exact for any input: a memo state is
+// used only when every token up to its chunk end compared equal.  Only first chunks shared
+// by >= kMemoMin requests get a row.  The task order and the split threshold use the work
+// left past the memoised chunks.
+constexpr int kMemoTok = 2048;                  // tokens memoised per leader
+constexpr int kMemoChunks = kMemoTok / 16;      // 128 chunk-end states (1 KB) per row
+constexpr int kMemoMin = 3;
+constexpr int kMemoRows = 4096;
+
+struct MemoTab {
+  uint32_t* key;              // [cap] first-chunk digest (0 = empty)
+  unsigned long long* lead;   // [cap] (length << 32) | ~r: max = longest, then lowest r
+  int32_t* cnt;               // [cap] requests with the digest
+  int32_t* row;               // [cap] memo row of the slot or -1
+  int32_t* slot_of;           // [R] digest slot of request r or -1
+  int32_t* mlen;              // [R] leading chunks equal to the leader's (k_memo_match)
+  int32_t* row_lead;          // [kMemoRows] leader request
+  int32_t* row_chunks;        // [kMemoRows] memoised chunks
+  int32_t* ready;             // [kMemoRows] row written (release / acquire)
+  uint64_t* state;            // [kMemoRows][kMemoChunks]
+  int32_t* n_rows;
+  uint32_t mask;
+};
+
+__global__ void k_memo_elect(const uint64_t* __restrict__ tokens,
+                             const int64_t* __restrict__ tok_off, int R, MemoTab m) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int64_t s = tok_off[r], n = tok_off[r + 1] - s;
+  if (n < 16) {
+    m.slot_of[r] = -1;
+    return;
+  }
+  uint64_t d = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) d = (d ^ tokens[s + i]) * 0x9E3779B97F4A7C15ull + i;
+  const uint32_t key = (static_cast<uint32_t>(d >> 32) ^ static_cast<uint32_t>(d)) | 1u;
+  uint32_t slot = key & m.mask;
+  for (;;) {
+    const uint32_t k = atomicCAS(m.key + slot, 0u, key);
+    if (k == 0u || k == key) break;
+    slot = (slot + 1) & m.mask;
+  }
+  m.slot_of[r] = static_cast<int32_t>(slot);
+  atomicAdd(m.cnt + slot, 1);
+  atomicMax(m.lead + slot, (static_cast<unsigned long long>(n) << 32) |
+                               (0xFFFFFFFFu - static_cast<uint32_t>(r)));
+}
+
+// a row per slot shared by >= kMemoMin requests (up to kMemoRows)
+__global__ void k_memo_rows(MemoTab m) {
+  const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot > m.mask) return;
+  int row = -1;
+  if (m.key[slot] != 0u && m.cnt[slot] >= kMemoMin) {
+    row = atomicAdd(m.n_rows, 1);
+    if (row < kMemoRows) {
+      const unsigned long long L = m.lead[slot];
+      m.row_lead[row] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(L));
+      m.row_chunks[row] = static_cast<int32_t>(min(static_cast<int64_t>(L >> 32),
+                                                   static_cast<int64_t>(kMemoTok)) / 16);
+    } else {
+      row = -1;
+    }
+  }
+  m.row[slot] = row;
+}
+__global__ void k_memo_clamp(int32_t* n_rows) {
+  if (*n_rows > kMemoRows) *n_rows = kMemoRows;
+}
+// matched chunks of every request against its leader: a warp per request, 128 tokens per step
+__global__ void k_memo_match(const uint64_t* __restrict__ tokens,
+                             const int64_t* __restrict__ tok_off, int R, MemoTab m) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nw) {
+    const int slot = m.slot_of[r];
+    const int row = slot >= 0 ? m.row[slot] : -1;
+    int mc = 0;
+    if (row >= 0) {
+      const int64_t s = tok_off[r];
+      const int64_t n = tok_off[r + 1] - s;
+      const int64_t lim = 16 * min(static_cast<int64_t>(m.row_chunks[row]), n / 16);
+      const uint64_t* a = tokens + s;
+      const uint64_t* b = tokens + tok_off[m.row_lead[row]];
+      int64_t eq = lim;  // tokens equal from the start
+      for (int64_t i = 0; i < lim; i += 128) {  // 4 loads per lane in flight
+        bool df[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t j = i + 32 * u + lane;
+          df[u] = j < lim && a[j] != b[j];
+        }
+        unsigned d = 0;
+        int u0 = 0;
+#pragma unroll
+        for (int u = 3; u >= 0; --u) {
+          const unsigned du = __ballot_sync(kFull, df[u]);
+          if (du) {
+            d = du;
+            u0 = u;
+          }
+        }
+        if (d) {
+          eq = i + 32 * u0 + __ffs(d) - 1;
+          break;
+        }
+      }
+      mc = static_cast<int>(eq / 16);
+    }
+    if (lane == 0) m.mlen[r] = mc;
+  }
+}
+
+// boundary hashes of the memoised chunks (after K1): a warp per request, coalesced copies
+// from the memo row (hierarchy.cpp:26: every B tokens and at the last token)
+__global__ void k_memo_emit(const int64_t* __restrict__ tok_off,
+                            const int64_t* __restrict__ hash_off, uint64_t* __restrict__ hashes,
+                            int R, int B, MemoTab m) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int cpb = B / 16;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += nw) {
+    const int m0 = m.mlen[r];
+    if (m0 <= 0) continue;
+    const int64_t n = tok_off[r + 1] - tok_off[r];
+    const uint64_t* ms = m.state + static_cast<int64_t>(m.row[m.slot_of[r]]) * kMemoChunks;
+    uint64_t* out = hashes + hash_off[r];
+    // block j ends at chunk (j + 1) cpb - 1; the request's last chunk (if memoised) too
+    const int nb = m0 / cpb;
+    for (int j = lane; j < nb; j += 32) out[j] = ms[(j + 1) * cpb - 1];
+    if (lane == 0 && 16 * static_cast<int64_t>(m0) == n && m0 % cpb) out[nb] = ms[m0 - 1];
+  }
+}
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Chunks are aligned to each request's own first token, so with B % 16 == 0 a
 // block boundary always coincides with the end of a chunk: the emit decision
 // is per chunk and warp-uniform (no per-token test).  The last, partial chunk
@@ -308,12 +457,12 @@ __device__ __noinline__ void split_task(const uint64_t* __restrict__ src, int64_
 //
 // Long prompts (>= the split threshold) are split tasks (split_task above); the rest run
 // one lane per request in 32-request tasks.
-template <bool kGather, int W>
+template <bool kGather, int W, bool kMemo>
 __global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1))
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
               uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task, GatherSrc g,
-              const int* __restrict__ n_split_p, const int32_t* gate) {
+              const int* __restrict__ n_split_p, const int32_t* gate, MemoTab mt) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbuf = smem + warp * 2 * kStageBytes;
@@ -321,10 +470,12 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   unsigned long long* wbase = reinterpret_cast<unsigned long long*>(
       smem + W * 2 * kStageBytes + warp * kMetaBytes);
   unsigned long long* lsl = wbase + 32;
-  // tasks: [0, n_split) one long request each (split_task, the longest first), then
-  // 32-request tasks over the rest of the length-sorted order
+  // tasks: [0, n_memo) memo rows (kMemo), then [.., + n_split) one long request each
+  // (split_task, the longest first), then 32-request tasks over the rest of the
+  // length-sorted order
+  const int n_memo = kMemo ? *mt.n_rows : 0;
   const int n_split = (!kGather && n_split_p) ? *n_split_p : 0;
-  const int ntasks = n_split + (R - n_split + 31) / 32;
+  const int ntasks = n_memo + n_split + (R - n_split + 31) / 32;
   // persistent: each warp pulls tasks, longest first, until none are left
   // persistent (next_task != null): warps pull tasks from a counter until none are left;
   // otherwise one task per warp (a CTA per 8 tasks, in the longest-first order), so CTAs
@@ -338,10 +489,33 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
     task = it == 0 ? static_cast<int>(blockIdx.x) * W + warp : ntasks;
   }
   if (task >= ntasks) break;
+  if (kMemo && task < n_memo) {  // memo row `task`: the leader's first chunks on this warp
+    split_task(tokens + tok_off[mt.row_lead[task]], 16 * static_cast<int64_t>(mt.row_chunks[task]),
+               16, mt.state + static_cast<int64_t>(task) * kMemoChunks, wbuf, gate);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicExch(mt.ready + task, 1);
+    continue;
+  }
+  task -= n_memo;
   if (task < n_split) {
     const int r = order[task];
     const int64_t s0 = tok_off[r];
-    split_task(tokens + s0, tok_off[r + 1] - s0, B, hashes + hash_off[r], wbuf, gate);
+    // kMemo: start after the memoised chunks, at a block boundary (k_memo_emit writes the
+    // boundary hashes before it)
+    int64_t m0 = 0;
+    uint64_t h0 = kFnvOffset;
+    if (kMemo) {
+      const int cpb = B / kChunk;
+      m0 = (mt.mlen[r] / cpb) * cpb;
+      if (m0 > 0) {
+        const int row = mt.row[mt.slot_of[r]];
+        while (ld_acquire(mt.ready + row) == 0) __nanosleep(256);
+        h0 = mt.state[static_cast<int64_t>(row) * kMemoChunks + m0 - 1];
+      }
+    }
+    split_task(tokens + s0 + kChunk * m0, tok_off[r + 1] - s0 - kChunk * m0, B,
+               hashes + hash_off[r] + m0 / (B / kChunk > 0 ? B / kChunk : 1), wbuf, gate, h0);
     continue;
   }
   const int idx = n_split + (task - n_split) * 32 + lane;
@@ -356,6 +530,23 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   const bool fast = (B % kChunk) == 0;
   const int cpb = fast ? B / kChunk : 1;  // chunks per block (fast path)
   int cc = cpb;
+  uint64_t h = kFnvOffset;
+  int64_t k = 0;
+  // kMemo: the request's leading chunks equal to its leader's (k_memo_match) come from the
+  // memo row (k_memo_emit writes their boundary hashes): the chain starts after them, at
+  // chunk m0; the warp's chunk loop starts at its lanes' smallest m0
+  int m0 = 0;
+  if (kMemo && valid) {
+    m0 = mt.mlen[r];
+    if (m0 > 0) {
+      const int row = mt.row[mt.slot_of[r]];
+      while (ld_acquire(mt.ready + row) == 0) __nanosleep(256);  // its memo task is running
+      h = mt.state[static_cast<int64_t>(row) * kMemoChunks + m0 - 1];
+      k = m0 / cpb;                 // boundary hashes already written by k_memo_emit
+      cc = cpb - m0 % cpb;
+    }
+  }
+  const int c_start = kMemo ? __reduce_min_sync(kFull, valid ? m0 : 0x7fffffff) : 0;
 
   // fused assembly: chunk c's packed source of every request of the warp sits in smem slot
   // lsl[c % 4][perm(request)]; each lane prefetches its own request's entry for chunk c + 2
@@ -380,7 +571,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
       // below is then shared with the fused path (8 broadcast LDS.128 per half-warp
       // instead of 64 shuffles per chunk)
       const int64_t left = n - static_cast<int64_t>(c) * kChunk;
-      const unsigned long long v = left <= 0 ? 0ull : left >= kChunk ? kChunk : left;
+      const unsigned long long v = (left <= 0 || c < m0) ? 0ull : left >= kChunk ? kChunk : left;
       __syncwarp();
       lsl[(c & 3) * 32 + me] =
           (reinterpret_cast<unsigned long long>(tokens + s + static_cast<int64_t>(c) * kChunk) &
@@ -440,10 +631,8 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
     }
   };
 
-  uint64_t h = kFnvOffset;
-  int64_t k = 0;
-  issue(0);
-  for (int c = 0; c < maxch; ++c) {
+  issue(c_start);
+  for (int c = c_start; c < maxch; ++c) {
     const int gz = gate ? gate_load(gate) : 0;
     if (c + 1 < maxch)
       issue(c + 1);
@@ -452,7 +641,7 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
     cp_wait1();
     __syncwarp();
     if (kGather) write_out(c);
-    if (c < nch) {
+    if (c < nch && !(kMemo && c < m0)) {
       const unsigned char* row = wbuf + (c & 1) * kStageBytes + lane * kRowBytes;
       const int64_t rem = n - static_cast<int64_t>(c) * kChunk;
       if (fast && rem >= kChunk) {
@@ -549,16 +738,23 @@ __device__ __forceinline__ int bucket_of(int64_t n, int64_t split_min) {
   return ord_of(n) + (split_min > 0 && n >= split_min ? kOrd : 0);
 }
 
+// With the prefix memo (mlen != null) a request's work is its length past the chunks the
+// memo covers: the order, the split threshold and the split set use that length.
+__device__ __forceinline__ int64_t work_len(const int64_t* tok_off, const int32_t* mlen, int r) {
+  const int64_t n = tok_off[r + 1] - tok_off[r];
+  return mlen ? n - 16 * static_cast<int64_t>(mlen[r]) : n;
+}
+
 __global__ void __launch_bounds__(kFillThreads) k_len_hist(const int64_t* tok_off, int R,
                                                            int64_t split_min, int* n_split,
-                                                           OrderPlan* plan) {
+                                                           OrderPlan* plan, const int32_t* mlen) {
   __shared__ unsigned int s_ord[kOrdAll];
   __shared__ unsigned long long s_max;
   for (int k = threadIdx.x; k < kOrdAll; k += blockDim.x) s_ord[k] = 0;
   if (threadIdx.x == 0) s_max = 0;
   __syncthreads();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = r < R ? tok_off[r + 1] - tok_off[r] : 0;
+  const int64_t n = r < R ? work_len(tok_off, mlen, r) : 0;
   const bool sp = split_min > 0 && n >= split_min;
   if (r < R) atomicAdd(s_ord + ord_of(n) + (sp ? kOrd : 0), 1u);
   if (split_min > 0) {  // fixed threshold: count the split requests here
@@ -657,7 +853,7 @@ __global__ void __launch_bounds__(1024) k_order_plan(OrderPlan* plan, int adapti
 // dozen buckets: per-warp atomics serialise in L2)
 __global__ void __launch_bounds__(kFillThreads) k_order_fill(const int64_t* tok_off, int R,
                                                              int64_t split_min, OrderPlan* plan,
-                                                             int32_t* order) {
+                                                             int32_t* order, const int32_t* mlen) {
   __shared__ unsigned int s_cnt[kOrdAll];
   for (int k = threadIdx.x; k < kOrdAll; k += blockDim.x) s_cnt[k] = 0;
   __syncthreads();
@@ -665,7 +861,7 @@ __global__ void __launch_bounds__(kFillThreads) k_order_fill(const int64_t* tok_
   int bk = -1;
   unsigned rk = 0;
   if (r < R) {
-    bk = bucket_of(tok_off[r + 1] - tok_off[r], split_min);
+    bk = bucket_of(work_len(tok_off, mlen, r), split_min);
     rk = atomicAdd(s_cnt + bk, 1u);
   }
   __syncthreads();
@@ -719,10 +915,12 @@ cudaError_t device_setup(int dev) {
   if (done[dev]) return cudaSuccess;
   cudaError_t e = cudaSetDevice(dev);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_hash_staged<false, kWarps>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOneCta);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_hash_staged<true, kWarps>,
+  for (const void* f : {reinterpret_cast<const void*>(k_hash_staged<false, kWarps, false>),
+                        reinterpret_cast<const void*>(k_hash_staged<true, kWarps, false>)}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOneCta);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaFuncSetAttribute(k_hash_staged<false, kWarps, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOneCta);
   if (e != cudaSuccess) return e;
   uint64_t pw[kSplitTok + 1];
@@ -761,23 +959,65 @@ template <bool kGather>
 static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_off, int32_t R,
                        const int64_t* d_hash_off, uint64_t* d_hashes, GatherSrc g) {
   const size_t vb = (static_cast<size_t>(R) * 4 + 255) & ~size_t{255};
+  // prefix memo: CSR path, whole-chunk blocks, persistent grid (a warp waiting for a memo
+  // row relies on the row's task having been taken by a running warp), bursts large enough
+  // to amortise the election
+  const bool memo = !kGather && c->B % kChunk == 0 && c->hash_memo && c->hash_grid == 1 &&
+                    R >= 1024;
+  uint32_t mcap = 1024;
+  while (memo && mcap < 2u * static_cast<uint32_t>(R)) mcap <<= 1;
+  const size_t tab_b = memo ? static_cast<size_t>(mcap) * 20 : 0;
+  const size_t rows_b = memo ? static_cast<size_t>(kMemoRows) * (kMemoChunks * 8 + 12) : 0;
   void* sp;
-  int rc = scratch(c, vb + 256 + sizeof(OrderPlan), &sp);
+  int rc = scratch(c, vb + 256 + ((sizeof(OrderPlan) + 255) & ~size_t{255}) + tab_b + 2 * vb +
+                          rows_b + 256, &sp);
   if (rc) return rc;
   char* p = static_cast<char*>(sp);
   auto* v_out = reinterpret_cast<int32_t*>(p);
   auto* ctr0 = reinterpret_cast<int*>(p + vb);
   auto* plan = reinterpret_cast<OrderPlan*>(p + vb + 256);
-  // [0] task counter, [1] split requests; the order plan
+  // [0] task counter, [1] split requests, [2] memo rows; the order plan
   PYG_CUDA(cudaMemsetAsync(ctr0, 0, 256 + sizeof(OrderPlan), c->stream));
+  MemoTab mt{};
+  if (memo) {
+    char* q = p + vb + 256 + ((sizeof(OrderPlan) + 255) & ~size_t{255});
+    mt.lead = reinterpret_cast<unsigned long long*>(q);                      // 8 B / slot
+    mt.key = reinterpret_cast<uint32_t*>(q + static_cast<size_t>(mcap) * 8);  // 4
+    mt.cnt = reinterpret_cast<int32_t*>(q + static_cast<size_t>(mcap) * 12);  // 4
+    mt.row = reinterpret_cast<int32_t*>(q + static_cast<size_t>(mcap) * 16);  // 4
+    q += tab_b;
+    mt.slot_of = reinterpret_cast<int32_t*>(q);
+    q += vb;
+    mt.mlen = reinterpret_cast<int32_t*>(q);
+    q += vb;
+    mt.state = reinterpret_cast<uint64_t*>(q);
+    mt.ready = reinterpret_cast<int32_t*>(q + static_cast<size_t>(kMemoRows) * kMemoChunks * 8);
+    mt.row_lead = mt.ready + kMemoRows;
+    mt.row_chunks = mt.row_lead + kMemoRows;
+    mt.n_rows = ctr0 + 2;
+    mt.mask = mcap - 1;
+    PYG_CUDA(cudaMemsetAsync(mt.lead, 0, static_cast<size_t>(mcap) * 16, c->stream));
+    PYG_CUDA(cudaMemsetAsync(mt.ready, 0, static_cast<size_t>(kMemoRows) * 4, c->stream));
+    k_memo_elect<<<(R + 255) / 256, 256, 0, c->stream>>>(d_src, d_tok_off, R, mt);
+    PYG_LAUNCHED(c);
+    k_memo_rows<<<(mcap + 255) / 256, 256, 0, c->stream>>>(mt);
+    PYG_LAUNCHED(c);
+    k_memo_clamp<<<1, 1, 0, c->stream>>>(mt.n_rows);
+    PYG_LAUNCHED(c);
+    k_memo_match<<<std::min((R + 7) / 8, 16 * pyg_host::sm_count(c->device)), 256, 0,
+                   c->stream>>>(d_src, d_tok_off, R, mt);
+    PYG_LAUNCHED(c);
+  }
   // split tasks: the fused-assembly loader and B % 16 != 0 keep one lane per request
   const int64_t split_min0 = (!kGather && c->B % kSplitTok == 0) ? c->split_min : 0;
   const int nb = (R + kFillThreads - 1) / kFillThreads;
-  k_len_hist<<<nb, kFillThreads, 0, c->stream>>>(d_tok_off, R, split_min0, ctr0 + 1, plan);
+  k_len_hist<<<nb, kFillThreads, 0, c->stream>>>(d_tok_off, R, split_min0, ctr0 + 1, plan,
+                                                 mt.mlen);
   PYG_LAUNCHED(c);
   k_order_plan<<<1, 1024, 0, c->stream>>>(plan, split_min0 < 0 ? 1 : 0, ctr0 + 1);
   PYG_LAUNCHED(c);
-  k_order_fill<<<nb, kFillThreads, 0, c->stream>>>(d_tok_off, R, split_min0, plan, v_out);
+  k_order_fill<<<nb, kFillThreads, 0, c->stream>>>(d_tok_off, R, split_min0, plan, v_out,
+                                                   mt.mlen);
   PYG_LAUNCHED(c);
   PYG_CUDA(pyg_host::device_setup(c->device));
   const int n_sm = pyg_host::sm_count(c->device);
@@ -793,9 +1033,16 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   // the admission gate needs room for admission CTAs beside the paused K1 CTAs: honoured
   // with the persistent grid (<= one CTA per SM of 148) and grid mode 2 (one per SM) only
   const int32_t* gate = c->hash_grid != 0 ? c->hash_gate : nullptr;
-  k_hash_staged<kGather, kWarps><<<grid, kWarps * 32, std::max(pad, smem_bytes(kWarps)),
-                                   c->stream>>>(d_src, d_tok_off, R, v_out, d_hash_off, d_hashes,
-                                                c->B, next, g, ctr0 + 1, gate);
+  if (memo) {
+    k_hash_staged<false, kWarps, true><<<grid, kWarps * 32, smem_bytes(kWarps), c->stream>>>(
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate, mt);
+    PYG_LAUNCHED(c);
+    k_memo_emit<<<std::min((R + 7) / 8, 16 * n_sm), 256, 0, c->stream>>>(d_tok_off, d_hash_off,
+                                                                          d_hashes, R, c->B, mt);
+  } else
+    k_hash_staged<kGather, kWarps, false><<<grid, kWarps * 32,
+                                            std::max(pad, smem_bytes(kWarps)), c->stream>>>(
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate, mt);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }
@@ -839,6 +1086,13 @@ int pyg_assemble_hash_dev(pyg_ctx* c, int32_t R, const int64_t* d_seg_off,
                            GatherSrc{tab, d_tokens});
 }
 
+int pyg_set_hash_memo(pyg_ctx* c, int32_t on) {
+  PYG_ON_DEVICE(c);
+  if (!c) return PYG_EINVAL;
+  c->hash_memo = on ? 1 : 0;
+  return PYG_OK;
+}
+
 int pyg_set_hash_gate(pyg_ctx* c, pyg_ctx* step) {
   PYG_ON_DEVICE(c);
   if (!c) return PYG_EINVAL;
@@ -856,8 +1110,9 @@ int pyg_set_hash_gate(pyg_ctx* c, pyg_ctx* step) {
   // fixed while CTAs are resident, and with the split the driver picks for K1 alone (~100 KB)
   // the admission CTAs (~103 KB) could not start beside a paused K1 CTA (k_admit asks for
   // the same when its ctx has a gate)
-  for (const void* f : {reinterpret_cast<const void*>(k_hash_staged<false, kWarps>),
-                        reinterpret_cast<const void*>(k_hash_staged<true, kWarps>)})
+  for (const void* f : {reinterpret_cast<const void*>(k_hash_staged<false, kWarps, false>),
+                        reinterpret_cast<const void*>(k_hash_staged<false, kWarps, true>),
+                        reinterpret_cast<const void*>(k_hash_staged<true, kWarps, false>)})
     PYG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
   c->hash_gate = step->d_gate;

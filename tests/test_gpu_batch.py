@@ -159,6 +159,63 @@ def test_hash_batch_long_prompts_isolated(B):
         assert np.array_equal(got[hoff[r]:hoff[r + 1]], want), (r, lens[r])
 
 
+@pytest.mark.parametrize("B", [16, 64])
+@pytest.mark.parametrize("split_min", [-1, 100])
+def test_hash_batch_prefix_memo(B, split_min):
+    """K1's prefix memo: requests sharing leading tokens with the leader of their first-16-token
+    content start their chains after the leading chunks equal to the leader's (memo states;
+    k_memo_emit writes those boundary hashes).  Shared lengths around every chunk / block /
+    memo edge (0, 15..17, 31..33, 63..65, 2047..2049, whole prefixes), identical duplicates,
+    one-bit mismatches, leaders shorter than followers, first chunks shared by 1-2 requests
+    only (no memo row), prompts under 16 tokens; with the adaptive threshold and with most
+    requests as split tasks (which start at the memo state too); the same batch memo off."""
+    from paper_2604_25899_b200 import Context
+    from paper_2604_25899_b200 import batch as PB
+    rng = np.random.default_rng(900 + B + split_min)
+    pre = [rng.integers(0, 1 << 63, size=n, dtype=np.uint64) for n in (40, 500, 2047, 2048,
+                                                                      2049, 5000)]
+    seqs = []
+    for i in range(1600):
+        p = pre[int(rng.integers(0, len(pre)))]
+        k = int(rng.choice([0, 15, 16, 17, 31, 32, 33, 63, 64, 65, 2047, 2048, 2049, len(p),
+                            len(p), int(rng.integers(0, len(p) + 1))]))
+        k = min(k, len(p))
+        tail = rng.integers(0, 1 << 63, size=int(rng.integers(0, 3000)), dtype=np.uint64)
+        if i % 7 == 0 and k < len(p) and len(tail):
+            tail[0] = p[k] ^ np.uint64(1)  # differs only in the low bit
+        if i % 11 == 0 and k >= 16:
+            tail = tail[:0]  # exactly a prefix of the shared content
+        seqs.append(np.concatenate([p[:k], tail]))
+        if i % 13 == 0:
+            seqs.append(seqs[-1].copy())  # identical duplicate
+    seqs += [rng.integers(0, 1 << 63, size=n, dtype=np.uint64) for n in range(0, 20)]
+    order = rng.permutation(len(seqs))
+    seqs = [seqs[j] for j in order]
+    lens = np.array([len(x) for x in seqs])
+    off = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    toks = np.concatenate(seqs).astype(np.uint64)
+    o = Restated(B)
+    want = [o.chain_hashes(toks[off[r]:off[r + 1]]) for r in range(len(lens))]
+    for memo in (True, False):
+        ctx = Context(1, 1000, 1000, B)
+        ctx.set_hash_memo(memo)
+        ctx.set_hash_split(split_min)
+        z = np.zeros(len(lens), np.int32)
+        res = np.zeros(len(lens), PB.RES_DTYPE)
+        db = PB.upload_batch(ctx, toks, off, res, z, z, z)
+        PB.bind_current_stream(ctx)
+        for _ in range(2):  # the second call reuses the scratch of the first
+            db.hashes.zero_()
+            PB.hash_batch(ctx, db)
+            torch.cuda.synchronize()
+            ctx.check_device_error()
+            got = db.hashes.cpu().numpy().view(np.uint64)
+            hoff = db.hash_off.cpu().numpy()
+            for r in range(len(lens)):
+                assert np.array_equal(got[hoff[r]:hoff[r + 1]], want[r]), (memo, r, lens[r])
+
+
 @pytest.mark.parametrize("B", [16, 32, 64, 5])
 @pytest.mark.parametrize("split_min", [1, 100, 777])
 def test_hash_batch_split_tasks(B, split_min):

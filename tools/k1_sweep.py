@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--splits", default="-1,8192,4096,0")
     ap.add_argument("--workload", default="bursty")
     ap.add_argument("--grids", default="persistent,tasks")
+    ap.add_argument("--memo", default="1")
     a = ap.parse_args()
     from paper_2604_25899_b200 import Context
     from paper_2604_25899_b200 import batch as PB
@@ -35,9 +36,11 @@ def main():
         b = S.upload_burst(tr, 16, dev, 3)
         L = np.diff(tr.tok_off)
         nbytes = 8 * int(L.sum()) + 8 * b.b.n_hashes + 16 * (R + 1)
-        for sm, grid in [(int(x), gm) for x in a.splits.split(",") for gm in a.grids.split(",")]:
+        for sm, grid, memo in [(int(x), gm, int(mm)) for x in a.splits.split(",")
+                               for gm in a.grids.split(",") for mm in a.memo.split(",")]:
             ctx = Context(0, [], [], 16, device=0)
             ctx.set_hash_grid(grid)
+            ctx.set_hash_memo(memo)
             ctx.set_stream(ctypes.c_void_p(s.cuda_stream))
             ctx.set_hash_split(sm)
             ts = []
@@ -50,7 +53,7 @@ def main():
                 if i >= 2:
                     ts.append(e0.elapsed_time(e1))
             ms = float(np.median(ts))
-            print(json.dumps({"R": R, "split_min": sm, "grid": grid, "ms": ms, "tokens": int(L.sum()),
+            print(json.dumps({"R": R, "split_min": sm, "grid": grid, "memo": memo, "ms": ms, "tokens": int(L.sum()),
                               "max_len": int(L.max()), "gbs": nbytes / ms / 1e6}), flush=True)
             ctx.close()
 
