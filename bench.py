@@ -80,13 +80,16 @@ def parse():
     ap.add_argument("--split-min", type=int, default=-1,
                     help="K1: prompts of >= this many tokens are split tasks (0 = never, "
                          "-1 = from the batch's token count)")
-    ap.add_argument("--k1-after", default="staged", choices=["start", "staged"],
+    ap.add_argument("--k1-after", default="auto", choices=["auto", "start", "staged"],
                     help="K1 of burst k+1 starts with step k (start) or once step k's K2 is "
                          "done (staged: K2 runs alone, K1 overlaps the latency-bound K3 / "
-                         "admission)")
-    ap.add_argument("--k1-grid", default="persistent", choices=["persistent", "tasks", "tasks1"],
+                         "admission); auto: start at N = 1, staged at N > 1")
+    ap.add_argument("--k1-grid", default="auto",
+                    choices=["auto", "persistent", "tasks", "tasks1"],
                     help="K1 grid: persistent CTAs, or one task per warp (CTAs retire so the "
-                         "step's kernels interleave)")
+                         "step's kernels interleave; tasks1: at most one K1 CTA per SM); "
+                         "auto: tasks1 at N = 1, persistent at N > 1 (the sharded step's "
+                         "cross-rank phases want SMs of their own)")
     ap.add_argument("--k1-memo", default="off", choices=["on", "off"],
                     help="K1 prefix memo of shared leading tokens (pyg_set_hash_memo)")
     ap.add_argument("--k1-gate", default="off", choices=["on", "off"],
@@ -96,6 +99,13 @@ def parse():
                     help="K1 of step k+1 overlaps step k on a second stream, its grid capped at "
                          "(SMs - free_sms); -1 = no overlap (serial step)")
     a = ap.parse_args()
+    # measured best per GPU count: one GPU -- K1 of the next burst from the
+    # step's start on retiring CTAs; several -- a persistent K1 after the step's K2
+    multi = a.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1
+    if a.k1_after == "auto":
+        a.k1_after = "staged" if multi else "start"
+    if a.k1_grid == "auto":
+        a.k1_grid = "persistent" if multi else "tasks1"
     for k, v in DEFAULTS[a.workload].items():
         if not getattr(a, k):
             setattr(a, k, v)
@@ -491,9 +501,9 @@ def run_ours(args):
             "l2_flush": "none needed: every step reads a distinct burst (%.2f GB of tokens) "
                         "larger than the 126 MB L2" % (arm.bursts[-1].b.n_tokens * 8 / 1e9),
             "parallelism": "one GPU holds every replica",
-            "k1_overlap": (f"K1 of burst k+1 on a second stream (grid = SMs - {args.free_sms}) "
-                           f"from step k's {'K2 end' if args.k1_after == 'staged' else 'start'}, "
-                           f"grid {args.k1_grid}"
+            "k1_overlap": (f"K1 of burst k+1 on a second stream from step k's "
+                           f"{'K2 end' if args.k1_after == 'staged' else 'start'}, "
+                           f"{k1_grid_desc(args)}"
                            f"{', paused while the admission runs' if args.k1_gate == 'on' else ''}; "
                            "the timed span holds K steps and K K1 launches (bursts k0+1 .. "
                            "k0+K; burst k0's K1 ran in the last warm-up step, as in the steady "
@@ -513,6 +523,14 @@ def run_ours(args):
         "e2e": e2e, "cpu_baseline": cpu, "cpu_baseline_hash_once": cpu_h1,
     }
     print(json.dumps(line), flush=True)
+
+
+def k1_grid_desc(args):
+    return {"persistent": f"persistent grid of SMs - {args.free_sms} CTAs",
+            "tasks": "one task per warp (CTAs retire as they finish)",
+            "tasks1": "one task per warp, at most one K1 CTA per SM (CTAs retire as they "
+                      "finish; the step's kernels take the SMs they free, higher stream "
+                      "priority)"}[args.k1_grid]
 
 
 def hash_traffic(args):
@@ -935,8 +953,9 @@ def run_sharded(args):
                                 "over NVLink peer memory (flag barrier), K3 per model on its "
                                 "owner, placed requests pulled by the owner over NVLink, L3 "
                                 "promotions chained over the ranks in engine order"),
-                "k1_overlap": (f"K1 of burst k+1 on a second stream (grid = SMs - "
-                               f"{args.free_sms}); the timed span holds K steps and K K1 "
+                "k1_overlap": (f"K1 of burst k+1 on a second stream from step k's "
+                               f"{'K2 end' if args.k1_after == 'staged' else 'start'}, "
+                               f"{k1_grid_desc(args)}; the timed span holds K steps and K K1 "
                                "launches (bursts k0+1 .. k0+K; burst k0's K1 ran in the last "
                                "warm-up step)")},
             "roofline": {"bound": "hbm", "kernel": "k_hash_staged (K1), rank 0",
