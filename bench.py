@@ -126,6 +126,10 @@ def maybe_self_launch(args):
         os.execv(sys.executable, cmd)
 
 
+# the step's stream outranks K1's (0): CTAs of its kernels are dispatched first as SMs free
+STEP_PRIORITY = int(os.environ.get("PYG_STEP_PRIORITY", "-1"))
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -336,7 +340,7 @@ class Arm:
         cl = self.cl
         self.ctx = Context(cl.n_replicas, cl.kv_capacity, cl.l2_capacity, args.block,
                            device=dev.index)
-        torch.cuda.set_stream(torch.cuda.Stream(device=dev, priority=-1))
+        torch.cuda.set_stream(torch.cuda.Stream(device=dev, priority=STEP_PRIORITY))
         self.S_stream = torch.cuda.current_stream(dev)
         from paper_2604_25899_b200 import batch as PB
         self.PB = PB
@@ -858,7 +862,7 @@ def run_sharded(args):
     per = cl.n_replicas // ws
     lo, hi = rank * per, (rank + 1) * per
     ctx = Context(per, cl.kv_capacity[lo:hi], cl.l2_capacity[lo:hi], args.block, device=local)
-    Sst = torch.cuda.Stream(device=dev, priority=-1)
+    Sst = torch.cuda.Stream(device=dev, priority=STEP_PRIORITY)
     torch.cuda.set_stream(Sst)
     PB.bind_current_stream(ctx)
     warm, ops, off, placed = warm_inputs(args, cl, dev)
