@@ -95,17 +95,22 @@ def parse():
     ap.add_argument("--k1-gate", default="off", choices=["on", "off"],
                     help="K1 of the next burst pauses while the step's admission runs "
                          "(pyg_set_hash_gate)")
-    ap.add_argument("--free-sms", type=int, default=8,
+    ap.add_argument("--free-sms", type=int, default=None,
                     help="K1 of step k+1 overlaps step k on a second stream, its grid capped at "
                          "(SMs - free_sms); -1 = no overlap (serial step)")
     a = ap.parse_args()
     # measured best per GPU count: one GPU -- K1 of the next burst from the
     # step's start on retiring CTAs; several -- a persistent K1 after the step's K2
+    # config 3 (few, long prompts): a persistent K1 spread over all but 48 SMs, from the
+    # step's start, leaves the step's kernels SMs of their own
     multi = a.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1
+    lc = a.workload == "long_context" and not multi
     if a.k1_after == "auto":
         a.k1_after = "staged" if multi else "start"
     if a.k1_grid == "auto":
-        a.k1_grid = "persistent" if multi else "tasks1"
+        a.k1_grid = "persistent" if (multi or lc) else "tasks1"
+    if a.free_sms is None:
+        a.free_sms = 48 if lc else 8
     for k, v in DEFAULTS[a.workload].items():
         if not getattr(a, k):
             setattr(a, k, v)

@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(W * 32, (W <= 8 ? 2 : 1))
 k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ tok_off,
               int R, const int32_t* __restrict__ order, const int64_t* __restrict__ hash_off,
               uint64_t* __restrict__ hashes, int B, int* __restrict__ next_task, GatherSrc g,
-              const int* __restrict__ n_split_p, const int32_t* gate, MemoTab mt) {
+              const int* __restrict__ n_split_p, const int32_t* gate, MemoTab mt, int n_sm) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbuf = smem + warp * 2 * kStageBytes;
@@ -480,11 +480,20 @@ k_hash_staged(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ t
   // persistent (next_task != null): warps pull tasks from a counter until none are left;
   // otherwise one task per warp (a CTA per 8 tasks, in the longest-first order), so CTAs
   // retire continually and a higher-priority stream's kernels get SMs between them
+  // fewer tasks than warps on the SMs (a burst of few, long one-lane chains, config 3):
+  // spread them -- at most ceil(tasks / CTAs) warps of each CTA take tasks, so each chain
+  // gets an SM scheduler (nearly) to itself instead of sharing one on a few SMs
+  const int ctas = next_task ? static_cast<int>(gridDim.x) : min(static_cast<int>(gridDim.x), n_sm);
+  const bool sparse = ntasks < ctas * W;
+  if (sparse && (warp >= (ntasks + ctas - 1) / ctas || static_cast<int>(blockIdx.x) >= ctas))
+    return;
   for (int it = 0;; ++it) {
   int task = 0;
   if (next_task) {
     if (lane == 0) task = atomicAdd(next_task, 1);
     task = __shfl_sync(kFull, task, 0);
+  } else if (sparse) {
+    task = it == 0 ? warp * ctas + static_cast<int>(blockIdx.x) : ntasks;
   } else {
     task = it == 0 ? static_cast<int>(blockIdx.x) * W + warp : ntasks;
   }
@@ -1035,14 +1044,14 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
   const int32_t* gate = c->hash_grid != 0 ? c->hash_gate : nullptr;
   if (memo) {
     k_hash_staged<false, kWarps, true><<<grid, kWarps * 32, smem_bytes(kWarps), c->stream>>>(
-        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate, mt);
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate, mt, n_sm);
     PYG_LAUNCHED(c);
     k_memo_emit<<<std::min((R + 7) / 8, 16 * n_sm), 256, 0, c->stream>>>(d_tok_off, d_hash_off,
                                                                           d_hashes, R, c->B, mt);
   } else
     k_hash_staged<kGather, kWarps, false><<<grid, kWarps * 32,
                                             std::max(pad, smem_bytes(kWarps)), c->stream>>>(
-        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate, mt);
+        d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate, mt, n_sm);
   PYG_LAUNCHED(c);
   return PYG_OK;
 }

@@ -38,6 +38,13 @@ def test_explicit_overlap_kept(monkeypatch):
     assert (a.k1_grid, a.k1_after) == ("tasks1", "start")
 
 
+def test_auto_overlap_config3(monkeypatch):
+    a = _parse(["--workload", "long_context"], monkeypatch=monkeypatch)
+    assert (a.k1_grid, a.k1_after, a.free_sms) == ("persistent", "start", 48)
+    a = _parse([], monkeypatch=monkeypatch)
+    assert a.free_sms == 8
+
+
 def test_reference_arm_and_config3(monkeypatch):
     a = _parse(["--impl", "reference", "--workload", "long_context", "--steps", "2",
                 "--warmup", "3"], monkeypatch=monkeypatch)
