@@ -1,3 +1,5 @@
+"""K1 prefix memo on a synthetic batch: 40k requests of 4,096 tokens sharing 2,048-token
+prefixes (64 distinct), memo on / off (profiles/r02_k1_prefix_memo_ab.txt)."""
 import sys, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 from paper_2604_25899_b200 import Context
