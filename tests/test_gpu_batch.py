@@ -216,6 +216,37 @@ def test_hash_batch_prefix_memo(B, split_min):
                 assert np.array_equal(got[hoff[r]:hoff[r + 1]], want[r]), (memo, r, lens[r])
 
 
+@pytest.mark.parametrize("grid", ["persistent", "tasks", "tasks1"])
+@pytest.mark.parametrize("n_long", [40, 3000])
+def test_hash_batch_grid_modes(grid, n_long):
+    """K1's grid modes (persistent, one task per warp, one CTA per SM) on a sparse batch (few
+    long one-lane chains: spread over the SMs, at most ceil(tasks / CTAs) warps per CTA) and
+    a dense one, against the oracle."""
+    from paper_2604_25899_b200 import Context
+    from paper_2604_25899_b200 import batch as PB
+    rng = np.random.default_rng(len(grid) * 31 + n_long)
+    lens = np.concatenate([rng.integers(2000, 9000, n_long), rng.integers(0, 200, 60)])
+    rng.shuffle(lens)
+    off = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    toks = rng.integers(0, 1 << 63, size=int(off[-1]), dtype=np.uint64)
+    ctx = Context(1, 1000, 1000, 16)
+    ctx.set_hash_grid(grid)
+    ctx.set_hash_split(0)  # one lane per request: the chains the spreading is for
+    z = np.zeros(len(lens), np.int32)
+    res = np.zeros(len(lens), PB.RES_DTYPE)
+    db = PB.upload_batch(ctx, toks, off, res, z, z, z)
+    PB.bind_current_stream(ctx)
+    PB.hash_batch(ctx, db)
+    torch.cuda.synchronize()
+    got = db.hashes.cpu().numpy().view(np.uint64)
+    hoff = db.hash_off.cpu().numpy()
+    o = Restated(16)
+    for r in range(len(lens)):
+        assert np.array_equal(got[hoff[r]:hoff[r + 1]], o.chain_hashes(toks[off[r]:off[r + 1]])), \
+            (grid, r, lens[r])
+
+
 @pytest.mark.parametrize("B", [16, 32, 64, 5])
 @pytest.mark.parametrize("split_min", [1, 100, 777])
 def test_hash_batch_split_tasks(B, split_min):
