@@ -1048,7 +1048,22 @@ static int hash_launch(pyg_ctx* c, const uint64_t* d_src, const int64_t* d_tok_o
     PYG_LAUNCHED(c);
     k_memo_emit<<<std::min((R + 7) / 8, 16 * n_sm), 256, 0, c->stream>>>(d_tok_off, d_hash_off,
                                                                           d_hashes, R, c->B, mt);
-  } else
+  } else {
+    // grid mode 2: the SM's shared memory at its 164 KB setting (carveout 72 %), which holds
+    // the padded K1 CTA (117 KB) and a K3 CTA (46 KB) but not an admission CTA (104 KB):
+    // measured 86 vs 84 M req/s against the driver's choice for K1 alone (132 KB), 71 with
+    // the 196 / 228 KB settings (an admission CTA then slows the K1 beside it).  The
+    // attribute is per function: set when the mode changes (the gate sets its own).
+    static int carve_set[64] = {};  // per device: 0 unset, else carveout + 1
+    const int want = c->hash_grid == 2 ? 72 : -1;  // -1: the driver's default
+    const int dev = c->device >= 0 && c->device < 64 ? c->device : 0;
+    if (!c->hash_gate && carve_set[dev] != want + 1) {
+      PYG_CUDA(cudaFuncSetAttribute(k_hash_staged<kGather, kWarps, false>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, want));
+      carve_set[dev] = want + 1;
+    }
+  }
+  if (!memo)
     k_hash_staged<kGather, kWarps, false><<<grid, kWarps * 32,
                                             std::max(pad, smem_bytes(kWarps)), c->stream>>>(
         d_src, d_tok_off, R, v_out, d_hash_off, d_hashes, c->B, next, g, ctr0 + 1, gate, mt, n_sm);
