@@ -88,8 +88,7 @@ def parse():
                     choices=["auto", "persistent", "tasks", "tasks1"],
                     help="K1 grid: persistent CTAs, or one task per warp (CTAs retire so the "
                          "step's kernels interleave; tasks1: at most one K1 CTA per SM); "
-                         "auto: tasks1 at N = 1, persistent at N > 1 (the sharded step's "
-                         "cross-rank phases want SMs of their own)")
+                         "auto: tasks1 (persistent for config 3)")
     ap.add_argument("--k1-memo", default="off", choices=["on", "off"],
                     help="K1 prefix memo of shared leading tokens (pyg_set_hash_memo)")
     ap.add_argument("--k1-gate", default="off", choices=["on", "off"],
@@ -99,8 +98,9 @@ def parse():
                     help="K1 of step k+1 overlaps step k on a second stream, its grid capped at "
                          "(SMs - free_sms); -1 = no overlap (serial step)")
     a = ap.parse_args()
-    # measured best per GPU count: one GPU -- K1 of the next burst from the
-    # step's start on retiring CTAs; several -- a persistent K1 after the step's K2
+    # measured best per GPU count: K1 of the next burst on retiring CTAs, one
+    # per SM -- from the step's start on one GPU, after the step's K2 on several (the sharded
+    # step's cross-rank phases suffer most beside K1)
     # config 3 (few, long prompts): a persistent K1 spread over all but 48 SMs, from the
     # step's start, leaves the step's kernels SMs of their own
     multi = a.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1
@@ -108,7 +108,7 @@ def parse():
     if a.k1_after == "auto":
         a.k1_after = "staged" if multi else "start"
     if a.k1_grid == "auto":
-        a.k1_grid = "persistent" if (multi or lc) else "tasks1"
+        a.k1_grid = "persistent" if lc else "tasks1"
     if a.free_sms is None:
         a.free_sms = 48 if lc else 8
     for k, v in DEFAULTS[a.workload].items():

@@ -29,7 +29,7 @@ def test_auto_overlap_one_gpu(monkeypatch):
                                         ([], "8")])
 def test_auto_overlap_several_gpus(argv, world, monkeypatch):
     a = _parse(argv, world, monkeypatch)
-    assert (a.k1_grid, a.k1_after) == ("persistent", "staged")
+    assert (a.k1_grid, a.k1_after) == ("tasks1", "staged")
 
 
 def test_explicit_overlap_kept(monkeypatch):
